@@ -1,0 +1,1199 @@
+// homfe_oracle.cpp -- TEST INFRASTRUCTURE ONLY (see homfe_oracle.h).
+//
+// CPU restatement of the reference `homfe` PCG hot path, written from the
+// reference's behaviour, not copied. Loop orders follow the reference so that
+// rounding matches it as closely as a different FFT / dense-LA backend allows:
+//   grid tables           proj/src/grid.cpp:114-145 (TwoTriangles), 81-112
+//                         (BilinearQuad), 147-188 (FourTrianglesTwoNode),
+//                         190-229 (TrilinearHex), 267-288 (strides / wrap)
+//   operators             proj/src/operators.cpp:11-265
+//   fields / reductions   proj/src/fields.cpp:5-61
+//   Mandel stiffness      proj/src/mandel.cpp:105-134
+//   FFT conventions       proj/src/fft.cpp:23-79 (FFTW replaced, see below)
+//   preconditioner        proj/src/precond.cpp:13-162
+//   PCG / Newton          proj/src/solver.cpp:50-296
+// Third-party replacements (the reference links Eigen >= 3.3 and FFTW3,
+// proj/CMakeLists.txt:18-24, neither present in this image):
+//   * FFTW3 r2c/c2r (FFTW_ESTIMATE) -> own mixed-radix c2c FFT, unnormalised,
+//     half spectrum N_last/2+1 on the last axis, c2r via Hermitian extension.
+//   * Eigen LLT / PartialPivLU inverse / SelfAdjointEigenSolver -> own
+//     Cholesky, Gauss-Jordan and cyclic Jacobi on the real 2n x 2n embedding
+//     of the Hermitian block.
+// Both replacements agree with the originals up to rounding only.
+
+#include "homfe_oracle.h"
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace {
+
+using Index = int64_t;
+using cplx = std::complex<double>;
+
+struct ValidationError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct NumericalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NonConvergence : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ValidationError& e) {
+    g_last_error = e.what();
+    return 2;
+  } catch (const NumericalError& e) {
+    g_last_error = e.what();
+    return 4;
+  } catch (const NonConvergence& e) {
+    g_last_error = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return 4;
+  }
+}
+
+// ----------------------------------------------------------------- layout
+
+struct Entry {
+  int off;
+  int node;
+  double dphi[3];
+};
+struct QuadSpec {
+  double w;
+  std::vector<Entry> entries;
+};
+
+struct Layout {
+  int d = 0;
+  Index N[3] = {1, 1, 1};
+  double L[3] = {1, 1, 1};
+  int kind = 0;
+  int Nn = 1;
+  Index np = 0;
+  Index strides[3] = {0, 0, 0};
+  std::vector<std::array<Index, 3>> offsets;
+  std::vector<QuadSpec> quads;
+
+  int nq() const { return static_cast<int>(quads.size()); }
+  Index num_nodes() const { return np * Nn; }
+  Index num_quads() const { return np * nq(); }
+  double h(int a) const { return L[a] / static_cast<double>(N[a]); }
+  double pixel_volume() const {
+    double v = 1.0;
+    for (int a = 0; a < d; ++a) v *= h(a);
+    return v;
+  }
+  double cell_volume() const {
+    double v = 1.0;
+    for (int a = 0; a < d; ++a) v *= L[a];
+    return v;
+  }
+};
+
+int mandel_dim(int d) { return d * (d + 1) / 2; }
+int grad_components(int d, int c) { return c == 1 ? d : mandel_dim(d); }
+
+const std::vector<std::array<Index, 3>> kQuadOff{
+    {0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {1, 1, 0}};
+const std::vector<std::array<Index, 3>> kHexOff{
+    {0, 0, 0}, {0, 0, 1}, {0, 1, 0}, {0, 1, 1},
+    {1, 0, 0}, {1, 0, 1}, {1, 1, 0}, {1, 1, 1}};
+
+Layout make_layout(const or_grid* g) {
+  if (!g) throw ValidationError("grid: null descriptor");
+  Layout l;
+  l.d = g->dim;
+  if (l.d != 2 && l.d != 3) {
+    throw ValidationError("cell: dimension must be 2 or 3, got " +
+                          std::to_string(l.d));
+  }
+  for (int a = 0; a < l.d; ++a) {
+    l.N[a] = g->dims[a];
+    l.L[a] = g->lengths[a];
+    if (l.N[a] < 2) {
+      throw ValidationError("cell.dims[" + std::to_string(a) +
+                            "]: must be >= 2, got " + std::to_string(l.N[a]));
+    }
+    if (!(l.L[a] > 0.0)) {
+      throw ValidationError("cell.lengths[" + std::to_string(a) + "]: must be > 0");
+    }
+  }
+  l.kind = g->stencil;
+  if (l.kind < 0 || l.kind > 3) throw ValidationError("stencil: invalid kind");
+  const int want = l.kind == OR_TRILINEAR_HEX ? 3 : 2;
+  if (l.d != want) {
+    throw ValidationError("stencil: requires a " + std::to_string(want) +
+                          "d cell, got " + std::to_string(l.d) + "d");
+  }
+  l.np = 1;
+  for (int a = 0; a < l.d; ++a) l.np *= l.N[a];
+  Index stride = 1;
+  for (int a = l.d - 1; a >= 0; --a) {
+    l.strides[a] = stride;
+    stride *= l.N[a];
+  }
+  const double vp = l.pixel_volume();
+  if (l.kind == OR_TWO_TRIANGLES) {
+    const double h0 = l.h(0), h1 = l.h(1);
+    l.offsets = kQuadOff;
+    l.quads.push_back({vp / 2.0,
+                       {{0, 0, {-1.0 / h0, -1.0 / h1, 0.0}},
+                        {1, 0, {1.0 / h0, 0.0, 0.0}},
+                        {2, 0, {0.0, 1.0 / h1, 0.0}}}});
+    l.quads.push_back({vp / 2.0,
+                       {{3, 0, {1.0 / h0, 1.0 / h1, 0.0}},
+                        {2, 0, {-1.0 / h0, 0.0, 0.0}},
+                        {1, 0, {0.0, -1.0 / h1, 0.0}}}});
+  } else if (l.kind == OR_BILINEAR_QUAD) {
+    const double h0 = l.h(0), h1 = l.h(1);
+    l.offsets = kQuadOff;
+    const double gq = 0.5 / std::sqrt(3.0);
+    const double gp[2] = {0.5 - gq, 0.5 + gq};
+    for (int i = 0; i < 2; ++i) {
+      for (int j = 0; j < 2; ++j) {
+        QuadSpec q;
+        q.w = vp / 4.0;
+        const double x = gp[i], y = gp[j];
+        const double xi[2] = {1.0 - x, x}, dxi[2] = {-1.0 / h0, 1.0 / h0};
+        const double et[2] = {1.0 - y, y}, det[2] = {-1.0 / h1, 1.0 / h1};
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b)
+            q.entries.push_back({a + 2 * b, 0, {dxi[a] * et[b], xi[a] * det[b], 0.0}});
+        l.quads.push_back(q);
+      }
+    }
+  } else if (l.kind == OR_FOUR_TRIANGLES_TWO_NODE) {
+    const double h0 = l.h(0), h1 = l.h(1);
+    l.offsets = kQuadOff;
+    l.Nn = 2;
+    auto tri = [&](Entry a, Entry b, Entry c) { l.quads.push_back({vp / 4.0, {a, b, c}}); };
+    tri({0, 0, {-1.0 / h0, -1.0 / h1, 0.0}}, {1, 0, {1.0 / h0, -1.0 / h1, 0.0}},
+        {0, 1, {0.0, 2.0 / h1, 0.0}});
+    tri({1, 0, {1.0 / h0, -1.0 / h1, 0.0}}, {3, 0, {1.0 / h0, 1.0 / h1, 0.0}},
+        {0, 1, {-2.0 / h0, 0.0, 0.0}});
+    tri({3, 0, {1.0 / h0, 1.0 / h1, 0.0}}, {2, 0, {-1.0 / h0, 1.0 / h1, 0.0}},
+        {0, 1, {0.0, -2.0 / h1, 0.0}});
+    tri({2, 0, {-1.0 / h0, 1.0 / h1, 0.0}}, {0, 0, {-1.0 / h0, -1.0 / h1, 0.0}},
+        {0, 1, {2.0 / h0, 0.0, 0.0}});
+  } else {  // trilinear hex
+    const double h0 = l.h(0), h1 = l.h(1), h2 = l.h(2);
+    l.offsets = kHexOff;
+    const double gq = 0.5 / std::sqrt(3.0);
+    const double gp[2] = {0.5 - gq, 0.5 + gq};
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j)
+        for (int k = 0; k < 2; ++k) {
+          QuadSpec q;
+          q.w = vp / 8.0;
+          const double x = gp[i], y = gp[j], z = gp[k];
+          const double xi[2] = {1.0 - x, x}, dxi[2] = {-1.0 / h0, 1.0 / h0};
+          const double et[2] = {1.0 - y, y}, det[2] = {-1.0 / h1, 1.0 / h1};
+          const double ze[2] = {1.0 - z, z}, dze[2] = {-1.0 / h2, 1.0 / h2};
+          for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b)
+              for (int c = 0; c < 2; ++c)
+                q.entries.push_back({(a * 2 + b) * 2 + c, 0,
+                                     {dxi[a] * et[b] * ze[c], xi[a] * det[b] * ze[c],
+                                      xi[a] * et[b] * dze[c]}});
+          l.quads.push_back(q);
+        }
+  }
+  return l;
+}
+
+// Neighbour pixels of the current pixel for every stencil offset, with the
+// "+1 wraps to 0" rule of the reference walker (operators.cpp:65-84).
+struct Walker {
+  const Layout& l;
+  Index coords[3] = {0, 0, 0};
+  Index nbr[8];
+  explicit Walker(const Layout& lay) : l(lay) {}
+  void neighbors() {
+    Index cur[3] = {0, 0, 0}, nxt[3] = {0, 0, 0};
+    for (int a = 0; a < l.d; ++a) {
+      cur[a] = coords[a] * l.strides[a];
+      const Index up = coords[a] + 1 == l.N[a] ? 0 : coords[a] + 1;
+      nxt[a] = up * l.strides[a];
+    }
+    for (size_t o = 0; o < l.offsets.size(); ++o) {
+      Index f = 0;
+      for (int a = 0; a < l.d; ++a) f += l.offsets[o][a] ? nxt[a] : cur[a];
+      nbr[o] = f;
+    }
+  }
+  void advance() {
+    for (int a = l.d - 1; a >= 0; --a) {
+      if (++coords[a] < l.N[a]) return;
+      coords[a] = 0;
+    }
+  }
+};
+
+const double kHalfSqrt2 = std::sqrt(2.0) / 2.0;
+
+// Mandel gradient rows of one node contribution (operators.cpp:16-32).
+inline void add_rows(int d, int c, const double* dp, const double* uv, double* g) {
+  if (c == 1) {
+    for (int a = 0; a < d; ++a) g[a] += dp[a] * uv[0];
+  } else if (d == 2) {
+    g[0] += dp[0] * uv[0];
+    g[1] += dp[1] * uv[1];
+    g[2] += kHalfSqrt2 * (dp[1] * uv[0] + dp[0] * uv[1]);
+  } else {
+    g[0] += dp[0] * uv[0];
+    g[1] += dp[1] * uv[1];
+    g[2] += dp[2] * uv[2];
+    g[3] += kHalfSqrt2 * (dp[2] * uv[1] + dp[1] * uv[2]);
+    g[4] += kHalfSqrt2 * (dp[2] * uv[0] + dp[0] * uv[2]);
+    g[5] += kHalfSqrt2 * (dp[1] * uv[0] + dp[0] * uv[1]);
+  }
+}
+
+// Weighted adjoint of add_rows (operators.cpp:36-53).
+inline void adj_rows(int d, int c, const double* dp, const double* s, double w,
+                     double* out) {
+  if (c == 1) {
+    double acc = 0.0;
+    for (int a = 0; a < d; ++a) acc += dp[a] * s[a];
+    out[0] += w * acc;
+  } else if (d == 2) {
+    out[0] += w * (dp[0] * s[0] + kHalfSqrt2 * dp[1] * s[2]);
+    out[1] += w * (dp[1] * s[1] + kHalfSqrt2 * dp[0] * s[2]);
+  } else {
+    out[0] += w * (dp[0] * s[0] + kHalfSqrt2 * (dp[2] * s[4] + dp[1] * s[5]));
+    out[1] += w * (dp[1] * s[1] + kHalfSqrt2 * (dp[2] * s[3] + dp[0] * s[5]));
+    out[2] += w * (dp[2] * s[2] + kHalfSqrt2 * (dp[1] * s[3] + dp[0] * s[4]));
+  }
+}
+
+void check_c(const Layout& l, int c) {
+  if (c != 1 && c != l.d) throw ValidationError("nodal field shape does not match layout");
+}
+
+void gradient(const Layout& l, int c, const double* u, double* out) {
+  check_c(l, c);
+  const int m = grad_components(l.d, c), nq = l.nq();
+  const Index nn = l.num_nodes();
+  std::fill(out, out + l.num_quads() * m, 0.0);
+  Walker w(l);
+  for (Index p = 0; p < l.np; ++p) {
+    w.neighbors();
+    for (int lq = 0; lq < nq; ++lq) {
+      double* g = out + (p * nq + lq) * m;
+      for (const Entry& e : l.quads[lq].entries) {
+        const Index node = static_cast<Index>(e.node) * l.np + w.nbr[e.off];
+        double uv[3];
+        for (int k = 0; k < c; ++k) uv[k] = u[k * nn + node];
+        add_rows(l.d, c, e.dphi, uv, g);
+      }
+    }
+    w.advance();
+  }
+}
+
+void divergence(const Layout& l, int c, const double* s, bool weighted, double* out) {
+  check_c(l, c);
+  const int m = grad_components(l.d, c), nq = l.nq();
+  const Index nn = l.num_nodes();
+  std::fill(out, out + c * nn, 0.0);
+  Walker w(l);
+  for (Index p = 0; p < l.np; ++p) {
+    w.neighbors();
+    for (int lq = 0; lq < nq; ++lq) {
+      const QuadSpec& q = l.quads[lq];
+      const double wt = weighted ? q.w : 1.0;
+      const double* sv = s + (p * nq + lq) * m;
+      for (const Entry& e : q.entries) {
+        const Index node = static_cast<Index>(e.node) * l.np + w.nbr[e.off];
+        double acc[3] = {0.0, 0.0, 0.0};
+        adj_rows(l.d, c, e.dphi, sv, wt, acc);
+        for (int k = 0; k < c; ++k) out[k * nn + node] += acc[k];
+      }
+    }
+    w.advance();
+  }
+}
+
+// Fused gather -> m x m col-major multiply -> weighted scatter
+// (operators.cpp:197-243). TangentAt(q) returns the block of quad q.
+template <class TangentAt>
+void fused(const Layout& l, int c, const double* u, bool weighted, TangentAt&& tan_at,
+           double* out) {
+  check_c(l, c);
+  const int m = grad_components(l.d, c), nq = l.nq();
+  const Index nn = l.num_nodes();
+  std::fill(out, out + c * nn, 0.0);
+  Walker w(l);
+  double g[6], t[6];
+  for (Index p = 0; p < l.np; ++p) {
+    w.neighbors();
+    for (int lq = 0; lq < nq; ++lq) {
+      const QuadSpec& q = l.quads[lq];
+      for (int k = 0; k < m; ++k) g[k] = 0.0;
+      for (const Entry& e : q.entries) {
+        const Index node = static_cast<Index>(e.node) * l.np + w.nbr[e.off];
+        double uv[3];
+        for (int k = 0; k < c; ++k) uv[k] = u[k * nn + node];
+        add_rows(l.d, c, e.dphi, uv, g);
+      }
+      const double* cm = tan_at(p * nq + lq);
+      for (int i = 0; i < m; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < m; ++j) acc += cm[j * m + i] * g[j];
+        t[i] = acc;
+      }
+      const double wt = weighted ? q.w : 1.0;
+      for (const Entry& e : q.entries) {
+        const Index node = static_cast<Index>(e.node) * l.np + w.nbr[e.off];
+        double acc[3] = {0.0, 0.0, 0.0};
+        adj_rows(l.d, c, e.dphi, t, wt, acc);
+        for (int k = 0; k < c; ++k) out[k * nn + node] += acc[k];
+      }
+    }
+    w.advance();
+  }
+}
+
+void apply_phase(const Layout& l, int c, int n_phases, const double* cmat,
+                 const uint8_t* phase, const double* u, bool weighted, double* out) {
+  const int m = grad_components(l.d, c), nq = l.nq();
+  for (Index p = 0; p < l.np; ++p) {
+    if (phase[p] >= n_phases) throw ValidationError("materials: phase id missing from catalog");
+  }
+  fused(l, c, u, weighted,
+        [&](Index q) { return cmat + static_cast<Index>(phase[q / nq]) * m * m; }, out);
+}
+
+void apply_reference(const Layout& l, int c, const double* c_ref, const double* u,
+                     bool weighted, double* out) {
+  fused(l, c, u, weighted, [&](Index) { return c_ref; }, out);
+}
+
+// ----------------------------------------------------------------- mandel
+
+void isotropic_stiffness(double K, double G, int d, double* out) {
+  if (d != 2 && d != 3) throw ValidationError("mandel: dimension must be 2 or 3");
+  if (!(K > 0.0) || !(G > 0.0)) {
+    throw ValidationError("isotropic_stiffness: moduli must be positive");
+  }
+  double c3[36];
+  const double tk = 3.0 * K, tg = 2.0 * G;
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) {
+      const double mi = i < 3 ? 1.0 : 0.0, mj = j < 3 ? 1.0 : 0.0;
+      const double pv = mi * mj / 3.0;
+      const double pd = (i == j ? 1.0 : 0.0) - pv;
+      c3[j * 6 + i] = tk * pv + tg * pd;
+    }
+  if (d == 3) {
+    std::memcpy(out, c3, sizeof(c3));
+    return;
+  }
+  const int idx[3] = {0, 1, 5};
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) out[b * 3 + a] = c3[idx[b] * 6 + idx[a]];
+}
+
+// Symmetric + Cholesky check (material.cpp:13-29, precond.cpp:13-24).
+void check_spd(const double* a, int n, const char* what) {
+  double scale = 0.0, asym = 0.0;
+  for (int i = 0; i < n * n; ++i) scale = std::max(scale, std::abs(a[i]));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) asym = std::max(asym, std::abs(a[j * n + i] - a[i * n + j]));
+  if (asym > 1e-10 * scale) throw ValidationError(std::string(what) + " must be symmetric");
+  std::vector<double> lmat(n * n, 0.0);
+  for (int j = 0; j < n; ++j) {
+    double dsum = a[j * n + j];
+    for (int k = 0; k < j; ++k) dsum -= lmat[k * n + j] * lmat[k * n + j];
+    if (!(dsum > 0.0)) throw ValidationError(std::string(what) + " must be positive definite");
+    const double ljj = std::sqrt(dsum);
+    lmat[j * n + j] = ljj;
+    for (int i = j + 1; i < n; ++i) {
+      double s = a[j * n + i];
+      for (int k = 0; k < j; ++k) s -= lmat[k * n + i] * lmat[k * n + j];
+      lmat[j * n + i] = s / ljj;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- FFT
+
+// One 1D complex transform of length n, mixed radix, decimation in time.
+struct Fft1d {
+  Index n = 0;
+  std::vector<int> factors;  // radices in use order
+  std::vector<cplx> tw;      // tw[k] = exp(-2 pi i k / n)
+  explicit Fft1d(Index n_) : n(n_) {
+    Index r = n;
+    while (r % 4 == 0) { factors.push_back(4); r /= 4; }
+    while (r % 2 == 0) { factors.push_back(2); r /= 2; }
+    for (Index p = 3; r > 1;) {
+      if (r % p == 0) { factors.push_back(static_cast<int>(p)); r /= p; }
+      else { p += 2; if (p * p > r) p = r; }
+    }
+    if (factors.empty()) factors.push_back(1);
+    tw.resize(n);
+    for (Index k = 0; k < n; ++k) {
+      const double ang = -2.0 * M_PI * static_cast<double>(k) / static_cast<double>(n);
+      tw[k] = cplx(std::cos(ang), std::sin(ang));
+    }
+  }
+
+  // out[0..L) = DFT_L of in[0], in[s], ..., with L*fstride == n.
+  void work(cplx* out, const cplx* in, Index fstride, size_t fi, bool inv) const {
+    const int p = factors[fi];
+    const Index L = n / fstride;
+    const Index m = L / p;
+    if (m == 1) {
+      for (int j = 0; j < p; ++j) out[j] = in[j * fstride];
+    } else {
+      for (int j = 0; j < p; ++j) work(out + j * m, in + j * fstride, fstride * p, fi + 1, inv);
+    }
+    auto W = [&](Index k) { const cplx t = tw[k % n]; return inv ? std::conj(t) : t; };
+    if (p == 1) return;
+    if (p == 2) {
+      for (Index k = 0; k < m; ++k) {
+        const cplx a = out[k], b = out[k + m] * W(k * fstride);
+        out[k] = a + b;
+        out[k + m] = a - b;
+      }
+      return;
+    }
+    if (p == 4) {
+      const cplx mi = inv ? cplx(0, 1) : cplx(0, -1);  // W_4^1
+      for (Index k = 0; k < m; ++k) {
+        const cplx a0 = out[k];
+        const cplx a1 = out[k + m] * W(k * fstride);
+        const cplx a2 = out[k + 2 * m] * W(2 * k * fstride);
+        const cplx a3 = out[k + 3 * m] * W(3 * k * fstride);
+        const cplx s02 = a0 + a2, d02 = a0 - a2, s13 = a1 + a3, d13 = (a1 - a3) * mi;
+        out[k] = s02 + s13;
+        out[k + m] = d02 + d13;
+        out[k + 2 * m] = s02 - s13;
+        out[k + 3 * m] = d02 - d13;
+      }
+      return;
+    }
+    std::vector<cplx> sc(p);
+    for (Index k = 0; k < m; ++k) {
+      for (int q = 0; q < p; ++q) sc[q] = out[k + q * m] * W(q * k * fstride);
+      for (int q2 = 0; q2 < p; ++q2) {
+        cplx acc = 0.0;
+        for (int q = 0; q < p; ++q) acc += sc[q] * W(static_cast<Index>(q) * q2 * m * fstride);
+        out[k + q2 * m] = acc;
+      }
+    }
+  }
+  void exec(const cplx* in, cplx* out, bool inv) const { work(out, in, 1, 0, inv); }
+};
+
+struct FftGrid {
+  int rank;
+  std::vector<Index> dims, spec;
+  Index real_size = 1, spec_size = 1;
+  std::vector<Fft1d> plans;
+  explicit FftGrid(const std::vector<Index>& d) : rank(static_cast<int>(d.size())), dims(d) {
+    if (rank != 2 && rank != 3) throw ValidationError("fft: rank must be 2 or 3");
+    spec = dims;
+    spec.back() = dims.back() / 2 + 1;
+    for (int a = 0; a < rank; ++a) {
+      real_size *= dims[a];
+      spec_size *= spec[a];
+      plans.emplace_back(dims[a]);
+    }
+  }
+  // In-place c2c over every axis of a full row-major complex array.
+  void c2c(std::vector<cplx>& a, bool inv) const {
+    std::vector<cplx> line, res;
+    for (int ax = 0; ax < rank; ++ax) {
+      const Index n = dims[ax];
+      Index stride = 1;
+      for (int b = ax + 1; b < rank; ++b) stride *= dims[b];
+      const Index outer = real_size / (n * stride);
+      line.resize(n);
+      res.resize(n);
+      for (Index o = 0; o < outer; ++o)
+        for (Index s = 0; s < stride; ++s) {
+          cplx* base = a.data() + o * n * stride + s;
+          for (Index i = 0; i < n; ++i) line[i] = base[i * stride];
+          plans[ax].exec(line.data(), res.data(), inv);
+          for (Index i = 0; i < n; ++i) base[i * stride] = res[i];
+        }
+    }
+  }
+  void forward(const double* in, cplx* out) const {
+    std::vector<cplx> a(real_size);
+    for (Index i = 0; i < real_size; ++i) a[i] = cplx(in[i], 0.0);
+    c2c(a, false);
+    const Index nl = dims.back(), sl = spec.back();
+    const Index rows = real_size / nl;
+    for (Index r = 0; r < rows; ++r)
+      for (Index k = 0; k < sl; ++k) out[r * sl + k] = a[r * nl + k];
+  }
+  void inverse(const cplx* in, double* out) const {
+    std::vector<cplx> a(real_size);
+    const Index nl = dims.back(), sl = spec.back();
+    Index idx[3] = {0, 0, 0};
+    for (Index f = 0; f < real_size; ++f) {
+      Index t = f;
+      for (int ax = rank - 1; ax >= 0; --ax) { idx[ax] = t % dims[ax]; t /= dims[ax]; }
+      if (idx[rank - 1] < sl) {
+        Index h = 0;
+        for (int ax = 0; ax < rank; ++ax) h = h * spec[ax] + idx[ax];
+        a[f] = in[h];
+      } else {
+        Index h = 0;
+        for (int ax = 0; ax < rank; ++ax) {
+          const Index mirror = ax == rank - 1 ? nl - idx[ax] : (dims[ax] - idx[ax]) % dims[ax];
+          h = h * spec[ax] + mirror;
+        }
+        a[f] = std::conj(in[h]);
+      }
+    }
+    c2c(a, true);
+    for (Index i = 0; i < real_size; ++i) out[i] = a[i].real();
+  }
+  std::array<Index, 3> frequency(Index k) const {
+    std::array<Index, 3> f{0, 0, 0};
+    for (int a = rank - 1; a >= 0; --a) { f[a] = k % spec[a]; k /= spec[a]; }
+    return f;
+  }
+};
+
+// --------------------------------------------------- small dense (complex) LA
+
+// Real symmetric cyclic Jacobi: a (n x n col-major) -> eigenvalues lam, vectors v.
+void jacobi_sym(std::vector<double> a, int n, std::vector<double>& lam, std::vector<double>& v) {
+  v.assign(n * n, 0.0);
+  for (int i = 0; i < n; ++i) v[i * n + i] = 1.0;
+  auto A = [&](int i, int j) -> double& { return a[j * n + i]; };
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int i = 0; i < n; ++i) {
+      diag += A(i, i) * A(i, i);
+      for (int j = 0; j < n; ++j) if (i != j) off += A(i, j) * A(i, j);
+    }
+    if (off <= 1e-34 * diag || off == 0.0) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = A(p, q);
+        if (apq == 0.0) continue;
+        const double theta = (A(q, q) - A(p, p)) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
+        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < n; ++k) {
+          const double akp = A(k, p), akq = A(k, q);
+          A(k, p) = cs * akp - sn * akq;
+          A(k, q) = sn * akp + cs * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double apk = A(p, k), aqk = A(q, k);
+          A(p, k) = cs * apk - sn * aqk;
+          A(q, k) = sn * apk + cs * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = v[p * n + k], vkq = v[q * n + k];
+          v[p * n + k] = cs * vkp - sn * vkq;
+          v[q * n + k] = sn * vkp + cs * vkq;
+        }
+      }
+  }
+  lam.resize(n);
+  for (int i = 0; i < n; ++i) lam[i] = A(i, i);
+}
+
+// Real 2n x 2n embedding [[Re, -Im], [Im, Re]] of a Hermitian block (col-major).
+std::vector<double> embed(const cplx* b, int n) {
+  const int N2 = 2 * n;
+  std::vector<double> r(N2 * N2);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) {
+      const cplx z = b[j * n + i];
+      r[j * N2 + i] = z.real();
+      r[(j + n) * N2 + (i + n)] = z.real();
+      r[j * N2 + (i + n)] = z.imag();
+      r[(j + n) * N2 + i] = -z.imag();
+    }
+  return r;
+}
+
+// Complex inverse by Gauss-Jordan with partial pivoting (Eigen PartialPivLU role).
+void inverse_gj(const cplx* b, int n, cplx* out) {
+  std::vector<cplx> a(b, b + n * n), inv(n * n, 0.0);
+  for (int i = 0; i < n; ++i) inv[i * n + i] = 1.0;
+  auto A = [&](int i, int j) -> cplx& { return a[j * n + i]; };
+  auto I = [&](int i, int j) -> cplx& { return inv[j * n + i]; };
+  for (int col = 0; col < n; ++col) {
+    int piv = col;
+    for (int i = col + 1; i < n; ++i) if (std::abs(A(i, col)) > std::abs(A(piv, col))) piv = i;
+    if (A(piv, col) == 0.0) throw NumericalError("inverse: singular matrix");
+    if (piv != col)
+      for (int j = 0; j < n; ++j) { std::swap(A(col, j), A(piv, j)); std::swap(I(col, j), I(piv, j)); }
+    const cplx d = A(col, col);
+    for (int j = 0; j < n; ++j) { A(col, j) /= d; I(col, j) /= d; }
+    for (int i = 0; i < n; ++i) {
+      if (i == col) continue;
+      const cplx f = A(i, col);
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) { A(i, j) -= f * A(col, j); I(i, j) -= f * I(col, j); }
+    }
+  }
+  std::copy(inv.begin(), inv.end(), out);
+}
+
+// ----------------------------------------------------------------- precond
+
+}  // namespace
+
+struct or_precond {
+  int bdim = 0, c = 0, Nn = 1;
+  Index nf = 0;
+  bool weighted = true, inverted = false;
+  std::vector<cplx> data;  // nf blocks, each bdim x bdim col-major
+  int op_apps = 0, fwd = 0;
+  std::shared_ptr<FftGrid> fft;
+  cplx* block(Index k) { return data.data() + k * bdim * bdim; }
+  const cplx* block(Index k) const { return data.data() + k * bdim * bdim; }
+};
+
+namespace {
+
+// Impulse probing (precond.cpp:44-85).
+or_precond* assemble(const Layout& l, const double* c_ref, int c, bool weighted) {
+  if (c != 1 && c != l.d) throw ValidationError("assemble_reference: bad component count");
+  const int m = grad_components(l.d, c);
+  check_spd(c_ref, m, "reference tangent");
+  auto* out = new or_precond();
+  out->c = c;
+  out->Nn = l.Nn;
+  out->bdim = c * l.Nn;
+  out->weighted = weighted;
+  std::vector<Index> dims(l.N, l.N + l.d);
+  out->fft = std::make_shared<FftGrid>(dims);
+  out->nf = out->fft->spec_size;
+  out->data.assign(out->nf * out->bdim * out->bdim, 0.0);
+  const Index np = l.np, nn = l.num_nodes();
+  const int bdim = out->bdim;
+  std::vector<cplx> spec(out->nf);
+  std::vector<double> impulse(c * nn), resp(c * nn);
+  for (int col = 0; col < bdim; ++col) {
+    std::fill(impulse.begin(), impulse.end(), 0.0);
+    impulse[static_cast<Index>(col) * np] = 1.0;
+    apply_reference(l, c, c_ref, impulse.data(), weighted, resp.data());
+    out->op_apps += 1;
+    for (int row = 0; row < bdim; ++row) {
+      out->fft->forward(resp.data() + static_cast<Index>(row) * np, spec.data());
+      out->fwd += 1;
+      for (Index k = 0; k < out->nf; ++k) out->block(k)[col * bdim + row] = spec[k];
+    }
+  }
+  return out;
+}
+
+// Zero frequency: (B0 + V V^T)^-1 - V V^T; others: V diag(1/lambda) V^H with
+// the 1e-12 singularity test (precond.cpp:87-124).
+void invert(or_precond* b) {
+  if (b->inverted) throw ValidationError("invert_blocks: blocks are already inverted");
+  const int n = b->bdim;
+  {
+    std::vector<cplx> vvt(n * n, 0.0), tmp(n * n);
+    const double scale = 1.0 / std::sqrt(static_cast<double>(b->Nn));
+    // V(c*Nn + node, c) = scale; (V V^T)(i, j) = scale^2 if same component.
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        if (i / b->Nn == j / b->Nn) vvt[j * n + i] = scale * scale;
+    cplx* b0 = b->block(0);
+    for (int i = 0; i < n * n; ++i) tmp[i] = b0[i] + vvt[i];
+    inverse_gj(tmp.data(), n, b0);
+    for (int i = 0; i < n * n; ++i) b0[i] -= vvt[i];
+  }
+  std::vector<double> lam, v;
+  for (Index k = 1; k < b->nf; ++k) {
+    cplx* blk = b->block(k);
+    jacobi_sym(embed(blk, n), 2 * n, lam, v);
+    double lmax = 0.0, lmin = std::numeric_limits<double>::infinity();
+    for (double x : lam) { lmax = std::max(lmax, std::abs(x)); lmin = std::min(lmin, x); }
+    if (lmin <= 1e-12 * lmax) {
+      const auto f = b->fft->frequency(k);
+      throw NumericalError("invert_blocks: singular non-zero-frequency block at (" +
+                           std::to_string(f[0]) + "," + std::to_string(f[1]) + "," +
+                           std::to_string(f[2]) + ")");
+    }
+    // Real inverse of the embedding, then read back Re / Im blocks.
+    const int N2 = 2 * n;
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        double re = 0.0, im = 0.0;
+        for (int e = 0; e < N2; ++e) {
+          re += v[e * N2 + i] * v[e * N2 + j] / lam[e];
+          im += v[e * N2 + (i + n)] * v[e * N2 + j] / lam[e];
+        }
+        blk[j * n + i] = cplx(re, im);
+      }
+  }
+  b->inverted = true;
+}
+
+// M^-1 r (precond.cpp:126-162).
+void precond_apply(const Layout& l, const or_precond* b, const double* r, double* out) {
+  if (!b->inverted) throw ValidationError("apply_preconditioner: blocks are not inverted");
+  const int bdim = b->bdim;
+  const Index np = l.np, nf = b->nf;
+  std::vector<cplx> spectra(nf * bdim);  // column s at s*nf
+  for (int s = 0; s < bdim; ++s) b->fft->forward(r + static_cast<Index>(s) * np, spectra.data() + s * nf);
+  std::vector<cplx> rhs(bdim), sol(bdim);
+  for (Index k = 0; k < nf; ++k) {
+    for (int s = 0; s < bdim; ++s) rhs[s] = spectra[s * nf + k];
+    const cplx* blk = b->block(k);
+    for (int i = 0; i < bdim; ++i) {
+      cplx acc = 0.0;
+      for (int j = 0; j < bdim; ++j) acc += blk[j * bdim + i] * rhs[j];
+      sol[i] = acc;
+    }
+    for (int s = 0; s < bdim; ++s) spectra[s * nf + k] = sol[s];
+  }
+  for (int s = 0; s < bdim; ++s) b->fft->inverse(spectra.data() + s * nf, out + static_cast<Index>(s) * np);
+  const double sc = 1.0 / static_cast<double>(np);
+  for (Index i = 0; i < bdim * np; ++i) out[i] *= sc;
+}
+
+// ----------------------------------------------------------------- fields
+
+void remove_means(double* u, int c, Index nodes) {
+  for (int k = 0; k < c; ++k) {
+    double* s = u + k * nodes;
+    double sum = 0.0;
+    for (Index i = 0; i < nodes; ++i) sum += s[i];
+    const double mean = sum / static_cast<double>(nodes);
+    for (Index i = 0; i < nodes; ++i) s[i] -= mean;
+  }
+}
+
+double dot(const double* a, const double* b, Index n) {
+  double s = 0.0;
+  for (Index i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+
+double weighted_dot(const Layout& l, int m, const double* a, const double* b) {
+  const int nq = l.nq();
+  double acc = 0.0;
+  for (Index q = 0; q < l.num_quads(); ++q) {
+    const double w = l.quads[q % nq].w;
+    double s = 0.0;
+    for (int k = 0; k < m; ++k) s += a[q * m + k] * b[q * m + k];
+    acc += w * s;
+  }
+  return acc;
+}
+
+void volume_average(const Layout& l, int m, const double* s, double* out) {
+  const int nq = l.nq();
+  std::vector<double> avg(m, 0.0);
+  for (Index q = 0; q < l.num_quads(); ++q) {
+    const double w = l.quads[q % nq].w;
+    for (int k = 0; k < m; ++k) avg[k] += w * s[q * m + k];
+  }
+  const double vol = l.cell_volume();
+  for (int k = 0; k < m; ++k) out[k] = avg[k] / vol;
+}
+
+// ----------------------------------------------------------------- PCG
+
+struct PcgOut {
+  int iterations = 0;
+  bool converged = false;
+  std::vector<double> history;
+};
+
+using Op = std::function<void(const double*, double*)>;
+
+// solver.cpp:50-97.
+PcgOut pcg(const Op& apply_a, const Op& apply_minv, const double* b, Index n, int c,
+           Index nodes, double eta, int it_max, double* x) {
+  PcgOut out;
+  std::fill(x, x + n, 0.0);
+  std::vector<double> r(b, b + n), z(n), p(n), ap(n);
+  apply_minv(r.data(), z.data());
+  double rz = std::max(dot(r.data(), z.data(), n), 0.0);
+  const double norm0 = std::sqrt(rz);
+  out.history.push_back(norm0);
+  if (norm0 == 0.0) {
+    out.converged = true;
+    return out;
+  }
+  p = z;
+  for (int k = 1; k <= it_max; ++k) {
+    apply_a(p.data(), ap.data());
+    const double pap = dot(p.data(), ap.data(), n);
+    if (pap <= 0.0) throw NumericalError("pcg: non-positive curvature, operator is not positive definite");
+    const double alpha = rz / pap;
+    for (Index i = 0; i < n; ++i) x[i] += alpha * p[i];
+    for (Index i = 0; i < n; ++i) r[i] -= alpha * ap[i];
+    apply_minv(r.data(), z.data());
+    const double rzn = std::max(dot(r.data(), z.data(), n), 0.0);
+    out.iterations = k;
+    out.history.push_back(std::sqrt(rzn));
+    if (std::sqrt(rzn) <= eta * norm0) {
+      out.converged = true;
+      break;
+    }
+    const double beta = rzn / rz;
+    for (Index i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    rz = rzn;
+  }
+  remove_means(x, c, nodes);
+  return out;
+}
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+
+extern "C" {
+
+const char* or_last_error(void) { return g_last_error.c_str(); }
+
+int or_layout_info(const or_grid* g, int64_t* num_pixels, int32_t* npp, int32_t* qpp,
+                   int64_t* strides3, double* weights) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    if (num_pixels) *num_pixels = l.np;
+    if (npp) *npp = l.Nn;
+    if (qpp) *qpp = l.nq();
+    if (strides3) for (int a = 0; a < 3; ++a) strides3[a] = l.strides[a];
+    if (weights) for (int q = 0; q < l.nq(); ++q) weights[q] = l.quads[q].w;
+  });
+}
+
+int or_neighbor_table(const or_grid* g, int64_t* nbr, int32_t* n_off) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    const int no = static_cast<int>(l.offsets.size());
+    if (n_off) *n_off = no;
+    if (!nbr) return;
+    Walker w(l);
+    for (Index p = 0; p < l.np; ++p) {
+      w.neighbors();
+      for (int o = 0; o < no; ++o) nbr[p * no + o] = w.nbr[o];
+      w.advance();
+    }
+  });
+}
+
+int or_stencil_table(const or_grid* g, int32_t* ne, int32_t* offs, int32_t* nodes, double* dphi) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    int i = 0;
+    for (int q = 0; q < l.nq(); ++q) {
+      if (ne) ne[q] = static_cast<int32_t>(l.quads[q].entries.size());
+      for (const Entry& e : l.quads[q].entries) {
+        if (offs) offs[i] = e.off;
+        if (nodes) nodes[i] = e.node;
+        if (dphi) for (int a = 0; a < 3; ++a) dphi[i * 3 + a] = e.dphi[a];
+        ++i;
+      }
+    }
+  });
+}
+
+int or_isotropic_stiffness(double bulk, double shear, int32_t d, double* out) {
+  return guarded([&] { isotropic_stiffness(bulk, shear, d, out); });
+}
+
+int or_gradient(const or_grid* g, int32_t c, const double* u, double* grad) {
+  return guarded([&] { gradient(make_layout(g), c, u, grad); });
+}
+
+int or_divergence(const or_grid* g, int32_t c, const double* s, int32_t weighted, double* out) {
+  return guarded([&] { divergence(make_layout(g), c, s, weighted != 0, out); });
+}
+
+int or_apply_tangent(const or_grid* g, int32_t c, const double* tangent, const double* u,
+                     int32_t weighted, double* out) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    const int m = grad_components(l.d, c);
+    fused(l, c, u, weighted != 0, [&](Index q) { return tangent + q * m * m; }, out);
+  });
+}
+
+int or_apply_phase(const or_grid* g, int32_t c, int32_t n_phases, const double* cmat,
+                   const uint8_t* phase, const double* u, int32_t weighted, double* out) {
+  return guarded([&] { apply_phase(make_layout(g), c, n_phases, cmat, phase, u, weighted != 0, out); });
+}
+
+int or_apply_reference(const or_grid* g, int32_t c, const double* c_ref, const double* u,
+                       int32_t weighted, double* out) {
+  return guarded([&] { apply_reference(make_layout(g), c, c_ref, u, weighted != 0, out); });
+}
+
+int or_fft_forward(int32_t rank, const int64_t* dims, const double* in, double* out_c) {
+  return guarded([&] {
+    FftGrid f(std::vector<Index>(dims, dims + rank));
+    f.forward(in, reinterpret_cast<cplx*>(out_c));
+  });
+}
+
+int or_fft_inverse(int32_t rank, const int64_t* dims, const double* in_c, double* out) {
+  return guarded([&] {
+    FftGrid f(std::vector<Index>(dims, dims + rank));
+    f.inverse(reinterpret_cast<const cplx*>(in_c), out);
+  });
+}
+
+int or_precond_assemble(const or_grid* g, const double* c_ref, int32_t c, int32_t weighted,
+                        int32_t do_invert, or_precond** out) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    or_precond* p = assemble(l, c_ref, c, weighted != 0);
+    try {
+      if (do_invert) invert(p);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int or_precond_blocks(const or_precond* p, int64_t* nf, int32_t* bdim, double* blocks) {
+  return guarded([&] {
+    if (nf) *nf = p->nf;
+    if (bdim) *bdim = p->bdim;
+    if (blocks) std::memcpy(blocks, p->data.data(), sizeof(cplx) * p->data.size());
+  });
+}
+
+int or_precond_apply(const or_grid* g, const or_precond* p, const double* r, double* z) {
+  return guarded([&] { precond_apply(make_layout(g), p, r, z); });
+}
+
+void or_precond_destroy(or_precond* p) { delete p; }
+
+int or_pcg(const or_grid* g, int32_t c, int32_t n_phases, const double* cmat,
+           const uint8_t* phase, const or_precond* p, const double* b, double eta,
+           int32_t it_max, double* x, int32_t* iterations, double* history,
+           int32_t* converged) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    const Index nodes = l.num_nodes(), n = c * nodes;
+    Op A = [&](const double* v, double* out) { apply_phase(l, c, n_phases, cmat, phase, v, true, out); };
+    Op M = [&](const double* v, double* out) { precond_apply(l, p, v, out); };
+    PcgOut o = pcg(A, M, b, n, c, nodes, eta, it_max, x);
+    if (iterations) *iterations = o.iterations;
+    if (converged) *converged = o.converged ? 1 : 0;
+    if (history) std::copy(o.history.begin(), o.history.end(), history);
+  });
+}
+
+int or_volume_average(const or_grid* g, int32_t m, const double* s, double* out) {
+  return guarded([&] { volume_average(make_layout(g), m, s, out); });
+}
+
+int or_weighted_dot(const or_grid* g, int32_t m, const double* a, const double* b, double* out) {
+  return guarded([&] { *out = weighted_dot(make_layout(g), m, a, b); });
+}
+
+int or_uniform(uint64_t seed, int64_t n, double lo, double hi, double* out) {
+  return guarded([&] {
+    std::mt19937_64 gen(seed);
+    for (int64_t i = 0; i < n; ++i) {
+      const double u = static_cast<double>(gen() >> 11) * 0x1.0p-53;
+      out[i] = lo + (hi - lo) * u;
+    }
+  });
+}
+
+// Linear branch of newton_solve (solver.cpp:171-296) with the PrecondManager
+// semantics of solver.cpp:120-142 (one assembly for a linear tangent).
+int or_newton_solve(const or_grid* g, int32_t thermal, int32_t n_phases, const double* cmat,
+                    const uint8_t* phase, const double* e, const or_solve_cfg* cfg,
+                    const double* warm_u, double* u_out, double* avg_out, or_report* rep) {
+  return guarded([&] {
+    const auto t_total = Clock::now();
+    const Layout l = make_layout(g);
+    const int d = l.d, c = thermal ? 1 : d, m = grad_components(d, c), nq = l.nq();
+    if (!(cfg->eta_newton > 0.0 && cfg->eta_newton < 1.0) ||
+        !(cfg->eta_cg > 0.0 && cfg->eta_cg < 1.0))
+      throw ValidationError("solver: tolerances must lie in (0,1)");
+    if (cfg->max_newton < 1 || cfg->max_cg < 1) throw ValidationError("solver: iteration caps must be >= 1");
+    if (!(cfg->reassembly_threshold >= 0.0)) throw ValidationError("solver: reassembly threshold must be >= 0");
+    if (n_phases < 1) throw ValidationError("materials: catalog is empty");
+    for (int ph = 0; ph < n_phases; ++ph) check_spd(cmat + ph * m * m, m, "material tangent");
+    for (Index p = 0; p < l.np; ++p)
+      if (phase[p] >= n_phases) throw ValidationError("materials: phase id missing from catalog");
+    for (int k = 0; k < m; ++k)
+      if (!std::isfinite(e[k])) throw ValidationError("load vector has non-finite entries");
+
+    const Index nodes = l.num_nodes(), n = c * nodes, nQ = l.num_quads();
+    auto tan_at = [&](Index q) { return cmat + static_cast<Index>(phase[q / nq]) * m * m; };
+
+    std::vector<double> u(n, 0.0);
+    if (warm_u) std::copy(warm_u, warm_u + n, u.begin());
+
+    // Reference tangent per policy (solver.cpp:99-118), volume mean as the
+    // sequential weighted sum of fields.cpp:52-61.
+    std::vector<double> c_ref(m * m, 0.0);
+    if (cfg->policy == 0) {
+      if (!(cfg->policy_scale > 0.0)) throw ValidationError("reference: identity scale must be > 0");
+      for (int i = 0; i < m; ++i) c_ref[i * m + i] = cfg->policy_scale;
+    } else if (cfg->policy == 1) {
+      for (Index q = 0; q < nQ; ++q) {
+        const double w = l.quads[q % nq].w;
+        const double* blk = tan_at(q);
+        for (int i = 0; i < m * m; ++i) c_ref[i] += w * blk[i];
+      }
+      const double vol = l.cell_volume();
+      for (int i = 0; i < m * m; ++i) c_ref[i] /= vol;
+    } else if (cfg->policy == 2) {
+      std::copy(cfg->policy_matrix, cfg->policy_matrix + m * m, c_ref.begin());
+    } else {
+      throw ValidationError("reference: invalid policy");
+    }
+
+    std::unique_ptr<or_precond> minv;
+    std::vector<double> eps(nQ * m), sig(nQ * m), b(n), z(n), x(n), gz(nQ * m), tmpq(nQ * m);
+    double bnorm0 = 0.0, inc_rel = std::numeric_limits<double>::infinity();
+    bool have_inc = false;
+    rep->n_steps = 0;
+    rep->assemblies = 0;
+    rep->seconds_cg = rep->seconds_assembly = 0.0;
+    Op A = [&](const double* v, double* out) { fused(l, c, v, true, tan_at, out); };
+    Op M = [&](const double* v, double* out) { precond_apply(l, minv.get(), v, out); };
+    for (int step = 0;; ++step) {
+      gradient(l, c, u.data(), eps.data());
+      for (Index q = 0; q < nQ; ++q) {
+        double et[6];
+        for (int k = 0; k < m; ++k) {
+          et[k] = e[k] + eps[q * m + k];
+          if (!std::isfinite(et[k])) throw NumericalError("evaluate: non-finite strain input");
+        }
+        const double* cm = tan_at(q);
+        for (int i = 0; i < m; ++i) {
+          double acc = 0.0;
+          for (int j = 0; j < m; ++j) acc += cm[j * m + i] * et[j];
+          sig[q * m + i] = acc;
+        }
+      }
+      divergence(l, c, sig.data(), true, b.data());
+      for (Index i = 0; i < n; ++i) b[i] = -b[i];
+      bool reassembled = false;
+      auto t0 = Clock::now();
+      if (!minv) {
+        minv.reset(assemble(l, c_ref.data(), c, true));
+        invert(minv.get());
+        reassembled = true;
+        rep->assemblies += 1;
+      }
+      rep->seconds_assembly += since(t0);
+      precond_apply(l, minv.get(), b.data(), z.data());
+      const double bnorm = std::sqrt(std::max(0.0, dot(b.data(), z.data(), n)));
+      if (step == 0) bnorm0 = bnorm;
+      for (Index q = 0; q < nQ; ++q)
+        for (int k = 0; k < m; ++k) tmpq[q * m + k] = eps[q * m + k] + e[k];
+      const double strain_scale = std::sqrt(weighted_dot(l, m, tmpq.data(), tmpq.data()));
+      bool b_zero = bnorm == 0.0;
+      if (!b_zero) {
+        gradient(l, c, z.data(), gz.data());
+        b_zero = std::sqrt(weighted_dot(l, m, gz.data(), gz.data())) <= 1e-12 * strain_scale;
+      }
+      const bool residual_ok = bnorm <= cfg->eta_newton * bnorm0;
+      const bool increment_ok = have_inc && inc_rel <= cfg->eta_newton;
+      if (step > 0 && (increment_ok || residual_ok)) {
+        rep->cause = 0;
+        rep->converged = 1;
+        break;
+      }
+      if (step == cfg->max_newton) {
+        rep->cause = 2;
+        rep->converged = 0;
+        break;
+      }
+      t0 = Clock::now();
+      PcgOut po;
+      if (b_zero) {
+        std::fill(x.begin(), x.end(), 0.0);
+        po.history = {bnorm};
+        po.converged = true;
+      } else {
+        po = pcg(A, M, b.data(), n, c, nodes, cfg->eta_cg, cfg->max_cg, x.data());
+      }
+      rep->seconds_cg += since(t0);
+      for (Index i = 0; i < n; ++i) u[i] += x[i];
+      remove_means(u.data(), c, nodes);
+      if (cfg->criterion == 0) {
+        gradient(l, c, x.data(), gz.data());
+        gradient(l, c, u.data(), tmpq.data());
+        const double num = std::sqrt(weighted_dot(l, m, gz.data(), gz.data()));
+        const double den = std::sqrt(weighted_dot(l, m, tmpq.data(), tmpq.data()));
+        inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+      } else {
+        const double num = std::sqrt(dot(x.data(), x.data(), n));
+        const double den = std::sqrt(dot(u.data(), u.data(), n));
+        inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+      }
+      have_inc = true;
+      if (rep->n_steps < 32) {
+        or_newton_step& s = rep->steps[rep->n_steps];
+        s.cg_iterations = po.iterations;
+        s.residual_initial = bnorm;
+        s.residual_final = po.history.back();
+        s.increment_rel = inc_rel;
+        s.precond_reassembled = reassembled ? 1 : 0;
+      }
+      rep->n_steps += 1;
+      if (!po.converged) {
+        rep->cause = 1;
+        rep->converged = 0;
+        // Stress at the returned iterate (solver.cpp:281-290).
+        gradient(l, c, u.data(), eps.data());
+        for (Index q = 0; q < nQ; ++q) {
+          double et[6];
+          for (int k = 0; k < m; ++k) et[k] = e[k] + eps[q * m + k];
+          const double* cm = tan_at(q);
+          for (int i = 0; i < m; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < m; ++j) acc += cm[j * m + i] * et[j];
+            sig[q * m + i] = acc;
+          }
+        }
+        break;
+      }
+    }
+    volume_average(l, m, sig.data(), avg_out);
+    if (u_out) std::copy(u.begin(), u.end(), u_out);
+    rep->seconds_total = since(t_total);
+    if (!rep->converged) throw NonConvergence(rep->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+/*
+ * homfe_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * C ABI of the CPU restatement of the reference (`homfe`, arXiv 2203.02962)
+ * PCG hot path. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library; the product
+ * (paper_2203_02962_b200/) never does.
+ *
+ * Status codes mirror the reference CLI (proj/tools/homog.cpp:23-26):
+ *   0 ok, 2 ValidationError, 3 non-convergence, 4 NumericalError.
+ */
+#ifndef HOMFE_ORACLE_H
+#define HOMFE_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* StencilKind order of proj/include/homfe/grid.hpp:30-35. */
+enum {
+  OR_BILINEAR_QUAD = 0,
+  OR_TWO_TRIANGLES = 1,
+  OR_FOUR_TRIANGLES_TWO_NODE = 2,
+  OR_TRILINEAR_HEX = 3
+};
+
+typedef struct {
+  int32_t dim;          /* 2 or 3 */
+  int32_t stencil;      /* OR_* */
+  int64_t dims[3];      /* pixel counts, row-major, last axis fastest */
+  double lengths[3];    /* cell edge lengths */
+} or_grid;
+
+typedef struct {
+  double eta_newton, eta_cg;
+  int32_t max_newton, max_cg;
+  double reassembly_threshold;
+  int32_t criterion;    /* 0 strain increment, 1 displacement increment */
+  int32_t policy;       /* 0 identity-scaled, 1 volume-mean, 2 explicit */
+  double policy_scale;
+  const double* policy_matrix; /* m*m col-major, for explicit */
+} or_solve_cfg;
+
+typedef struct {
+  int32_t cg_iterations;
+  double residual_initial, residual_final, increment_rel;
+  int32_t precond_reassembled;
+} or_newton_step;
+
+typedef struct {
+  int32_t n_steps;
+  or_newton_step steps[32];
+  int32_t cause;        /* 0 converged, 1 cg-stall, 2 newton-cap */
+  int32_t converged;
+  int32_t assemblies;
+  double seconds_cg, seconds_total, seconds_assembly;
+} or_report;
+
+const char* or_last_error(void);
+
+/* Grid / layout (grid.cpp). */
+int or_layout_info(const or_grid* g, int64_t* num_pixels, int32_t* nodes_per_pixel,
+                   int32_t* quads_per_pixel, int64_t* strides3, double* quad_weights);
+/* Periodic neighbour table: nbr[p*n_offsets + o] = flat pixel index reached from
+   pixel p by stencil offset o (operators.cpp PixelWalker semantics). */
+int or_neighbor_table(const or_grid* g, int64_t* nbr, int32_t* n_offsets);
+/* Stencil table: per quad, per entry (offset, node, dphi[3]). */
+int or_stencil_table(const or_grid* g, int32_t* n_entries_per_quad, int32_t* offsets,
+                     int32_t* nodes, double* dphi);
+
+/* Mandel / materials (mandel.cpp, material.cpp). */
+int or_isotropic_stiffness(double bulk, double shear, int32_t d, double* out);
+
+/* Operators (operators.cpp). Fields use the reference layouts:
+   nodal component-planar [c][Nn*Np], quad fields interleaved [q][m],
+   tangents column-major m*m per quadrature point. */
+int or_gradient(const or_grid* g, int32_t c, const double* u, double* grad);
+int or_divergence(const or_grid* g, int32_t c, const double* s, int32_t weighted,
+                  double* out);
+int or_apply_tangent(const or_grid* g, int32_t c, const double* tangent,
+                     const double* u, int32_t weighted, double* out);
+/* Same operator, tangent given per phase (n_phases m*m blocks) plus phase map;
+   bitwise identical to or_apply_tangent on the expanded TangentField. */
+int or_apply_phase(const or_grid* g, int32_t c, int32_t n_phases, const double* cmat,
+                   const uint8_t* phase, const double* u, int32_t weighted, double* out);
+int or_apply_reference(const or_grid* g, int32_t c, const double* c_ref,
+                       const double* u, int32_t weighted, double* out);
+
+/* FFT with FFTW conventions (fft.cpp): unnormalised r2c / c2r, half spectrum. */
+int or_fft_forward(int32_t rank, const int64_t* dims, const double* in, double* out_c);
+int or_fft_inverse(int32_t rank, const int64_t* dims, const double* in_c, double* out);
+
+/* Preconditioner (precond.cpp). Opaque handle. */
+typedef struct or_precond or_precond;
+int or_precond_assemble(const or_grid* g, const double* c_ref, int32_t c,
+                        int32_t weighted, int32_t invert, or_precond** out);
+int or_precond_blocks(const or_precond* p, int64_t* num_freq, int32_t* bdim,
+                      double* blocks_c /* nullable: nf*bdim*bdim complex */);
+int or_precond_apply(const or_grid* g, const or_precond* p, const double* r, double* z);
+void or_precond_destroy(or_precond* p);
+
+/* PCG (solver.cpp:50-97) with A = phase-indexed K and M^-1 = p.
+   history must hold it_max+1 doubles. */
+int or_pcg(const or_grid* g, int32_t c, int32_t n_phases, const double* cmat,
+           const uint8_t* phase, const or_precond* p, const double* b, double eta,
+           int32_t it_max, double* x, int32_t* iterations, double* history,
+           int32_t* converged);
+
+/* Linear Newton solve (solver.cpp:171-296) for a phase-indexed linear catalog.
+   thermal=1: c=1, m=d; else c=d, m=mandel_dim(d). */
+int or_newton_solve(const or_grid* g, int32_t thermal, int32_t n_phases,
+                    const double* cmat, const uint8_t* phase, const double* e,
+                    const or_solve_cfg* cfg, const double* warm_u, double* u_out,
+                    double* avg_stress_out, or_report* report);
+
+/* Field reductions (fields.cpp). */
+int or_volume_average(const or_grid* g, int32_t m, const double* s, double* out);
+int or_weighted_dot(const or_grid* g, int32_t m, const double* a, const double* b,
+                    double* out);
+
+/* Deterministic RNG convention (tests/support/oracles.hpp:154-160):
+   std::mt19937_64(seed), u = lo + (hi-lo)*(gen()>>11)*2^-53. */
+int or_uniform(uint64_t seed, int64_t n, double lo, double hi, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

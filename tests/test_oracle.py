@@ -1,0 +1,133 @@
+"""Pins the CPU oracle (test infrastructure) against the golden fixtures made
+from dense oracles (tests/golden/make_golden.py) and against the reference's
+known-answer tests. Tolerances are the reference's own:
+  K vs dense D^T W C D < 1e-12     proj/tests/test_operators.cpp:168-193
+  D vs dense < 1e-13               proj/tests/test_operators.cpp:79-91
+  blocks vs F K F^H < 1e-11 scale  proj/tests/test_precond.cpp:47-82
+  M^-1 vs dense pinv < 1e-10       proj/tests/test_precond.cpp:201-252
+  PCG vs dense solve < 1e-8 max|x| proj/tests/test_solver.cpp:82-103
+"""
+import numpy as np
+import pytest
+
+
+def _grid(oracle_mod, meta):
+    return oracle_mod.Grid(meta["dims"], meta["lengths"], meta["stencil"])
+
+
+def test_mt19937_64_known_answer(oracle_mod, golden):
+    gen = golden.MT19937_64(77)
+    ref = np.array([gen.uniform() for _ in range(1000)])
+    np.testing.assert_array_equal(oracle_mod.uniform(77, 1000), ref)
+    g2 = golden.MT19937_64(5489)
+    for _ in range(9999):
+        g2()
+    assert g2() == 9981545732273789042
+
+
+@pytest.mark.parametrize("shape", [(2, 2), (3, 5), (4, 6), (6, 5), (5, 3, 2), (2, 2, 2), (8, 4, 6), (16, 12),
+                                   (7, 9), (32, 32, 8)])
+def test_fft_matches_numpy(oracle_mod, shape):
+    rng = np.random.default_rng(sum(shape))
+    x = rng.standard_normal(shape)
+    X = oracle_mod.fft_forward(x)
+    ref = np.fft.rfftn(x)
+    assert np.abs(X - ref).max() <= 1e-12 * np.abs(ref).max()
+    y = oracle_mod.fft_inverse(X, shape)
+    assert np.abs(y / x.size - x).max() <= 1e-13 * np.abs(x).max()
+
+
+def test_operators_match_dense_oracles(oracle_mod, golden):
+    for case in golden.load("operators.npz"):
+        g = _grid(oracle_mod, case["meta"])
+        c = case["meta"]["c"]
+        ku = oracle_mod.apply_phase(g, c, case["cmats"], case["phase"], case["u"])
+        assert np.abs(ku - case["Ku"]).max() < 1e-12, case["meta"]
+        grad = oracle_mod.gradient(g, c, case["u"])
+        assert np.abs(grad - case["grad"]).max() < 1e-13, case["meta"]
+        div = oracle_mod.divergence(g, c, case["s"])
+        assert np.abs(div - case["div"]).max() < 1e-13, case["meta"]
+        # per-quad tangent path is bitwise the phase-indexed one
+        nq = g.quads_per_pixel
+        tangent = case["cmats"][np.repeat(case["phase"], nq)]
+        np.testing.assert_array_equal(oracle_mod.apply_tangent(g, c, tangent, case["u"]), ku)
+
+
+def test_precond_blocks_and_pinv(oracle_mod, golden):
+    for case in golden.load("precond.npz"):
+        g = _grid(oracle_mod, case["meta"])
+        c = case["meta"]["c"]
+        raw = oracle_mod.Preconditioner(g, case["c_ref"], c, invert=False).blocks()
+        scale = np.abs(case["blocks"]).max()
+        assert np.abs(raw - case["blocks"]).max() < 1e-11 * scale, case["meta"]
+        inv = oracle_mod.Preconditioner(g, case["c_ref"], c)
+        z = inv.apply(case["r"])
+        assert np.abs(z - case["z"]).max() < 1e-10, case["meta"]
+
+
+def test_pcg_matches_dense_solve(oracle_mod, golden):
+    for case in golden.load("pcg.npz"):
+        g = _grid(oracle_mod, case["meta"])
+        c = case["meta"]["c"]
+        pre = oracle_mod.Preconditioner(g, case["c_ref"], c)
+        out = oracle_mod.pcg(g, c, case["cmats"], case["phase"], pre, case["b"], 1e-10, 500)
+        assert out["converged"]
+        x = case["x"]
+        assert np.abs(out["x"] - x).max() < 1e-8 * np.abs(x).max(), case["meta"]
+
+
+def test_isotropic_stiffness_kat(oracle_mod):
+    """proj/tests/test_mandel.cpp special values."""
+    c_id = oracle_mod.isotropic_stiffness(1.0 / 3.0, 0.5, 3)
+    assert np.abs(c_id - np.eye(6)).max() < 1e-15
+    c = oracle_mod.isotropic_stiffness(1.0, 0.6, 3)
+    assert abs(c[0, 0] - 1.8) < 1e-15 * 1.8
+    lam = np.linalg.eigvalsh(c)
+    assert abs(lam[5] - 3.0) < 1e-13 * 3
+    assert np.abs(lam[:5] - 1.2).max() < 1e-13 * 1.2
+    c2 = oracle_mod.isotropic_stiffness(1.0, 0.6, 2)
+    np.testing.assert_array_equal(c2, c[np.ix_([0, 1, 5], [0, 1, 5])])
+
+
+def test_one_iteration_when_reference_equals_material(oracle_mod):
+    """acceptance.cpp:45-80 / test_solver.cpp:47-65."""
+    for dims, kind in [((6, 5), "two-triangles"), ((4, 4, 4), "trilinear-hex"), ((5, 6), "bilinear-quad")]:
+        g = oracle_mod.Grid(dims, [1.0] * len(dims), kind)
+        for c in (1, g.dim):
+            m = g.m(c)
+            rng = np.random.default_rng(9001 + c)
+            a = rng.uniform(-1, 1, (m, m))
+            cm = a @ a.T + 0.5 * np.eye(m)
+            s = rng.uniform(-1, 1, (g.num_quads, m))
+            b = -oracle_mod.divergence(g, c, s)
+            pre = oracle_mod.Preconditioner(g, cm, c)
+            out = oracle_mod.pcg(g, c, cm[None], np.zeros(g.num_pixels, np.uint8), pre, b, 1e-12, 10)
+            assert out["iterations"] == 1
+            assert out["history"][-1] < 1e-12 * out["history"][0]
+
+
+def test_uniform_material_no_fluctuation(oracle_mod):
+    """test_solver.cpp:177-198."""
+    g = oracle_mod.Grid((6, 6), (1.0, 1.0), "bilinear-quad")
+    c = oracle_mod.isotropic_stiffness(1.3, 0.5, 2)
+    e = np.array([0.2, 0.0, 0.7])
+    out = oracle_mod.newton_solve(g, False, c[None], np.zeros(36, np.uint8), e)
+    assert out["converged"] and len(out["steps"]) == 1
+    assert out["steps"][0]["cg_iterations"] == 0
+    assert np.abs(out["u"]).max() < 1e-12
+    assert np.abs(out["average_stress"] - c @ e).max() < 1e-12
+
+
+def test_linear_newton_one_step_and_errors(oracle_mod):
+    g = oracle_mod.Grid((8, 8), (1.0, 1.0), "two-triangles")
+    cm = np.stack([oracle_mod.isotropic_stiffness(1.0, 0.5, 2), oracle_mod.isotropic_stiffness(25.0, 14.0, 2)])
+    ph = np.zeros((8, 8), np.uint8)
+    ph[3:5, 3:5] = 1
+    out = oracle_mod.newton_solve(g, False, cm, ph, [1.0, -0.3, 0.4], eta_cg=1e-6)
+    assert out["converged"] and len(out["steps"]) == 1 and out["assemblies"] == 1
+    with pytest.raises(oracle_mod.OracleError) as ei:
+        oracle_mod.newton_solve(g, False, cm, ph, [1.0, -0.3, 0.4], eta_newton=0.0)
+    assert ei.value.code == 2
+    with pytest.raises(oracle_mod.OracleError) as ei:
+        oracle_mod.Preconditioner(g, -np.eye(3), 2)
+    assert ei.value.code == 2
