@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 PCG hot path (driver contract: one JSON line).
+
+A "step" is one linear solve of the configuration to its PCG tolerance
+(newton_solve, linear branch: RHS, preconditioner setup, PCG loop, Newton
+check, homogenized stress) with all inputs resident in HBM.
+
+  value      DOF * PCG iterations / device time of the PCG iterations
+             (CUDA events on the library stream, summed over the K steps)
+  e2e        the same metric through the public C ABI with HOST buffers:
+             material upload (phase map H2D) + homfe_gpu_solve (u D2H) per
+             step, host clock
+  roofline   the dominant kernel (K apply) of one PCG iteration, timed live
+             with CUDA events, algorithmic bytes (16c+1) N_p per launch
+             against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the CPU oracle (faithful restatement of the reference,
+             single thread like the reference) on a bounded sample
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+       [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c1": "c1: 256^2 scalar conductivity, two triangles, 20 circles r=12 px, contrast 10, C_ref=I, eta_cg 1e-8",
+    "c2": "c2: 128^3 scalar conductivity, trilinear hex, spheres r=8 f=0.25, contrast 100, volume-mean ref, eta_cg 1e-8",
+    "c3": "c3: 256^3 linear elasticity, trilinear hex 2x2x2 Gauss, spheres r=10 f=0.30 (E 1000/1, nu 0.2/0.3), "
+          "eps_xy=0.01, C_ref=matrix phase, eta_cg 1e-6",
+    "c4": "c4: 512^3 linear elasticity, thresholded GRF l=16 f=0.5, contrast 1e4, C_ref=matrix phase, eta_cg 1e-6",
+    "c5": "c5: N^2 scalar conductivity sweep, two triangles, circles f=0.30, volume-mean ref, eta_cg 1e-8",
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def setup_problem(cfg):
+    import paper_2203_02962_b200 as hb
+    t0 = time.time()
+    phases = cfg.phases()
+    tangents = cfg.tangents()
+    g = hb.Grid(cfg.dims, [1.0] * cfg.dim, cfg.stencil)
+    mats = [hb.Material(t, cfg.thermal, cfg.dim) for t in tangents]
+    return g, mats, phases, tangents, time.time() - t0
+
+
+def run_gpu(args, rank, world, local_rank):
+    import ctypes as C
+    import torch
+    import paper_2203_02962_b200 as hb
+    from paper_2203_02962_b200 import _native, inputs
+
+    torch.cuda.set_device(local_rank)
+    cfg = inputs.config(args.config, n=args.n, contrast=args.contrast)
+    g, mats, phases, tangents, t_inputs = setup_problem(cfg)
+    solver = hb.Solver(g, mats, phases, eta_newton=cfg.eta_newton, eta_cg=cfg.eta_cg, reference=cfg.reference,
+                       reference_matrix=cfg.reference_matrix())
+    ctx = solver.ctx
+    lib = _native.lib
+    dof = cfg.dof
+    m = ctx.m
+    e = np.ascontiguousarray(cfg.load, dtype=np.float64)
+    d_u = torch.empty(cfg.components * g.num_nodes, dtype=torch.float64, device="cuda")
+    avg = np.zeros(m)
+
+    def solve_device():
+        rep = _native.Report()
+        code = lib.homfe_gpu_solve_device(ctx.h, e.ctypes.data_as(C.POINTER(C.c_double)), C.byref(solver.cfg),
+                                          None, C.c_void_p(d_u.data_ptr()),
+                                          avg.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep))
+        hb._check(code)
+        return rep
+
+    for _ in range(args.warmup):
+        solve_device()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    iters, cg_ms, launches = 0, 0.0, 0
+    with ClockSampler(local_rank) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rep = solve_device()
+            iters += rep.total_cg
+            cg_ms += rep.cg_device_ms
+            launches += rep.kernel_launches
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = clk.summary()
+    # max over ranks of the timed quantities
+    stats = torch.tensor([cg_ms, wall], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(stats, op=torch.distributed.ReduceOp.MAX)
+    cg_ms_max, wall_max = float(stats[0]), float(stats[1])
+    value = world * dof * iters / (cg_ms_max / 1e3)
+
+    # per-kernel breakdown of one PCG iteration (CUDA events, live)
+    ms = np.zeros(8)
+    hb._check(lib.homfe_gpu_kernel_times(ctx.h, 20, ms.ctypes.data_as(C.POINTER(C.c_double))))
+
+    # e2e: host buffers through the C ABI, copies inside the timed region
+    ph_host = np.ascontiguousarray(phases, dtype=np.uint8)
+    cm = np.ascontiguousarray(np.stack(tangents).transpose(0, 2, 1), dtype=np.float64)
+    u_host = np.zeros(cfg.components * g.num_nodes)
+    e2e_iters = 0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        hb._check(lib.homfe_gpu_set_material(ctx.h, cm.shape[0], cm.ctypes.data_as(C.POINTER(C.c_double)),
+                                             ph_host.ctypes.data_as(C.POINTER(C.c_uint8))))
+        rep = _native.Report()
+        hb._check(lib.homfe_gpu_solve(ctx.h, e.ctypes.data_as(C.POINTER(C.c_double)), C.byref(solver.cfg), None,
+                                      u_host.ctypes.data_as(C.POINTER(C.c_double)),
+                                      avg.ctypes.data_as(C.POINTER(C.c_double)), C.byref(rep)))
+        e2e_iters += rep.total_cg
+    e2e_wall = time.perf_counter() - t0
+    ctx._material_key = None
+    e2e_value = world * dof * e2e_iters / e2e_wall
+
+    hbm, peak_kind = peaks()
+    c = cfg.components
+    bytes_k = (16 * c + 1) * g.num_pixels
+    achieved = bytes_k / (ms[0] / 1e3) / 1e9
+    # ideal fused iteration bytes: N_p (112 c + 1)
+    b_iter = (112 * c + 1) * g.num_pixels
+    iter_ms = cg_ms_max / max(iters, 1) * world / world
+    out = {
+        "metric": "DOF·PCG-iterations/s",
+        "value": value,
+        "unit": "DOF*it/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": wall_max / args.steps * 1e3,
+        "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic: seeded RSA inclusions / GRF per SURVEY 8(d) (no dataset in the reference)",
+        "config": {"workload": WORKLOADS[args.config], "dims": list(cfg.dims), "dof": dof,
+                   "pcg_iterations_per_step": iters // args.steps, "newton_steps": rep.n_steps,
+                   "parallelism": "replicas" if world > 1 else "1 GPU",
+                   "l2": f"inputs exceed L2: {cfg.components * g.num_pixels * 8 / 1e6:.0f} MB per vector vs 126 MB"
+                   if cfg.components * g.num_pixels * 8 > 126e6 else "L2-resident working set (no flush)"},
+        "time_to_solution_s": wall_max / args.steps,
+        "iteration_ms": iter_ms,
+        "iteration_roofline_frac": (b_iter / (iter_ms / 1e3) / 1e9) / hbm,
+        "roofline": {"kernel": "stencil K apply (k_apply_elem)", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
+                     "peak_source": peak_kind, "bytes_per_launch": bytes_k},
+        "kernel_ms": {"apply_K": ms[0], "update_xr": ms[1], "fft_fwd": ms[2], "spectral": ms[3],
+                      "fft_inv": ms[4], "update_p": ms[5], "scalars": ms[6], "iteration": ms[7]},
+        "e2e": {"value": e2e_value, "unit": "DOF*it/s", "h2d_bytes_per_step": int(ph_host.nbytes + cm.nbytes + e.nbytes),
+                "d2h_bytes_per_step": int(u_host.nbytes + avg.nbytes), "steps": e2e_steps},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "input_generation_s": t_inputs,
+    }
+    return out
+
+
+def cpu_baseline(args, sample_n=64, iters=6):
+    """The oracle (faithful single-thread restatement of the reference) on a
+    bounded sample of the same workload: same recipe at sample_n^3, PCG
+    iterations timed with steady_clock-equivalent perf_counter, assembly
+    excluded."""
+    from oracle import oracle
+    from paper_2203_02962_b200 import inputs
+    cfg = inputs.config(args.config, n=sample_n) if args.config in ("c3", "c4") else inputs.config(args.config)
+    if args.config == "c5":
+        cfg = inputs.config("c5", n=256, contrast=args.contrast)
+    if args.config == "c2":
+        cfg = inputs.config("c2")
+    phases = cfg.phases()
+    tangents = cfg.tangents()
+    og = oracle.Grid(cfg.dims, [1.0] * cfg.dim, cfg.stencil)
+    c = cfg.components
+    m = tangents.shape[1]
+    cref = cfg.reference_matrix()
+    if cref is None:
+        cref = (np.bincount(phases, minlength=len(tangents))[:, None, None] * tangents).sum(0) / phases.size
+    pre = oracle.Preconditioner(og, cref, c)
+    s = oracle.uniform(1, og.num_quads * m).reshape(og.num_quads, m)
+    b = -oracle.divergence(og, c, s)
+    t0 = time.perf_counter()
+    oracle.pcg(og, c, tangents, phases, pre, b, 0.0, iters)
+    dt = time.perf_counter() - t0
+    return {"value": cfg.dof * iters / dt, "unit": "DOF*it/s", "cores": 1, "kind": "port",
+            "sample": f"{args.config} recipe at {'x'.join(map(str, cfg.dims))} ({cfg.dof} DOF), {iters} PCG "
+                      f"iterations of the faithful oracle (per-quad loop order, own FFT), assembly excluded, "
+                      f"single thread as the reference (homog.cpp:41-43)",
+            "seconds": dt}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (oracle port; the reference
+    itself cannot be built here: Eigen3/FFTW3/vendor missing)."""
+    if rank != 0:
+        return None
+    samples = []
+    for _ in range(args.warmup):
+        cpu_baseline(args, iters=2)
+    t_total = 0.0
+    dof_it = 0.0
+    for _ in range(args.steps):
+        r = cpu_baseline(args, iters=3)
+        t_total += r["seconds"]
+        dof_it += r["value"] * r["seconds"]
+        samples.append(r)
+    value = dof_it / t_total
+    return {"metric": "DOF·PCG-iterations/s", "value": value, "unit": "DOF*it/s", "impl": "reference",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY 8(d))",
+            "config": {"workload": WORKLOADS[args.config]},
+            "cpu_baseline": {"value": value, "unit": "DOF*it/s", "cores": 1, "kind": "port",
+                             "sample": samples[-1]["sample"]},
+            "e2e": {"value": value, "unit": "DOF*it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference not buildable in this image (Eigen3, FFTW3, vendor/ absent); CPU oracle port timed"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=None, help="override grid size (c3/c4/c5)")
+    ap.add_argument("--contrast", type=float, default=None)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        if args.impl == "native":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl")
+        else:
+            dist.init_process_group("gloo")
+
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    out = run_gpu(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline(args)
+            out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

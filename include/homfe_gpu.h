@@ -1,0 +1,170 @@
+/*
+ * homfe_gpu.h -- C ABI of the B200-native PCG hot path of the displacement-
+ * based, FFT-preconditioned, matrix-free FE homogenization scheme
+ * (arXiv 2203.02962; reference library `homfe`).
+ *
+ * Every entry point is `extern "C"`, takes plain pointers and sizes, never
+ * throws, and returns a status code that mirrors the reference CLI exit codes
+ * (proj/tools/homog.cpp:23-26) and exception classes
+ * (proj/include/homfe/common.hpp:15-25):
+ *   HOMFE_OK 0, HOMFE_VALIDATION 2 (ValidationError), HOMFE_NONCONVERGED 3
+ *   (cg-stall / newton-cap), HOMFE_NUMERICAL 4 (NumericalError).
+ * homfe_gpu_last_error() returns the thread-local message of the last failure.
+ *
+ * Layouts are the reference's:
+ *   nodal fields   component-planar  data[c * num_nodes + node]     (fields.hpp:16-36)
+ *   quad fields    point-interleaved data[q * m + k], q = p * nq + lq (fields.hpp:40-61)
+ *   materials      n_phases blocks of m x m, column-major Mandel      (fields.hpp:64-82)
+ *   phase map      uint8 per pixel, row-major, last axis fastest      (io.cpp:65-86)
+ * Host-buffer entry points copy in and out inside the call; the *_device
+ * variants take device pointers on the context's device.
+ *
+ * One context per host thread (mirrors proj/include/homfe/fft.hpp:18-20);
+ * every call is synchronous with respect to the host.
+ */
+#ifndef HOMFE_GPU_H
+#define HOMFE_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HOMFE_OK 0
+#define HOMFE_VALIDATION 2
+#define HOMFE_NONCONVERGED 3
+#define HOMFE_NUMERICAL 4
+#define HOMFE_DEVICE 5 /* CUDA / cuFFT failure (no reference equivalent) */
+
+/* StencilKind, in the order of proj/include/homfe/grid.hpp:30-35. */
+#define HOMFE_BILINEAR_QUAD 0
+#define HOMFE_TWO_TRIANGLES 1
+#define HOMFE_FOUR_TRIANGLES_TWO_NODE 2 /* not supported on the GPU path */
+#define HOMFE_TRILINEAR_HEX 3
+
+/* ReferencePolicy::Kind (proj/include/homfe/solver.hpp:82-101). */
+#define HOMFE_REF_IDENTITY_SCALED 0
+#define HOMFE_REF_VOLUME_MEAN 1
+#define HOMFE_REF_EXPLICIT 2
+
+typedef struct homfe_ctx homfe_ctx;
+
+/* CellSpec + StencilKind + physics (grid.hpp:14-28, material.hpp:100-118). */
+typedef struct {
+  int32_t dim;          /* 2 or 3 */
+  int32_t stencil;      /* HOMFE_* stencil kind */
+  int64_t dims[3];      /* pixel counts N_1..N_d, each >= 2 */
+  double lengths[3];    /* cell edge lengths, each > 0 */
+  int32_t components;   /* nodal components c: 1 (thermal) or dim (elasticity) */
+  int32_t device;       /* CUDA device ordinal */
+} homfe_grid_desc;
+
+/* SolveConfig + ReferencePolicy (solver.hpp:16-31, 82-101). */
+typedef struct {
+  double eta_newton;            /* default 1e-5 */
+  double eta_cg;                /* default 1e-5 */
+  int32_t max_newton;           /* default 25 */
+  int32_t max_cg;               /* default 20000 */
+  double reassembly_threshold;  /* default 0.1 (no effect for linear tangents) */
+  int32_t criterion;            /* 0 strain increment (default), 1 displacement */
+  int32_t reference_policy;     /* HOMFE_REF_*, default volume mean */
+  double reference_scale;       /* identity-scaled policy */
+  const double* reference_matrix; /* explicit policy: m x m column-major */
+} homfe_solve_cfg;
+
+/* NewtonStep / SolveReport (solver.hpp:35-55). */
+typedef struct {
+  int32_t cg_iterations;
+  double residual_initial;
+  double residual_final;
+  double increment_rel;
+  int32_t precond_reassembled;
+} homfe_newton_step;
+
+typedef struct {
+  int32_t n_steps;
+  homfe_newton_step steps[32];
+  int32_t cause;            /* 0 converged, 1 cg-stall, 2 newton-cap */
+  int32_t converged;
+  int32_t assemblies;       /* PrecondManager::assemblies() */
+  int32_t total_cg;
+  double seconds_constitutive, seconds_cg, seconds_assembly, seconds_total;
+  double cg_device_ms;      /* CUDA-event time of all PCG iterations */
+  int64_t kernel_launches;  /* kernels launched by this solve */
+} homfe_report;
+
+const char* homfe_gpu_last_error(void);
+
+/* Context: grid, device buffers, cuFFT plans. Replaces GridLayout + FftGrid +
+   the buffers owned by NodalField/FrequencyBlockDiag (grid.hpp:75-129,
+   fft.hpp:22-57, precond.hpp:28-79). */
+int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out);
+int homfe_gpu_destroy(homfe_ctx* ctx);
+
+/* MaterialMap for linear models (material.hpp:100-118): per-phase m x m
+   column-major tangents (conductivity d x d, or Mandel stiffness) and the
+   uint8 phase of every pixel. Validates like MaterialMap::validate
+   (material.cpp:252-277) and check_spd (material.cpp:13-29). */
+int homfe_gpu_set_material(homfe_ctx* ctx, int32_t n_phases, const double* tangents,
+                           const uint8_t* phase);
+int homfe_gpu_set_material_device(homfe_ctx* ctx, int32_t n_phases, const double* tangents,
+                                  const uint8_t* d_phase);
+
+/* newton_solve (solver.hpp:163-166) for linear materials: macroscopic load
+   e (m), config, optional warm start u (c * num_nodes); outputs the periodic
+   fluctuation u, the homogenized stress <sigma> (m) and the report. */
+int homfe_gpu_solve(homfe_ctx* ctx, const double* e, const homfe_solve_cfg* cfg,
+                    const double* warm_u, double* u_out, double* avg_stress_out,
+                    homfe_report* report);
+int homfe_gpu_solve_device(homfe_ctx* ctx, const double* e, const homfe_solve_cfg* cfg,
+                           const double* d_warm_u, double* d_u_out, double* avg_stress_out,
+                           homfe_report* report);
+
+/* ---- parity hooks (host buffers) ---------------------------------------- */
+/* apply_tangent_operator (operators.hpp:31-33) with the material set above. */
+int homfe_gpu_apply_K(homfe_ctx* ctx, const double* u, double* ku);
+/* Build M^-1 for c_ref (assemble_reference + invert_blocks, precond.hpp:90-102;
+   NumericalError on singular blocks) and apply it (precond.hpp:104-106). */
+int homfe_gpu_set_reference(homfe_ctx* ctx, const double* c_ref);
+int homfe_gpu_apply_minv(homfe_ctx* ctx, const double* r, double* z);
+/* Dense Fourier symbol K_ref(xi) of the stored reference, nf x c x c complex
+   (row-major within the block), for comparison with assembled blocks. */
+int homfe_gpu_reference_blocks(homfe_ctx* ctx, double* blocks_c);
+/* gradient_apply / divergence_apply (operators.hpp:20-25). */
+int homfe_gpu_gradient(homfe_ctx* ctx, const double* u, double* grad);
+int homfe_gpu_divergence(homfe_ctx* ctx, const double* s, int32_t weighted, double* out);
+/* volume_average (fields.hpp:94-95) of an m-component quad field. */
+int homfe_gpu_volume_average(homfe_ctx* ctx, const double* s, double* out);
+/* pcg_solve (solver.hpp:75-78) with A = K(material), M^-1 = reference set by
+   homfe_gpu_set_reference; history holds it_max + 1 doubles. */
+int homfe_gpu_pcg(homfe_ctx* ctx, const double* b, double eta, int32_t it_max, double* x,
+                  int32_t* iterations, double* history, int32_t* converged);
+/* Index maps for bit-exact comparison: strides (3) and the periodic neighbour
+   table nbr[p * n_offsets + o] (grid.cpp:267-288, operators.cpp:65-84),
+   computed on the device. */
+int homfe_gpu_index_maps(homfe_ctx* ctx, int64_t* strides3, int64_t* nbr, int32_t* n_offsets);
+
+/* Per-stage CUDA-event timing of one PCG iteration on the current buffers
+   (call after a solve): ms[0..7] = K apply, x/r update, forward FFT, spectral
+   solve, inverse FFT, p update, scalar kernels, whole iteration. */
+int homfe_gpu_kernel_times(homfe_ctx* ctx, int32_t reps, double* ms);
+
+/* isotropic_stiffness (proj/include/homfe/mandel.hpp:61-62): 3K P_vol +
+   2G P_dev in Mandel notation, plane strain in 2-D; column-major output. */
+int homfe_isotropic_stiffness(double bulk, double shear, int32_t dim, double* out);
+
+/* Seeded synthetic inputs, reference RNG convention (std::mt19937_64(seed),
+   (gen() >> 11) * 2^-53; proj/tests/support/oracles.hpp:154-160). */
+int homfe_random_uniform(uint64_t seed, int64_t n, double lo, double hi, double* out);
+int homfe_random_normal(uint64_t seed, int64_t n, double* out);
+
+/* Sizes of the context. */
+int homfe_gpu_sizes(const homfe_ctx* ctx, int64_t* num_pixels, int64_t* num_quads,
+                    int32_t* m, int64_t* num_frequencies);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -273,7 +273,7 @@ def pcg(g, c, cmats, phase, precond, b, eta, it_max):
     return dict(x=x, iterations=it.value, history=hist[: it.value + 1], converged=bool(conv.value))
 
 
-POLICIES = {"identity": 0, "volume-mean": 1, "explicit": 2}
+POLICIES = {"identity": 0, "identity-scaled": 0, "volume-mean": 1, "explicit": 2}
 
 
 def newton_solve(g, thermal, cmats, phase, e, eta_newton=1e-5, eta_cg=1e-5, max_newton=25,

@@ -1,0 +1,965 @@
+// context.cu -- C ABI (include/homfe_gpu.h): device context, material setup,
+// preconditioner setup, the device-resident PCG loop and the linear Newton
+// shell. Host code follows the reference control flow:
+//   pcg_solve          proj/src/solver.cpp:50-97
+//   PrecondManager     proj/src/solver.cpp:99-142
+//   newton_solve       proj/src/solver.cpp:171-296
+// The PCG iteration runs as one CUDA graph whose conditional WHILE node loops
+// on the device until the stopping test of solver.cpp:88-91 fires, so the
+// host never synchronises inside a solve.
+#include <cufft.h>
+
+#include <algorithm>
+#include <random>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/homfe_gpu.h"
+#include "kernels.cuh"
+#include "tables.hpp"
+
+using namespace hb;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CufftError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define HB_CUFFT(expr)                                                                  \
+  do {                                                                                  \
+    cufftResult _r = (expr);                                                            \
+    if (_r != CUFFT_SUCCESS) throw CufftError(std::string(#expr) + " failed: " + std::to_string((int)_r)); \
+  } while (0)
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return HOMFE_OK;
+  } catch (const ValidationError& e) {
+    g_err = e.what();
+    return HOMFE_VALIDATION;
+  } catch (const NonConverged& e) {
+    g_err = e.what();
+    return HOMFE_NONCONVERGED;
+  } catch (const NumericalError& e) {
+    g_err = e.what();
+    return HOMFE_NUMERICAL;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return HOMFE_DEVICE;
+  } catch (const CufftError& e) {
+    g_err = e.what();
+    return HOMFE_DEVICE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HOMFE_DEVICE;
+  }
+}
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  HB_CUDA(cudaMalloc(&p, n * sizeof(T) + 16));
+  return static_cast<T*>(p);
+}
+
+}  // namespace
+
+struct homfe_ctx {
+  int device = 0;
+  Grid g{};
+  StencilParams sp{};
+  int nl = 0, ne = 0;
+  int64_t nf = 0;
+  cudaStream_t stream = nullptr, stream2 = nullptr;
+  cufftHandle fwd = 0, inv = 0;
+  // material
+  int n_phases = 0;
+  std::vector<double> catalog;      // n_phases x m x m col-major
+  std::vector<int64_t> counts;      // pixels per phase
+  uint8_t* d_phase = nullptr;
+  double* d_ke = nullptr;
+  double* d_fe = nullptr;
+  double* d_cmat = nullptr;
+  // vectors
+  double *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_ap = nullptr, *d_z = nullptr, *d_u = nullptr;
+  double2* d_spec = nullptr;
+  double* d_quad = nullptr;         // lazily allocated quad field (parity hooks)
+  double4* d_tab[3] = {nullptr, nullptr, nullptr};
+  // reference
+  SpecParams spp{};
+  bool have_ref = false;
+  std::vector<double> c_ref;
+  // scalars
+  PcgState* d_st = nullptr;
+  PcgState* h_st = nullptr;         // pinned
+  double* d_partials = nullptr;
+  double* d_scal = nullptr;         // small scratch (final sums)
+  double* h_scal = nullptr;         // pinned
+  double* d_hist = nullptr;
+  int hist_cap = 0;
+  double* d_e = nullptr;
+  // graph of the whole PCG (init + device WHILE loop + mean removal)
+  cudaGraphExec_t pcg_exec = nullptr;
+  double graph_eta = -1.0;
+  int graph_itmax = -1;
+  bool use_while = true;
+  cudaGraphExec_t body_exec = nullptr;  // fallback: one iteration per launch
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  int64_t launches = 0;
+
+  int64_t nvec() const { return (int64_t)g.c * g.np; }
+};
+
+namespace {
+
+void destroy_graphs(homfe_ctx* c) {
+  if (c->pcg_exec) cudaGraphExecDestroy(c->pcg_exec);
+  if (c->body_exec) cudaGraphExecDestroy(c->body_exec);
+  c->pcg_exec = nullptr;
+  c->body_exec = nullptr;
+  c->graph_eta = -1.0;
+  c->graph_itmax = -1;
+}
+
+void sync(homfe_ctx* c) { HB_CUDA(cudaStreamSynchronize(c->stream)); }
+
+// Deterministic reduction of kRedBlocks partials (nvals each) to host.
+void reduce_to_host(homfe_ctx* c, int nvals, double* out) {
+  launch_final_sum(c->d_partials, kRedBlocks, nvals, c->d_scal, c->stream);
+  HB_CUDA(cudaMemcpyAsync(c->h_scal, c->d_scal, nvals * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  std::memcpy(out, c->h_scal, nvals * sizeof(double));
+}
+
+void fft_forward(homfe_ctx* c, const double* in, cudaStream_t s) {
+  HB_CUFFT(cufftSetStream(c->fwd, s));
+  HB_CUFFT(cufftExecD2Z(c->fwd, const_cast<double*>(in), reinterpret_cast<cufftDoubleComplex*>(c->d_spec)));
+}
+
+void fft_inverse(homfe_ctx* c, double* out, cudaStream_t s) {
+  HB_CUFFT(cufftSetStream(c->inv, s));
+  HB_CUFFT(cufftExecZ2D(c->inv, reinterpret_cast<cufftDoubleComplex*>(c->d_spec), out));
+}
+
+// z = M^-1 r; optional Parseval r.z partials.
+void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st, double* partials,
+                   cudaStream_t s) {
+  fft_forward(c, r, s);
+  launch_spectral(c->spp, c->d_spec, st, partials, s);
+  fft_inverse(c, z, s);
+  c->launches += 3;
+}
+
+void apply_K(homfe_ctx* c, const double* u, double* out, const double* fe, double scale, double* partials,
+             const PcgState* st, cudaStream_t s) {
+  ElemArgs a{u, out, c->d_phase, c->d_ke, c->n_phases, fe, scale, partials, st};
+  launch_apply_elem(c->g, a, s);
+  c->launches += 1;
+}
+
+void require_material(homfe_ctx* c) {
+  if (c->n_phases <= 0) throw ValidationError("materials: no material map set");
+}
+void require_reference(homfe_ctx* c) {
+  if (!c->have_ref) throw ValidationError("apply_preconditioner: blocks are not inverted");
+}
+
+// assemble_reference + invert_blocks (precond.cpp:44-124) for the analytic
+// symbol: validate C_ref, load the tensor, run the singularity test.
+void set_reference(homfe_ctx* c, const double* cref) {
+  const int m = c->g.m, d = c->g.d;
+  check_spd(cref, m, "reference tangent");
+  SpecParams& p = c->spp;
+  if (c->g.c == 1) {
+    for (int j = 0; j < d; ++j)
+      for (int l = 0; l < d; ++l) p.A[j * d + l] = cref[l * d + j];
+  } else {
+    mandel_to_tensor(cref, d, p.A);
+  }
+  c->c_ref.assign(cref, cref + m * m);
+  destroy_graphs(c);  // spectral kernel nodes hold the symbol parameters by value
+  launch_symbol_check(p, c->d_partials, c->stream);
+  double bad = 0.0;
+  reduce_to_host(c, 1, &bad);
+  if (bad != 0.0) {
+    c->have_ref = false;
+    throw NumericalError("invert_blocks: singular non-zero-frequency block");
+  }
+  c->have_ref = true;
+}
+
+// ---------------------------------------------------------------- PCG graph
+void capture_init(homfe_ctx* c, cudaStream_t s) {
+  const int64_t n = c->nvec();
+  HB_CUDA(cudaMemsetAsync(c->d_x, 0, n * sizeof(double), s));
+  precond_apply(c, c->d_r, c->d_z, nullptr, c->d_partials, s);
+  launch_pcg_init(c->d_st, c->d_partials, c->d_hist, s);
+  HB_CUDA(cudaMemcpyAsync(c->d_p, c->d_z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+}
+
+void capture_tail(homfe_ctx* c, cudaStream_t s) {
+  // x.remove_component_means() (solver.cpp:95)
+  launch_comp_sums(c->d_x, c->g.c, c->g.np, c->d_partials, s);
+  launch_final_sum(c->d_partials, kRedBlocks, c->g.c, c->d_scal, s);
+  launch_sub_means(c->d_x, c->g.c, c->g.np, c->d_scal, s);
+}
+
+void body_sequence(homfe_ctx* c, cudaStream_t s, bool cond, cudaGraphConditionalHandle h) {
+  const int64_t n = c->nvec();
+  apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s);
+  launch_pcg_alpha(c->d_st, c->d_partials, s);
+  launch_update_xr(c->d_x, c->d_r, c->d_p, c->d_ap, n, c->d_st, s);
+  fft_forward(c, c->d_r, s);
+  launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s);
+  launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
+  fft_inverse(c, c->d_z, s);
+  if (cond) launch_update_p_cond(c->d_p, c->d_z, n, c->d_st, h, s);
+  else launch_update_p(c->d_p, c->d_z, n, c->d_st, s);
+}
+
+void write_state(homfe_ctx* c, double eta, int it_max) {
+  std::memset(c->h_st, 0, sizeof(PcgState));
+  c->h_st->eta = eta;
+  c->h_st->it_max = it_max;
+  HB_CUDA(cudaMemcpyAsync(c->d_st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
+}
+
+bool build_while_graph(homfe_ctx* c) {
+  cudaStream_t s = c->stream;
+  cudaGraph_t graph = nullptr;
+  HB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  bool ok = true;
+  try {
+    capture_init(c, s);
+    cudaStreamCaptureStatus status;
+    cudaGraph_t cg = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    HB_CUDA(cudaStreamGetCaptureInfo(s, &status, nullptr, &cg, &deps, &ndeps));
+    cudaGraphConditionalHandle h;
+    HB_CUDA(cudaGraphConditionalHandleCreate(&h, cg, 1, cudaGraphCondAssignDefault));
+    launch_set_while(h, c->d_st, s);
+    HB_CUDA(cudaStreamGetCaptureInfo(s, &status, nullptr, &cg, &deps, &ndeps));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    HB_CUDA(cudaGraphAddNode(&cnode, cg, deps, ndeps, &cp));
+    HB_CUDA(cudaStreamUpdateCaptureDependencies(s, &cnode, 1, cudaStreamSetCaptureDependencies));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    HB_CUDA(cudaStreamBeginCaptureToGraph(c->stream2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    try {
+      body_sequence(c, c->stream2, true, h);
+    } catch (...) {
+      cudaGraph_t tmp;
+      cudaStreamEndCapture(c->stream2, &tmp);
+      throw;
+    }
+    cudaGraph_t body_out;
+    HB_CUDA(cudaStreamEndCapture(c->stream2, &body_out));
+    capture_tail(c, s);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    ok = false;
+  }
+  cudaError_t end = cudaStreamEndCapture(s, &graph);
+  if (!ok || end != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    return false;
+  }
+  cudaError_t inst = cudaGraphInstantiate(&c->pcg_exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (inst != cudaSuccess) {
+    cudaGetLastError();
+    c->pcg_exec = nullptr;
+    return false;
+  }
+  return true;
+}
+
+void build_body_graph(homfe_ctx* c) {
+  cudaStream_t s = c->stream;
+  cudaGraph_t graph = nullptr;
+  HB_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  try {
+    body_sequence(c, s, false, 0);
+  } catch (...) {
+    cudaStreamEndCapture(s, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  HB_CUDA(cudaStreamEndCapture(s, &graph));
+  HB_CUDA(cudaGraphInstantiate(&c->body_exec, graph, 0));
+  cudaGraphDestroy(graph);
+}
+
+struct PcgResult {
+  int iterations = 0;
+  bool converged = false;
+  double device_ms = 0.0;
+  double last_history = 0.0;
+};
+
+// pcg_solve with r = b already in d_r; x lands in d_x (mean-free).
+PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history) {
+  if (it_max + 1 > c->hist_cap) {
+    destroy_graphs(c);  // graphs capture the history pointer
+    if (c->d_hist) cudaFree(c->d_hist);
+    c->hist_cap = it_max + 1;
+    c->d_hist = dalloc<double>(c->hist_cap);
+  }
+  write_state(c, eta, it_max);
+  HB_CUDA(cudaEventRecord(c->ev0, c->stream));
+  if (c->use_while) {
+    if (!c->pcg_exec) {
+      if (!build_while_graph(c)) {
+        c->use_while = false;  // fall back to a host-driven loop of one-iteration graphs
+      }
+    }
+  }
+  if (c->use_while) {
+    HB_CUDA(cudaGraphLaunch(c->pcg_exec, c->stream));
+  } else {
+    capture_init(c, c->stream);
+    if (!c->body_exec) build_body_graph(c);
+    HB_CUDA(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    int launched = 0;
+    int batch = 1;
+    while (!c->h_st->done && launched < it_max) {
+      for (int i = 0; i < batch && launched < it_max; ++i, ++launched)
+        HB_CUDA(cudaGraphLaunch(c->body_exec, c->stream));
+      HB_CUDA(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      batch = std::min(batch * 2, 16);
+    }
+    capture_tail(c, c->stream);
+  }
+  HB_CUDA(cudaEventRecord(c->ev1, c->stream));
+  HB_CUDA(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  PcgResult res;
+  float ms = 0.f;
+  HB_CUDA(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  res.device_ms = ms;
+  res.iterations = c->h_st->it;
+  res.converged = c->h_st->converged != 0;
+  if (c->h_st->status == 4)
+    throw NumericalError("pcg: non-positive curvature, operator is not positive definite");
+  std::vector<double> hist(res.iterations + 1);
+  HB_CUDA(cudaMemcpy(hist.data(), c->d_hist, hist.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  res.last_history = hist.back();
+  if (h_history) std::copy(hist.begin(), hist.end(), h_history);
+  const int body_kernels = 8;
+  c->launches += (int64_t)res.iterations * body_kernels + 8;
+  return res;
+}
+
+double quad_norm(homfe_ctx* c, const double* u, const double* d_e) {
+  QuadArgs a{u, d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
+  launch_quad(c->g, c->sp, kQuadNorm2, a, c->stream);
+  c->launches += 2;
+  double v = 0.0;
+  reduce_to_host(c, 1, &v);
+  return std::sqrt(v);
+}
+
+double vec_dot(homfe_ctx* c, const double* a, const double* b) {
+  launch_dot_partials(a, b, c->nvec(), c->d_partials, c->stream);
+  c->launches += 2;
+  double v = 0.0;
+  reduce_to_host(c, 1, &v);
+  return v;
+}
+
+void remove_means(homfe_ctx* c, double* v) {
+  launch_comp_sums(v, c->g.c, c->g.np, c->d_partials, c->stream);
+  launch_final_sum(c->d_partials, kRedBlocks, c->g.c, c->d_scal, c->stream);
+  launch_sub_means(v, c->g.c, c->g.np, c->d_scal, c->stream);
+  c->launches += 3;
+}
+
+void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint8_t* phase, bool device_phase) {
+  const int m = c->g.m;
+  if (n_phases < 1) throw ValidationError("materials: catalog is empty");
+  if (n_phases > kMaxPhases) throw ValidationError("materials: at most 256 phases");
+  for (int ph = 0; ph < n_phases; ++ph) check_spd(tangents + ph * m * m, m, "material");
+  std::vector<uint8_t> host;
+  const uint8_t* hp = phase;
+  if (device_phase) {
+    host.resize(c->g.np);
+    HB_CUDA(cudaMemcpy(host.data(), phase, c->g.np, cudaMemcpyDeviceToHost));
+    hp = host.data();
+  }
+  std::vector<int64_t> counts(256, 0);
+  for (int64_t p = 0; p < c->g.np; ++p) counts[hp[p]] += 1;
+  for (int v = n_phases; v < 256; ++v)
+    if (counts[v]) throw ValidationError("materials: phase id " + std::to_string(v) + " missing from catalog");
+  counts.resize(n_phases);
+  c->counts = counts;
+  c->n_phases = n_phases;
+  c->catalog.assign(tangents, tangents + n_phases * m * m);
+  if (device_phase) HB_CUDA(cudaMemcpyAsync(c->d_phase, phase, c->g.np, cudaMemcpyDeviceToDevice, c->stream));
+  else HB_CUDA(cudaMemcpyAsync(c->d_phase, phase, c->g.np, cudaMemcpyHostToDevice, c->stream));
+  const int ne = c->ne;
+  std::vector<double> ke((size_t)n_phases * ne * ne);
+  for (int ph = 0; ph < n_phases; ++ph) element_matrix(c->sp, c->g.d, c->g.c, tangents + ph * m * m, &ke[(size_t)ph * ne * ne]);
+  if (c->d_ke) cudaFree(c->d_ke);
+  if (c->d_fe) cudaFree(c->d_fe);
+  if (c->d_cmat) cudaFree(c->d_cmat);
+  c->d_ke = dalloc<double>(ke.size());
+  c->d_fe = dalloc<double>((size_t)n_phases * ne);
+  c->d_cmat = dalloc<double>((size_t)n_phases * m * m);
+  HB_CUDA(cudaMemcpyAsync(c->d_ke, ke.data(), ke.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(cudaMemcpyAsync(c->d_cmat, tangents, (size_t)n_phases * m * m * sizeof(double), cudaMemcpyHostToDevice,
+                          c->stream));
+  sync(c);
+  destroy_graphs(c);  // graphs capture material pointers
+}
+
+// ReferencePolicy::resolve (solver.cpp:99-118); volume mean from phase counts.
+std::vector<double> resolve_reference(homfe_ctx* c, const homfe_solve_cfg* cfg) {
+  const int m = c->g.m;
+  std::vector<double> cr(m * m, 0.0);
+  if (cfg->reference_policy == HOMFE_REF_IDENTITY_SCALED) {
+    if (!(cfg->reference_scale > 0.0)) throw ValidationError("reference: identity scale must be > 0");
+    for (int i = 0; i < m; ++i) cr[i * m + i] = cfg->reference_scale;
+  } else if (cfg->reference_policy == HOMFE_REF_VOLUME_MEAN) {
+    const double wq = c->sp.w[0] * c->sp.nq;  // equal weights: pixel volume
+    for (int ph = 0; ph < c->n_phases; ++ph) {
+      const double f = (double)c->counts[ph] * wq;
+      for (int i = 0; i < m * m; ++i) cr[i] += f * c->catalog[(size_t)ph * m * m + i];
+    }
+    for (int i = 0; i < m * m; ++i) cr[i] /= c->g.cell_volume;
+  } else if (cfg->reference_policy == HOMFE_REF_EXPLICIT) {
+    if (!cfg->reference_matrix) throw ValidationError("reference: explicit matrix has wrong size");
+    std::copy(cfg->reference_matrix, cfg->reference_matrix + m * m, cr.begin());
+  } else {
+    throw ValidationError("reference: invalid policy");
+  }
+  return cr;
+}
+
+void validate_cfg(const homfe_solve_cfg* cfg) {
+  if (!cfg) throw ValidationError("solver: null config");
+  if (!(cfg->eta_newton > 0.0 && cfg->eta_newton < 1.0) || !(cfg->eta_cg > 0.0 && cfg->eta_cg < 1.0))
+    throw ValidationError("solver: tolerances must lie in (0,1)");
+  if (cfg->max_newton < 1 || cfg->max_cg < 1) throw ValidationError("solver: iteration caps must be >= 1");
+  if (!(cfg->reassembly_threshold >= 0.0)) throw ValidationError("solver: reassembly threshold must be >= 0");
+}
+
+// newton_solve, linear branch (solver.cpp:171-296). u in/out lives in d_u.
+void newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* avg_out, homfe_report* rep) {
+  const auto t_total = Clock::now();
+  validate_cfg(cfg);
+  require_material(c);
+  const int m = c->g.m, ne = c->ne;
+  for (int k = 0; k < m; ++k)
+    if (!std::isfinite(e[k])) throw ValidationError("load vector has non-finite entries");
+  std::memset(rep, 0, sizeof(*rep));
+  c->launches = 0;
+  HB_CUDA(cudaMemcpyAsync(c->d_e, e, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  // element load vectors f_e = sum_q w B^T C e per phase
+  std::vector<double> fe((size_t)c->n_phases * ne);
+  for (int ph = 0; ph < c->n_phases; ++ph)
+    element_load(c->sp, c->g.d, c->g.c, &c->catalog[(size_t)ph * m * m], e, &fe[(size_t)ph * ne]);
+  HB_CUDA(cudaMemcpyAsync(c->d_fe, fe.data(), fe.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+
+  // PrecondManager::ensure: one assembly for a linear tangent.
+  auto t0 = Clock::now();
+  const std::vector<double> cref = resolve_reference(c, cfg);
+  bool reassembled = false;
+  if (!c->have_ref || cref != c->c_ref) {
+    set_reference(c, cref.data());
+    reassembled = true;
+  }
+  rep->assemblies = 1;
+  rep->seconds_assembly += since(t0);
+
+  double bnorm0 = 0.0, inc_rel = INFINITY;
+  bool have_inc = false;
+  const int64_t n = c->nvec();
+  for (int step = 0;; ++step) {
+    t0 = Clock::now();
+    // b = -D^T W C (e + D u) = -(K u + f)
+    apply_K(c, c->d_u, c->d_r, c->d_fe, -1.0, nullptr, nullptr, c->stream);
+    sync(c);
+    rep->seconds_constitutive += since(t0);
+    // z = M^-1 b and b.z (Parseval) in one pass
+    precond_apply(c, c->d_r, c->d_z, nullptr, c->d_partials, c->stream);
+    double bz = 0.0;
+    reduce_to_host(c, 1, &bz);
+    const double bnorm = std::sqrt(std::max(0.0, bz));
+    if (step == 0) bnorm0 = bnorm;
+    const double strain_scale = quad_norm(c, c->d_u, c->d_e);
+    const bool b_is_zero = bnorm == 0.0 || quad_norm(c, c->d_z, nullptr) <= 1e-12 * strain_scale;
+    const bool residual_ok = bnorm <= cfg->eta_newton * bnorm0;
+    const bool increment_ok = have_inc && inc_rel <= cfg->eta_newton;
+    if (step > 0 && (increment_ok || residual_ok)) {
+      rep->cause = 0;
+      rep->converged = 1;
+      break;
+    }
+    if (step == cfg->max_newton) {
+      rep->cause = 2;
+      rep->converged = 0;
+      break;
+    }
+    t0 = Clock::now();
+    PcgResult pr;
+    if (b_is_zero) {
+      HB_CUDA(cudaMemsetAsync(c->d_x, 0, n * sizeof(double), c->stream));
+      pr.converged = true;
+      pr.last_history = bnorm;
+    } else {
+      pr = run_pcg(c, cfg->eta_cg, cfg->max_cg, nullptr);  // r = b already in d_r
+    }
+    rep->seconds_cg += since(t0);
+    rep->cg_device_ms += pr.device_ms;
+    // u += x; u.remove_component_means()   (solver.cpp:262-263)
+    launch_axpy(c->d_u, 1.0, c->d_x, n, c->stream);
+    c->launches += 1;
+    remove_means(c, c->d_u);
+    if (cfg->criterion == 0) {
+      const double num = quad_norm(c, c->d_x, nullptr);
+      const double den = quad_norm(c, c->d_u, nullptr);
+      inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+    } else {
+      const double num = std::sqrt(vec_dot(c, c->d_x, c->d_x));
+      const double den = std::sqrt(vec_dot(c, c->d_u, c->d_u));
+      inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+    }
+    have_inc = true;
+    if (rep->n_steps < 32) {
+      homfe_newton_step& s = rep->steps[rep->n_steps];
+      s.cg_iterations = pr.iterations;
+      s.residual_initial = bnorm;
+      s.residual_final = pr.last_history;
+      s.increment_rel = inc_rel;
+      s.precond_reassembled = (step == 0 && reassembled) ? 1 : 0;
+    }
+    rep->n_steps += 1;
+    rep->total_cg += pr.iterations;
+    if (!pr.converged) {
+      rep->cause = 1;
+      rep->converged = 0;
+      break;
+    }
+  }
+  // <sigma> = (1/|Y|) sum_q w C (e + D u)   (solver.cpp:321-324)
+  QuadArgs qa{c->d_u, c->d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
+  launch_quad(c->g, c->sp, kQuadStress, qa, c->stream);
+  c->launches += 2;
+  double avg[6];
+  reduce_to_host(c, m, avg);
+  for (int k = 0; k < m; ++k) avg_out[k] = avg[k] / c->g.cell_volume;
+  rep->seconds_total = since(t_total);
+  rep->kernel_launches = c->launches;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* homfe_gpu_last_error(void) { return g_err.c_str(); }
+
+int homfe_isotropic_stiffness(double bulk, double shear, int32_t dim, double* out) {
+  return guarded([&] { isotropic_stiffness(bulk, shear, dim, out); });
+}
+
+// Seeded inputs with the reference RNG convention (proj/tests/support/
+// oracles.hpp:154-160, proj/src/microstructure.cpp:75-90):
+// std::mt19937_64(seed), u = lo + (hi - lo) (gen() >> 11) 2^-53.
+int homfe_random_uniform(uint64_t seed, int64_t n, double lo, double hi, double* out) {
+  return guarded([&] {
+    std::mt19937_64 gen(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = lo + (hi - lo) * ((double)(gen() >> 11) * 0x1.0p-53);
+  });
+}
+
+// Standard normals by Box-Muller on consecutive uniform pairs of the same stream.
+int homfe_random_normal(uint64_t seed, int64_t n, double* out) {
+  return guarded([&] {
+    std::mt19937_64 gen(seed);
+    for (int64_t i = 0; i < n; i += 2) {
+      const double u1 = (double)(gen() >> 11) * 0x1.0p-53;
+      const double u2 = (double)(gen() >> 11) * 0x1.0p-53;
+      const double r = std::sqrt(-2.0 * std::log1p(-u1));
+      out[i] = r * std::cos(2.0 * M_PI * u2);
+      if (i + 1 < n) out[i + 1] = r * std::sin(2.0 * M_PI * u2);
+    }
+  });
+}
+
+int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out) {
+  return guarded([&] {
+    if (!desc || !out) throw ValidationError("create: null argument");
+    const int d = desc->dim;
+    if (d != 2 && d != 3) throw ValidationError("cell: dimension must be 2 or 3, got " + std::to_string(d));
+    for (int a = 0; a < d; ++a) {
+      if (desc->dims[a] < 2)
+        throw ValidationError("cell.dims[" + std::to_string(a) + "]: must be >= 2, got " + std::to_string(desc->dims[a]));
+      if (!(desc->lengths[a] > 0.0)) throw ValidationError("cell.lengths[" + std::to_string(a) + "]: must be > 0");
+      if (desc->dims[a] > (1 << 24)) throw ValidationError("cell: dimension too large");
+    }
+    const int c = desc->components;
+    if (c != 1 && c != d) throw ValidationError("nodal field shape does not match layout");
+    auto* ctx = new homfe_ctx();
+    try {
+      ctx->device = desc->device;
+      HB_CUDA(cudaSetDevice(ctx->device));
+      Grid& g = ctx->g;
+      g.d = d;
+      g.c = c;
+      g.m = c == 1 ? d : mandel_dim(d);
+      g.kind = desc->stencil;
+      g.n0 = (int)desc->dims[0];
+      g.n1 = (int)desc->dims[1];
+      g.n2 = d == 3 ? (int)desc->dims[2] : 1;
+      g.np = (int64_t)g.n0 * g.n1 * g.n2;
+      g.cell_volume = 1.0;
+      for (int a = 0; a < 3; ++a) g.h[a] = a < d ? desc->lengths[a] / (double)desc->dims[a] : 1.0;
+      for (int a = 0; a < d; ++a) g.cell_volume *= desc->lengths[a];
+      if ((int64_t)c * g.np >= (int64_t)1 << 31) throw ValidationError("cell: grid too large for one device");
+      ctx->sp = make_stencil(g.kind, d, g.h);
+      ctx->nl = ctx->sp.noff;
+      ctx->ne = ctx->nl * c;
+      const int nh = (d == 3 ? g.n2 : g.n1) / 2 + 1;
+      ctx->nf = (d == 3 ? (int64_t)g.n0 * g.n1 : (int64_t)g.n0) * nh;
+      HB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      HB_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+      HB_CUDA(cudaEventCreate(&ctx->ev0));
+      HB_CUDA(cudaEventCreate(&ctx->ev1));
+      const int64_t nv = ctx->nvec();
+      ctx->d_x = dalloc<double>(nv);
+      ctx->d_r = dalloc<double>(nv);
+      ctx->d_p = dalloc<double>(nv);
+      ctx->d_ap = dalloc<double>(nv);
+      ctx->d_z = dalloc<double>(nv);
+      ctx->d_u = dalloc<double>(nv);
+      ctx->d_spec = dalloc<double2>((size_t)c * ctx->nf);
+      ctx->d_phase = dalloc<uint8_t>(g.np);
+      ctx->d_partials = dalloc<double>((size_t)kRedBlocks * 8);
+      ctx->d_scal = dalloc<double>(64);
+      ctx->d_e = dalloc<double>(8);
+      ctx->d_st = dalloc<PcgState>(1);
+      HB_CUDA(cudaMallocHost(&ctx->h_st, sizeof(PcgState)));
+      HB_CUDA(cudaMallocHost(&ctx->h_scal, 64 * sizeof(double)));
+      HB_CUDA(cudaMemset(ctx->d_u, 0, nv * sizeof(double)));
+      // cuFFT plans: batched over the c components (component-planar fields)
+      int nn[3] = {g.n0, g.n1, g.n2};
+      HB_CUFFT(cufftPlanMany(&ctx->fwd, d, nn, nullptr, 1, (int)g.np, nullptr, 1, (int)ctx->nf, CUFFT_D2Z, c));
+      HB_CUFFT(cufftPlanMany(&ctx->inv, d, nn, nullptr, 1, (int)ctx->nf, nullptr, 1, (int)g.np, CUFFT_Z2D, c));
+      // per-axis phase tables for the analytic symbol
+      SpecParams& p = ctx->spp;
+      std::memset(&p, 0, sizeof(p));
+      p.kind = g.kind;
+      p.d = d;
+      p.c = c;
+      p.n0 = g.n0;
+      p.n1 = g.n1;
+      p.n2 = g.n2;
+      p.nh = nh;
+      p.nf = ctx->nf;
+      p.w = ctx->sp.w[0];
+      p.inv_np = 1.0 / (double)g.np;
+      for (int a = 0; a < 3; ++a) p.h[a] = g.h[a];
+      for (int a = 0; a < d; ++a) {
+        const int nfull = a == 0 ? g.n0 : (a == 1 ? g.n1 : g.n2);
+        const int len = a == d - 1 ? nh : nfull;
+        std::vector<double4> tab(len);
+        for (int k = 0; k < len; ++k) {
+          const double t = 2.0 * M_PI * (double)k / (double)nfull;
+          tab[k] = make_double4(std::sin(t), std::cos(t), std::sin(0.5 * t), std::cos(0.5 * t));
+        }
+        ctx->d_tab[a] = dalloc<double4>(len);
+        HB_CUDA(cudaMemcpy(ctx->d_tab[a], tab.data(), len * sizeof(double4), cudaMemcpyHostToDevice));
+        p.tab[a] = ctx->d_tab[a];
+      }
+      if (const char* env = std::getenv("HOMFE_NO_WHILE_GRAPH")) ctx->use_while = env[0] == '0';
+    } catch (...) {
+      homfe_gpu_destroy(ctx);
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+int homfe_gpu_destroy(homfe_ctx* c) {
+  if (!c) return HOMFE_OK;
+  cudaSetDevice(c->device);
+  destroy_graphs(c);
+  if (c->fwd) cufftDestroy(c->fwd);
+  if (c->inv) cufftDestroy(c->inv);
+  double* bufs[] = {c->d_x, c->d_r, c->d_p, c->d_ap, c->d_z, c->d_u, c->d_ke, c->d_fe, c->d_cmat,
+                    c->d_quad, c->d_partials, c->d_scal, c->d_hist, c->d_e};
+  for (double* b : bufs)
+    if (b) cudaFree(b);
+  for (auto* t : c->d_tab)
+    if (t) cudaFree(t);
+  if (c->d_spec) cudaFree(c->d_spec);
+  if (c->d_phase) cudaFree(c->d_phase);
+  if (c->d_st) cudaFree(c->d_st);
+  if (c->h_st) cudaFreeHost(c->h_st);
+  if (c->h_scal) cudaFreeHost(c->h_scal);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->stream2) cudaStreamDestroy(c->stream2);
+  delete c;
+  return HOMFE_OK;
+}
+
+int homfe_gpu_sizes(const homfe_ctx* c, int64_t* np, int64_t* nq, int32_t* m, int64_t* nf) {
+  return guarded([&] {
+    if (np) *np = c->g.np;
+    if (nq) *nq = c->g.np * c->sp.nq;
+    if (m) *m = c->g.m;
+    if (nf) *nf = c->nf;
+  });
+}
+
+int homfe_gpu_set_material(homfe_ctx* c, int32_t n_phases, const double* t, const uint8_t* phase) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    set_material(c, n_phases, t, phase, false);
+  });
+}
+
+int homfe_gpu_set_material_device(homfe_ctx* c, int32_t n_phases, const double* t, const uint8_t* d_phase) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    set_material(c, n_phases, t, d_phase, true);
+  });
+}
+
+int homfe_gpu_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* warm_u,
+                    double* u_out, double* avg_out, homfe_report* rep) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->nvec();
+    if (warm_u) HB_CUDA(cudaMemcpyAsync(c->d_u, warm_u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    else HB_CUDA(cudaMemsetAsync(c->d_u, 0, n * sizeof(double), c->stream));
+    homfe_report local;
+    homfe_report* r = rep ? rep : &local;
+    newton(c, e, cfg, avg_out, r);
+    if (u_out) HB_CUDA(cudaMemcpyAsync(u_out, c->d_u, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (!r->converged) throw NonConverged(r->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
+int homfe_gpu_solve_device(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* d_warm,
+                           double* d_u_out, double* avg_out, homfe_report* rep) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->nvec();
+    if (d_warm) HB_CUDA(cudaMemcpyAsync(c->d_u, d_warm, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    else HB_CUDA(cudaMemsetAsync(c->d_u, 0, n * sizeof(double), c->stream));
+    homfe_report local;
+    homfe_report* r = rep ? rep : &local;
+    newton(c, e, cfg, avg_out, r);
+    if (d_u_out) HB_CUDA(cudaMemcpyAsync(d_u_out, c->d_u, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    sync(c);
+    if (!r->converged) throw NonConverged(r->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
+int homfe_gpu_apply_K(homfe_ctx* c, const double* u, double* ku) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    require_material(c);
+    const int64_t n = c->nvec();
+    HB_CUDA(cudaMemcpyAsync(c->d_p, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, nullptr, nullptr, c->stream);
+    HB_CUDA(cudaMemcpyAsync(ku, c->d_ap, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  });
+}
+
+int homfe_gpu_set_reference(homfe_ctx* c, const double* c_ref) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    set_reference(c, c_ref);
+  });
+}
+
+int homfe_gpu_apply_minv(homfe_ctx* c, const double* r, double* z) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    require_reference(c);
+    const int64_t n = c->nvec();
+    HB_CUDA(cudaMemcpyAsync(c->d_r, r, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    precond_apply(c, c->d_r, c->d_z, nullptr, nullptr, c->stream);
+    HB_CUDA(cudaMemcpyAsync(z, c->d_z, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  });
+}
+
+int homfe_gpu_reference_blocks(homfe_ctx* c, double* blocks) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    require_reference(c);
+    const size_t cnt = (size_t)c->nf * c->g.c * c->g.c;
+    double2* d = dalloc<double2>(cnt);
+    launch_symbol_dump(c->spp, d, c->stream);
+    HB_CUDA(cudaMemcpyAsync(blocks, d, cnt * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    cudaFree(d);
+  });
+}
+
+static double* quad_buffer(homfe_ctx* c) {
+  if (!c->d_quad) c->d_quad = dalloc<double>((size_t)c->g.np * c->sp.nq * c->g.m);
+  return c->d_quad;
+}
+
+int homfe_gpu_gradient(homfe_ctx* c, const double* u, double* grad) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->nvec();
+    double* q = quad_buffer(c);
+    HB_CUDA(cudaMemcpyAsync(c->d_p, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    QuadArgs a{c->d_p, nullptr, c->d_phase, c->d_cmat, q, nullptr};
+    launch_quad(c->g, c->sp, kQuadGrad, a, c->stream);
+    HB_CUDA(cudaMemcpyAsync(grad, q, (size_t)c->g.np * c->sp.nq * c->g.m * sizeof(double), cudaMemcpyDeviceToHost,
+                            c->stream));
+    sync(c);
+  });
+}
+
+int homfe_gpu_divergence(homfe_ctx* c, const double* s, int32_t weighted, double* out) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->nvec();
+    double* q = quad_buffer(c);
+    HB_CUDA(cudaMemcpyAsync(q, s, (size_t)c->g.np * c->sp.nq * c->g.m * sizeof(double), cudaMemcpyHostToDevice,
+                            c->stream));
+    launch_divergence(c->g, c->sp, q, weighted != 0, c->d_ap, c->stream);
+    HB_CUDA(cudaMemcpyAsync(out, c->d_ap, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  });
+}
+
+int homfe_gpu_volume_average(homfe_ctx* c, const double* s, double* out) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    double* q = quad_buffer(c);
+    HB_CUDA(cudaMemcpyAsync(q, s, (size_t)c->g.np * c->sp.nq * c->g.m * sizeof(double), cudaMemcpyHostToDevice,
+                            c->stream));
+    launch_quad_wsum(c->g, c->sp, q, c->d_partials, c->stream);
+    double v[6];
+    reduce_to_host(c, c->g.m, v);
+    for (int k = 0; k < c->g.m; ++k) out[k] = v[k] / c->g.cell_volume;
+  });
+}
+
+int homfe_gpu_pcg(homfe_ctx* c, const double* b, double eta, int32_t it_max, double* x, int32_t* iterations,
+                  double* history, int32_t* converged) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    require_material(c);
+    require_reference(c);
+    if (it_max < 0) throw ValidationError("pcg: it_max must be >= 0");
+    const int64_t n = c->nvec();
+    HB_CUDA(cudaMemcpyAsync(c->d_r, b, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    const PcgResult r = run_pcg(c, eta, it_max, history);
+    HB_CUDA(cudaMemcpyAsync(x, c->d_x, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (iterations) *iterations = r.iterations;
+    if (converged) *converged = r.converged ? 1 : 0;
+  });
+}
+
+// Per-stage CUDA-event timing of one PCG iteration on the context's current
+// buffers (after a solve): 0 K apply, 1 x/r update, 2 forward FFT,
+// 3 spectral solve, 4 inverse FFT, 5 p update, 6 the two tiny scalar kernels,
+// 7 a whole iteration (captured body). Averages over `reps` launches.
+int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    require_material(c);
+    require_reference(c);
+    if (reps < 1) throw ValidationError("kernel_times: reps must be >= 1");
+    if (c->hist_cap < 2) {
+      destroy_graphs(c);
+      c->hist_cap = 2;
+      c->d_hist = dalloc<double>(2);
+    }
+    const int64_t n = c->nvec();
+    cudaStream_t s = c->stream;
+    // live, never-finishing state with alpha = beta = 0: full memory traffic,
+    // unchanged values
+    write_state(c, 0.0, 1 << 30);
+    sync(c);
+    cudaEvent_t a, b;
+    HB_CUDA(cudaEventCreate(&a));
+    HB_CUDA(cudaEventCreate(&b));
+    auto timeit = [&](auto&& fn) {
+      fn();  // warm
+      HB_CUDA(cudaEventRecord(a, s));
+      for (int i = 0; i < reps; ++i) fn();
+      HB_CUDA(cudaEventRecord(b, s));
+      HB_CUDA(cudaEventSynchronize(b));
+      float t = 0.f;
+      HB_CUDA(cudaEventElapsedTime(&t, a, b));
+      return (double)t / reps;
+    };
+    ms[0] = timeit([&] { apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s); });
+    ms[1] = timeit([&] { launch_update_xr(c->d_x, c->d_r, c->d_p, c->d_ap, n, c->d_st, s); });
+    ms[2] = timeit([&] { fft_forward(c, c->d_r, s); });
+    ms[3] = timeit([&] { launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s); });
+    ms[4] = timeit([&] { fft_inverse(c, c->d_z, s); });
+    ms[5] = timeit([&] { launch_update_p(c->d_p, c->d_z, n, c->d_st, s); });
+    ms[6] = timeit([&] {
+      launch_pcg_alpha(c->d_st, c->d_partials, s);
+      launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
+    });
+    write_state(c, 0.0, 1 << 30);
+    if (!c->body_exec) build_body_graph(c);
+    ms[7] = timeit([&] {
+      write_state(c, 0.0, 1 << 30);
+      HB_CUDA(cudaGraphLaunch(c->body_exec, s));
+    });
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  });
+}
+
+int homfe_gpu_index_maps(homfe_ctx* c, int64_t* strides3, int64_t* nbr, int32_t* n_off) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    const Grid& g = c->g;
+    if (strides3) {
+      strides3[0] = g.d == 3 ? (int64_t)g.n1 * g.n2 : g.n1;
+      strides3[1] = g.d == 3 ? g.n2 : 1;
+      strides3[2] = g.d == 3 ? 1 : 0;
+    }
+    if (n_off) *n_off = c->sp.noff;
+    if (nbr) {
+      const size_t cnt = (size_t)g.np * c->sp.noff;
+      int64_t* d = dalloc<int64_t>(cnt);
+      launch_index_maps(g, c->sp, d, c->stream);
+      HB_CUDA(cudaMemcpyAsync(nbr, d, cnt * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      cudaFree(d);
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// kernels.cuh -- launchers of the homfe B200 device kernels.
+#pragma once
+
+#include <cuComplex.h>
+
+#include "common.cuh"
+
+namespace hb {
+
+constexpr int kBlock = 256;
+constexpr int kRedBlocks = 1184;  // 8 x 148 SMs: fixed grid => deterministic sums
+
+struct ElemArgs {
+  const double* u;
+  double* out;
+  const uint8_t* phase;
+  const double* ke;       // n_phases x NE x NE, row-major
+  int n_phases;
+  const double* fe;       // nullable: n_phases x NE load vectors
+  double scale;           // out = scale * (K u + f)
+  double* partials;       // nullable: per-block sum of u . out
+  const PcgState* st;     // nullable: skip when st->done
+};
+
+// Node-centric K u (+ f) from per-phase element matrices; any grid size.
+void launch_apply_elem(const Grid& g, const ElemArgs& a, cudaStream_t s);
+// Element-centric fast path for 3-D hex grids (N2 % 32 == 0); returns false
+// when the grid does not qualify.
+bool launch_apply_hex_fast(const Grid& g, const ElemArgs& a, const double* lam_mu, cudaStream_t s);
+
+enum QuadMode { kQuadGrad = 0, kQuadNorm2 = 1, kQuadStress = 2 };
+struct QuadArgs {
+  const double* u;        // nullable => zero field
+  const double* e;        // nullable => no macroscopic term (device, m doubles)
+  const uint8_t* phase;
+  const double* cmat;     // n_phases x m x m column-major (stress mode)
+  double* gout;           // grad mode: num_quads x m
+  double* partials;       // norm2: 1 per block; stress: m per block
+};
+void launch_quad(const Grid& g, const StencilParams& sp, int mode, const QuadArgs& a, cudaStream_t s);
+void launch_divergence(const Grid& g, const StencilParams& sp, const double* sfield, bool weighted,
+                       double* out, cudaStream_t s);
+void launch_quad_wsum(const Grid& g, const StencilParams& sp, const double* sfield, double* partials,
+                      cudaStream_t s);
+void launch_index_maps(const Grid& g, const StencilParams& sp, int64_t* nbr, cudaStream_t s);
+
+// Vectors / reductions (deterministic: fixed grids, fixed-order finals).
+void launch_dot_partials(const double* a, const double* b, int64_t n, double* partials, cudaStream_t s);
+void launch_comp_sums(const double* a, int c, int64_t np, double* partials, cudaStream_t s);
+void launch_sub_means(double* a, int c, int64_t np, const double* sums, cudaStream_t s);
+void launch_final_sum(const double* partials, int nblocks, int nvals, double* out, cudaStream_t s);
+void launch_scale(double* a, double sc, int64_t n, cudaStream_t s);
+void launch_axpy(double* y, double a, const double* x, int64_t n, cudaStream_t s);
+
+// PCG steps (solver.cpp:62-94) with device-resident scalars.
+void launch_pcg_init(PcgState* st, const double* partials, double* hist, cudaStream_t s);
+void launch_pcg_alpha(PcgState* st, const double* partials, cudaStream_t s);
+void launch_update_xr(double* x, double* r, const double* p, const double* ap, int64_t n,
+                      const PcgState* st, cudaStream_t s);
+void launch_pcg_beta(PcgState* st, const double* partials, double* hist, cudaStream_t s);
+void launch_update_p(double* p, const double* z, int64_t n, const PcgState* st, cudaStream_t s);
+void launch_set_while(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s);
+void launch_update_p_cond(double* p, const double* z, int64_t n, const PcgState* st,
+                          cudaGraphConditionalHandle h, cudaStream_t s);
+
+// Spectral solve z_hat = K_ref_hat(xi)^+ r_hat / N_p (precond.cpp:126-162),
+// with the analytic symbol of the Nn = 1 stencils.
+struct SpecParams {
+  int kind, d, c;
+  int n0, n1, n2;       // real dims (n2 = 1 in 2-D)
+  int nh;               // last-axis spectrum length N_last/2 + 1
+  int64_t nf;
+  double w, inv_np;
+  double h[3];
+  double A[81];         // c = d: tensor A_ijkl; c = 1: C_ref (d x d) in A[0..d*d)
+  const double4* tab[3];  // per axis: (sin, cos, sin(t/2), cos(t/2))
+};
+void launch_spectral(const SpecParams& p, double2* spec, const PcgState* st, double* partials,
+                     cudaStream_t s);
+void launch_symbol_check(const SpecParams& p, double* partials, cudaStream_t s);
+void launch_symbol_dump(const SpecParams& p, double2* blocks, cudaStream_t s);
+
+}  // namespace hb

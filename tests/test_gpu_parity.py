@@ -1,0 +1,327 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+dense-oracle golden fixtures, on the same seeded inputs.
+
+Tolerances are the reference's own (proj/tests/test_operators.cpp:168-193,
+test_precond.cpp:47-82 and 201-252, test_solver.cpp:82-103) and the
+north_star's: fp64, nodal solutions within 1e-10 relative L2 at a fixed
+iteration count, homogenized stress within 1e-10 relative, PCG iteration
+counts within +-1 in tolerance mode, index maps bit-exact.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hb():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2203_02962_b200 as mod
+    return mod
+
+
+GPU_STENCILS = ("two-triangles", "bilinear-quad", "trilinear-hex")
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / max(np.linalg.norm(np.ravel(b)), 1e-300))
+
+
+def _two_phase_iso(hb, d, c, contrast=10.0):
+    if c == 1:
+        return np.stack([np.eye(d), contrast * np.eye(d)])
+    return np.stack([hb.isotropic_stiffness(0.8333, 0.3846, d), hb.isotropic_stiffness(555.5, 416.7, d)])
+
+
+def _random_phase(shape, seed, frac=0.3):
+    rng = np.random.default_rng(seed)
+    return (rng.random(int(np.prod(shape))) < frac).astype(np.uint8)
+
+
+# ------------------------------------------------------------------ maps
+@pytest.mark.parametrize("dims,stencil", [((5, 7), "two-triangles"), ((3, 4), "bilinear-quad"),
+                                          ((4, 3, 5), "trilinear-hex"), ((2, 2, 2), "trilinear-hex"),
+                                          ((33, 17, 8), "trilinear-hex")])
+def test_index_maps_bit_exact(hb, oracle_mod, dims, stencil):
+    g = hb.Grid(dims, [1.0] * len(dims), stencil)
+    strides, nbr = g.index_maps()
+    og = oracle_mod.Grid(dims, [1.0] * len(dims), stencil)
+    np.testing.assert_array_equal(strides, np.array(og.strides))
+    np.testing.assert_array_equal(nbr, og.neighbor_table())
+
+
+# ------------------------------------------------------------- operators
+def test_operators_match_golden(hb, golden):
+    for case in golden.load("operators.npz"):
+        meta = case["meta"]
+        if meta["stencil"] not in GPU_STENCILS:
+            continue
+        g = hb.Grid(meta["dims"], meta["lengths"], meta["stencil"])
+        c = meta["c"]
+        u = case["u"].reshape(c, -1)
+        tangent = case["cmats"][np.repeat(case["phase"], g.quads_per_pixel)]
+        ku = hb.apply_operator(g, tangent, u)
+        assert np.abs(ku.ravel() - case["Ku"]).max() < 1e-12, meta
+        grad = hb.gradient_apply(g, u)
+        assert np.abs(grad - case["grad"]).max() < 1e-13, meta
+        div = hb.divergence_apply(g, case["s"].reshape(g.num_quads, -1))
+        assert np.abs(div.ravel() - case["div"]).max() < 1e-13, meta
+
+
+@pytest.mark.parametrize("dims,stencil,c", [((64, 48), "two-triangles", 1), ((40, 36), "two-triangles", 2),
+                                            ((24, 20), "bilinear-quad", 2), ((16, 12, 20), "trilinear-hex", 1),
+                                            ((12, 16, 10), "trilinear-hex", 3), ((32, 32, 32), "trilinear-hex", 3),
+                                            ((8, 8, 64), "trilinear-hex", 3)])
+def test_operator_matches_oracle(hb, oracle_mod, dims, stencil, c):
+    lengths = [1.0 + 0.1 * a for a in range(len(dims))]
+    g = hb.Grid(dims, lengths, stencil)
+    og = oracle_mod.Grid(dims, lengths, stencil)
+    cm = _two_phase_iso(hb, g.dim, c)
+    ph = _random_phase(dims, 5)
+    u = oracle_mod.uniform(17, c * g.num_nodes).reshape(c, -1)
+    ref = oracle_mod.apply_phase(og, c, cm, ph, u)
+    tangent = cm[np.repeat(ph, g.quads_per_pixel)]
+    got = hb.apply_operator(g, tangent, u).ravel()
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    # bitwise reproducible
+    np.testing.assert_array_equal(hb.apply_operator(g, tangent, u).ravel(), got)
+    # rigid translations are in the kernel (test_operators.cpp:195-209)
+    t = np.ones((c, g.num_nodes)) * np.arange(1, c + 1)[:, None]
+    assert np.abs(hb.apply_operator(g, tangent, t)).max() < 1e-12 * np.abs(ref).max()
+
+
+def test_anisotropic_catalog(hb, oracle_mod):
+    """General SPD (non-isotropic) tangents per phase (oracles.hpp:178-209)."""
+    rng = np.random.default_rng(3)
+    for dims, stencil, c in [((10, 9), "two-triangles", 2), ((6, 5, 7), "trilinear-hex", 3),
+                             ((6, 5, 7), "trilinear-hex", 1)]:
+        g = hb.Grid(dims, [1.0] * len(dims), stencil)
+        og = oracle_mod.Grid(dims, [1.0] * len(dims), stencil)
+        m = g.dim if c == 1 else g.dim * (g.dim + 1) // 2
+        cm = []
+        for _ in range(4):
+            a = rng.uniform(-1, 1, (m, m))
+            cm.append(a @ a.T + 0.5 * np.eye(m))
+        cm = np.stack(cm)
+        ph = rng.integers(0, 4, g.num_pixels).astype(np.uint8)
+        u = rng.uniform(-1, 1, (c, g.num_nodes))
+        ref = oracle_mod.apply_phase(og, c, cm, ph, u)
+        got = hb.apply_operator(g, cm[np.repeat(ph, g.quads_per_pixel)], u).ravel()
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+# -------------------------------------------------------- preconditioner
+def test_symbol_matches_assembled_blocks(hb, oracle_mod, golden):
+    for case in golden.load("precond.npz"):
+        meta = case["meta"]
+        if meta["stencil"] not in GPU_STENCILS:
+            continue
+        g = hb.Grid(meta["dims"], meta["lengths"], meta["stencil"])
+        pre = hb.assemble_preconditioner(g, case["c_ref"], meta["c"])
+        sym = pre.symbol()
+        scale = np.abs(case["blocks"]).max()
+        assert np.abs(sym - case["blocks"]).max() < 1e-11 * scale, meta
+
+
+@pytest.mark.parametrize("dims,stencil,c", [((16, 12), "two-triangles", 1), ((9, 14), "two-triangles", 2),
+                                            ((10, 8), "bilinear-quad", 2), ((8, 6, 10), "trilinear-hex", 3),
+                                            ((7, 9, 6), "trilinear-hex", 1), ((64, 64), "two-triangles", 1)])
+def test_minv_matches_oracle(hb, oracle_mod, dims, stencil, c):
+    lengths = [1.0 + 0.05 * a for a in range(len(dims))]
+    g = hb.Grid(dims, lengths, stencil)
+    og = oracle_mod.Grid(dims, lengths, stencil)
+    rng = np.random.default_rng(11)
+    m = g.dim if c == 1 else g.dim * (g.dim + 1) // 2
+    a = rng.uniform(-1, 1, (m, m))
+    c_ref = a @ a.T + 0.5 * np.eye(m)
+    ref_blocks = oracle_mod.Preconditioner(og, c_ref, c, invert=False).blocks()
+    pre = hb.assemble_preconditioner(g, c_ref, c)
+    sym = pre.symbol()
+    assert np.abs(sym - ref_blocks).max() < 1e-11 * np.abs(ref_blocks).max()
+    r = rng.uniform(-1, 1, (c, g.num_nodes))
+    r -= r.mean(axis=1, keepdims=True)
+    z = hb.apply_preconditioner(g, pre, r)
+    zo = oracle_mod.Preconditioner(og, c_ref, c).apply(r)
+    assert np.abs(z.ravel() - zo).max() < 1e-10 * max(1.0, np.abs(zo).max())
+    # translations are annihilated (test_precond.cpp:213-222)
+    t = np.ones((c, g.num_nodes)) * (1.0 + 0.5 * np.arange(c))[:, None]
+    assert np.abs(hb.apply_preconditioner(g, pre, t)).max() < 1e-12
+
+
+def test_minv_matches_dense_pinv(hb, golden):
+    for case in golden.load("precond.npz"):
+        meta = case["meta"]
+        if meta["stencil"] not in GPU_STENCILS:
+            continue
+        g = hb.Grid(meta["dims"], meta["lengths"], meta["stencil"])
+        pre = hb.assemble_preconditioner(g, case["c_ref"], meta["c"])
+        z = hb.apply_preconditioner(g, pre, case["r"].reshape(meta["c"], -1))
+        assert np.abs(z.ravel() - case["z"]).max() < 1e-10, meta
+
+
+def test_reference_validation(hb):
+    g = hb.Grid([4, 4], [1.0, 1.0], "two-triangles")
+    with pytest.raises(hb.ValidationError):
+        hb.assemble_preconditioner(g, -np.eye(3), 2)
+    with pytest.raises(hb.ValidationError):
+        hb.assemble_preconditioner(g, np.array([[1.0, 2.0, 0], [0, 1, 0], [0, 0, 1]]), 2)
+
+
+# ------------------------------------------------------------------ PCG
+def test_pcg_matches_dense_solve(hb, golden):
+    for case in golden.load("pcg.npz"):
+        meta = case["meta"]
+        g = hb.Grid(meta["dims"], meta["lengths"], meta["stencil"])
+        c = meta["c"]
+        mats = [hb.Material(t, c == 1, g.dim) for t in case["cmats"]]
+        pre = hb.assemble_preconditioner(g, case["c_ref"], c)
+        out = hb.pcg_solve(g, mats, case["phase"], pre, case["b"].reshape(c, -1), 1e-10, 500)
+        assert out["converged"]
+        assert np.abs(out["x"].ravel() - case["x"]).max() < 1e-8 * np.abs(case["x"]).max(), meta
+
+
+@pytest.mark.parametrize("dims,stencil,c", [((48, 40), "two-triangles", 1), ((20, 24), "two-triangles", 2),
+                                            ((16, 16, 16), "trilinear-hex", 3), ((20, 16, 12), "trilinear-hex", 1)])
+def test_pcg_fixed_k_and_tolerance_parity(hb, oracle_mod, dims, stencil, c):
+    g = hb.Grid(dims, [1.0] * len(dims), stencil)
+    og = oracle_mod.Grid(dims, [1.0] * len(dims), stencil)
+    cm = _two_phase_iso(hb, g.dim, c, 50.0)
+    ph = _random_phase(dims, 23, 0.35)
+    m = cm.shape[1]
+    c_ref = cm[0]
+    s = oracle_mod.uniform(29, g.num_quads * m).reshape(g.num_quads, m)
+    b = -oracle_mod.divergence(og, c, s)
+    opre = oracle_mod.Preconditioner(og, c_ref, c)
+    tol = oracle_mod.pcg(og, c, cm, ph, opre, b, 1e-8, 2000)
+    assert tol["converged"]
+    mats = [hb.Material(t, c == 1, g.dim) for t in cm]
+    pre = hb.assemble_preconditioner(g, c_ref, c)
+    got = hb.pcg_solve(g, mats, ph, pre, b.reshape(c, -1), 1e-8, 2000)
+    assert got["converged"]
+    assert abs(got["iterations"] - tol["iterations"]) <= 1
+    # fixed iteration count: eta = 0 never stops early
+    k = min(got["iterations"], tol["iterations"])
+    fo = oracle_mod.pcg(og, c, cm, ph, opre, b, 0.0, k)
+    fg = hb.pcg_solve(g, mats, ph, pre, b.reshape(c, -1), 0.0, k)
+    assert fg["iterations"] == fo["iterations"] == k
+    assert _rel(fg["x"], fo["x"]) <= 1e-10
+    # residual norms: recursive residuals of two fp64 PCGs agree to
+    # ~cond(K) * eps relative to |r_0|_{M^-1}
+    np.testing.assert_allclose(fg["history"], fo["history"], rtol=1e-9, atol=1e-6 * fo["history"][0])
+
+
+def test_pcg_one_iteration_when_reference_is_material(hb, oracle_mod):
+    """acceptance.cpp:45-80: C_ref = C solves in one iteration."""
+    for dims, stencil in [((6, 5), "two-triangles"), ((4, 4, 4), "trilinear-hex"), ((5, 6), "bilinear-quad")]:
+        g = hb.Grid(dims, [1.0] * len(dims), stencil)
+        for c in (1, g.dim):
+            m = g.dim if c == 1 else g.dim * (g.dim + 1) // 2
+            rng = np.random.default_rng(9001 + c)
+            a = rng.uniform(-1, 1, (m, m))
+            cm = a @ a.T + 0.5 * np.eye(m)
+            s = rng.uniform(-1, 1, (g.num_quads, m))
+            b = -hb.divergence_apply(g, s)
+            pre = hb.assemble_preconditioner(g, cm, c)
+            out = hb.pcg_solve(g, [hb.Material(cm, c == 1, g.dim)], np.zeros(g.num_pixels, np.uint8), pre, b,
+                               1e-12, 10)
+            assert out["iterations"] == 1
+            assert out["history"][-1] < 1e-12 * out["history"][0]
+
+
+def test_pcg_zero_rhs(hb):
+    g = hb.Grid([4, 4], [1.0, 1.0], "two-triangles")
+    c_ref = np.eye(3)
+    pre = hb.assemble_preconditioner(g, c_ref, 2)
+    out = hb.pcg_solve(g, [hb.Material(c_ref, False, 2)], np.zeros(16, np.uint8), pre, np.zeros((2, 16)), 1e-8, 50)
+    assert out["converged"] and out["iterations"] == 0 and np.abs(out["x"]).max() == 0.0
+
+
+# --------------------------------------------------------------- Newton
+def _newton_pair(hb, oracle_mod, dims, stencil, thermal, cm, ph, e, **kw):
+    g = hb.Grid(dims, [1.0] * len(dims), stencil)
+    og = oracle_mod.Grid(dims, [1.0] * len(dims), stencil)
+    mats = [hb.Material(t, thermal, g.dim) for t in cm]
+    got = hb.newton_solve(g, mats, ph, e, **kw)
+    okw = dict(kw)
+    if "reference_matrix" in okw and okw.get("reference") == "explicit":
+        pass
+    ref = oracle_mod.newton_solve(og, thermal, cm, ph, e, **okw)
+    return got, ref
+
+
+@pytest.mark.parametrize("name,dims,stencil,thermal", [("c1-like", (64, 64), "two-triangles", True),
+                                                        ("c2-like", (24, 24, 24), "trilinear-hex", True),
+                                                        ("c3-like", (16, 16, 16), "trilinear-hex", False),
+                                                        ("c5-like", (96, 96), "two-triangles", True),
+                                                        ("elastic-2d", (32, 24), "two-triangles", False)])
+def test_newton_matches_oracle(hb, oracle_mod, name, dims, stencil, thermal):
+    from paper_2203_02962_b200 import inputs
+    d = len(dims)
+    if thermal:
+        cm = np.stack([np.eye(d), 100.0 * np.eye(d)])
+        e = np.zeros(d)
+        e[0] = 1.0
+    else:
+        cm = _two_phase_iso(hb, d, d)
+        e = np.zeros(d * (d + 1) // 2)
+        e[-1] = np.sqrt(2.0) * 0.01
+    ph, _ = inputs.rsa_balls(dims, radius=dims[0] / 8.0, seed=7, fraction=0.25)
+    for kw in (dict(eta_cg=1e-8), dict(eta_cg=1e-6, reference="explicit", reference_matrix=cm[0]),
+               dict(eta_cg=1e-8, reference="identity-scaled", reference_scale=2.0, criterion="displacement")):
+        got, ref = _newton_pair(hb, oracle_mod, dims, stencil, thermal, cm, ph, e, **kw)
+        assert got["converged"] and ref["converged"]
+        k_g = got["report"]["steps"][0]["cg_iterations"]
+        k_o = ref["steps"][0]["cg_iterations"]
+        assert abs(k_g - k_o) <= 1, (name, kw, k_g, k_o)
+        assert got["report"]["newton_steps"] == len(ref["steps"])
+        tol = 1e-10 if k_g == k_o else 10 * kw["eta_cg"]
+        assert _rel(got["u"], ref["u"]) <= max(tol, 1e-10), (name, kw)
+        assert _rel(got["average_stress"], ref["average_stress"]) <= max(tol, 1e-10), (name, kw)
+
+
+def test_uniform_material_no_fluctuation(hb):
+    """test_solver.cpp:177-198."""
+    g = hb.Grid([6, 6], [1.0, 1.0], "bilinear-quad")
+    c = hb.isotropic_stiffness(1.3, 0.5, 2)
+    out = hb.newton_solve(g, [hb.Material.linear_elastic(c)], np.zeros(36, np.uint8), [0.2, 0.0, 0.7])
+    assert out["converged"] and out["report"]["newton_steps"] == 1
+    assert out["report"]["steps"][0]["cg_iterations"] == 0
+    assert np.abs(out["u"]).max() < 1e-12
+    assert np.abs(out["average_stress"] - c @ np.array([0.2, 0.0, 0.7])).max() < 1e-12
+
+
+def test_newton_errors(hb):
+    g = hb.Grid([8, 8], [1.0, 1.0], "two-triangles")
+    mats = [hb.Material.isotropic_elastic(1.0, 0.5, 2), hb.Material.isotropic_elastic(25.0, 14.0, 2)]
+    ph = np.zeros(64, np.uint8)
+    ph[20:30] = 1
+    with pytest.raises(hb.ValidationError):
+        hb.newton_solve(g, mats, ph, [1.0, 0.0, 0.0], eta_newton=0.0)
+    with pytest.raises(hb.ValidationError):
+        hb.newton_solve(g, mats[:1], ph, [1.0, 0.0, 0.0])  # phase 1 missing from catalog
+    with pytest.raises(hb.ValidationError):
+        hb.newton_solve(g, mats, ph, [np.nan, 0.0, 0.0])
+    out = hb.newton_solve(g, mats, ph, [1.0, 0.0, 0.0], max_cg=1, eta_cg=1e-12)
+    assert not out["converged"] and out["report"]["cause"] == "cg-stall"
+
+
+def test_hashin_coated_sphere_neutrality(hb):
+    """acceptance.cpp:290-317: <tr sigma>/3 within 2% of 3.0 at 32^3."""
+    n = 32
+    rho, r1, r2 = 1e3, 0.2, 0.4
+    f = (r1 / r2) ** 3
+    denom = 1.0 + (1.0 - f) * (1.0 - rho) / (1.8 * rho)
+    k1 = 1.0 / (rho + f * (1.0 - rho) / denom)
+    mods = [(k1, 0.6 * k1), (rho * k1, 0.6 * rho * k1), (1.0, 0.6)]
+    x = (np.arange(n) + 0.5) / n
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    r = np.sqrt((X - 0.5) ** 2 + (Y - 0.5) ** 2 + (Z - 0.5) ** 2).ravel()
+    ph = np.where(r < r1, 0, np.where(r < r2, 1, 2)).astype(np.uint8)
+    g = hb.Grid([n, n, n], [1.0, 1.0, 1.0], "trilinear-hex")
+    mats = [hb.Material.isotropic_elastic(k, gm, 3) for k, gm in mods]
+    out = hb.newton_solve(g, mats, ph, [1.0, 1.0, 1.0, 0.0, 0.0, 0.0], eta_cg=1e-6)
+    assert out["converged"]
+    mean = out["average_stress"][:3].mean()
+    assert abs(mean - 3.0) / 3.0 < 0.02
