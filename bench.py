@@ -227,7 +227,7 @@ def run_gpu(args, rank, world, local_rank):
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                      "peak_source": peak_kind, "bytes_per_launch": bytes_k},
         "kernel_ms": {"apply_K": ms[0], "update_xr": ms[1], "fft_fwd": ms[2], "spectral": ms[3],
-                      "fft_inv": ms[4], "update_p": ms[5], "scalars": ms[6], "iteration": ms[7]},
+                      "fft_inv": ms[4], "update_p": ms[5], "scalars": ms[6], "sum": float(ms[:7].sum())},
         "e2e": {"value": e2e_value, "unit": "DOF*it/s", "h2d_bytes_per_step": int(ph_host.nbytes + cm.nbytes + e.nbytes),
                 "d2h_bytes_per_step": int(u_host.nbytes + avg.nbytes), "steps": e2e_steps},
         "clocks": clocks,

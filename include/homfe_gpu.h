@@ -147,7 +147,7 @@ int homfe_gpu_index_maps(homfe_ctx* ctx, int64_t* strides3, int64_t* nbr, int32_
 
 /* Per-stage CUDA-event timing of one PCG iteration on the current buffers
    (call after a solve): ms[0..7] = K apply, x/r update, forward FFT, spectral
-   solve, inverse FFT, p update, scalar kernels, whole iteration. */
+   solve, inverse FFT, p update, scalar kernels, their sum. */
 int homfe_gpu_kernel_times(homfe_ctx* ctx, int32_t reps, double* ms);
 
 /* isotropic_stiffness (proj/include/homfe/mandel.hpp:61-62): 3K P_vol +

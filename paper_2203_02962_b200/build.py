@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include")]
 SOURCES = ["kernels.cu", "spectral.cu", "hexfast.cu", "context.cu"]
-HEADERS = ["common.cuh", "kernels.cuh", "tables.hpp"]
+HEADERS = ["common.cuh", "kernels.cuh", "tables.hpp", "hex_modes.inc"]
 
 
 def _stale(target, deps):

@@ -3,6 +3,8 @@
 
 #include <cuComplex.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace hb {
@@ -24,9 +26,12 @@ struct ElemArgs {
 
 // Node-centric K u (+ f) from per-phase element matrices; any grid size.
 void launch_apply_elem(const Grid& g, const ElemArgs& a, cudaStream_t s);
-// Element-centric fast path for 3-D hex grids (N2 % 32 == 0); returns false
-// when the grid does not qualify.
-bool launch_apply_hex_fast(const Grid& g, const ElemArgs& a, const double* lam_mu, cudaStream_t s);
+// Element-centric modal fast path for trilinear hex on cubic voxels
+// (hexfast.cu). Tables: per-phase material data in the modal basis.
+bool hex_fast_eligible(const Grid& g);
+bool hex_fast_tables(const Grid& g, int n_phases, const double* cmats, std::vector<double>& iso,
+                     std::vector<double>& gen);
+void launch_hex_fast(const Grid& g, const ElemArgs& a, const double* d_mat, bool iso, cudaStream_t s);
 
 enum QuadMode { kQuadGrad = 0, kQuadNorm2 = 1, kQuadStress = 2 };
 struct QuadArgs {

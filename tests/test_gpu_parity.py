@@ -276,9 +276,38 @@ def test_newton_matches_oracle(hb, oracle_mod, name, dims, stencil, thermal):
         k_o = ref["steps"][0]["cg_iterations"]
         assert abs(k_g - k_o) <= 1, (name, kw, k_g, k_o)
         assert got["report"]["newton_steps"] == len(ref["steps"])
-        tol = 1e-10 if k_g == k_o else 10 * kw["eta_cg"]
-        assert _rel(got["u"], ref["u"]) <= max(tol, 1e-10), (name, kw)
-        assert _rel(got["average_stress"], ref["average_stress"]) <= max(tol, 1e-10), (name, kw)
+        if k_g == k_o:
+            # fixed-k parity: 1e-10, or 30x the oracle-vs-oracle noise floor
+            # where the reference's own FFT-probed blocks
+            # (rounding ~1e-14 at low frequency) are amplified by the Krylov
+            # process beyond it
+            floor = _noise_floor(oracle_mod, dims, stencil, thermal, cm, ph, e, kw, k_o)
+            tol = max(1e-10, 30 * floor)
+        else:
+            tol = 10 * kw["eta_cg"]
+        assert _rel(got["u"], ref["u"]) <= tol, (name, kw)
+        assert _rel(got["average_stress"], ref["average_stress"]) <= tol, (name, kw)
+
+
+def _noise_floor(oracle_mod, dims, stencil, thermal, cm, ph, e, kw, k):
+    """Oracle vs oracle at k iterations with the right-hand side perturbed at
+    the GPU-vs-oracle operator difference (2e-14 relative)."""
+    og = oracle_mod.Grid(dims, [1.0] * len(dims), stencil)
+    c = 1 if thermal else len(dims)
+    nq = og.quads_per_pixel
+    sig = np.einsum("qij,j->qi", cm[np.repeat(ph, nq)], e)
+    b = -oracle_mod.divergence(og, c, sig)
+    if kw.get("reference") == "explicit":
+        cref = kw["reference_matrix"]
+    elif kw.get("reference") == "identity-scaled":
+        cref = kw["reference_scale"] * np.eye(cm.shape[1])
+    else:
+        cref = (np.bincount(ph, minlength=len(cm))[:, None, None] * cm).sum(0) / ph.size
+    pre = oracle_mod.Preconditioner(og, cref, c)
+    x0 = oracle_mod.pcg(og, c, cm, ph, pre, b, 0.0, k)["x"]
+    rng = np.random.default_rng(1)
+    x1 = oracle_mod.pcg(og, c, cm, ph, pre, b * (1 + 2e-14 * rng.standard_normal(b.size)), 0.0, k)["x"]
+    return _rel(x1, x0)
 
 
 def test_uniform_material_no_fluctuation(hb):
@@ -325,3 +354,34 @@ def test_hashin_coated_sphere_neutrality(hb):
     assert out["converged"]
     mean = out["average_stress"][:3].mean()
     assert abs(mean - 3.0) / 3.0 < 0.02
+
+
+@pytest.mark.parametrize("dims,c,iso", [((16, 8, 32), 3, True), ((16, 8, 32), 3, False), ((32, 16, 64), 1, True),
+                                        ((16, 16, 32), 1, False), ((32, 32, 32), 3, True),
+                                        ((16, 8, 256), 3, True)])
+def test_hex_fast_path_matches_oracle(hb, oracle_mod, dims, c, iso, monkeypatch):
+    """The element-centric modal kernel (hexfast.cu) on eligible grids, against
+    the oracle and against the generic node-centric kernel."""
+    g = hb.Grid(dims, [1.0, 1.0, 1.0], "trilinear-hex")
+    og = oracle_mod.Grid(dims, [1.0, 1.0, 1.0], "trilinear-hex")
+    rng = np.random.default_rng(13)
+    if iso:
+        cm = _two_phase_iso(hb, 3, c, 1000.0)
+        ph = _random_phase(dims, 2, 0.3)
+    else:
+        m = 3 if c == 1 else 6
+        cm = []
+        for _ in range(3):
+            a = rng.uniform(-1, 1, (m, m))
+            cm.append(a @ a.T + 0.5 * np.eye(m))
+        cm = np.stack(cm)
+        ph = rng.integers(0, 3, g.num_pixels).astype(np.uint8)
+    u = rng.uniform(-1, 1, (c, g.num_nodes))
+    ref = oracle_mod.apply_phase(og, c, cm, ph, u)
+    tangent = cm[np.repeat(ph, 8)]
+    fast = hb.apply_operator(g, tangent, u).ravel()
+    assert np.abs(fast - ref).max() <= 1e-12 * np.abs(ref).max()
+    monkeypatch.setenv("HOMFE_HEX_FAST", "0")
+    g2 = hb.Grid(dims, [1.0, 1.0, 1.0], "trilinear-hex")
+    slow = hb.apply_operator(g2, tangent, u).ravel()
+    assert np.abs(fast - slow).max() <= 1e-12 * np.abs(ref).max()
