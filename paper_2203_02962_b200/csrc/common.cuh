@@ -72,7 +72,7 @@ struct PcgState {
   int32_t done;     // loop finished (converged, cap, or breakdown)
   int32_t converged;
   int32_t status;   // 0 ok, 4 non-positive curvature
-  int32_t pad;
+  int32_t active;   // the current iteration computed alpha (not finished before it)
 };
 
 __host__ __device__ inline int mandel_dim(int d) { return d * (d + 1) / 2; }

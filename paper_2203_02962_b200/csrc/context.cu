@@ -98,6 +98,10 @@ struct homfe_ctx {
   double2* d_spec = nullptr;
   double* d_quad = nullptr;         // lazily allocated quad field (parity hooks)
   double4* d_tab[3] = {nullptr, nullptr, nullptr};
+  // fused three-pass preconditioner (fftfused.cu)
+  bool fused = false;
+  FusedFft ff{};
+  double2* d_tw = nullptr;          // W_{n1} then W_{n0}
   // reference
   SpecParams spp{};
   bool have_ref = false;
@@ -157,6 +161,12 @@ void fft_inverse(homfe_ctx* c, double* out, cudaStream_t s) {
 // z = M^-1 r; optional Parseval r.z partials.
 void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st, double* partials,
                    cudaStream_t s) {
+  if (c->fused) {
+    fused_forward(c->ff, c->spp, const_cast<double*>(r), nullptr, nullptr, partials, s);
+    fused_inverse(c->ff, nullptr, nullptr, z, nullptr, 0, s);
+    c->launches += 2;
+    return;
+  }
   fft_forward(c, r, s);
   launch_spectral(c->spp, c->d_spec, st, partials, s);
   fft_inverse(c, z, s);
@@ -206,6 +216,12 @@ void set_reference(homfe_ctx* c, const double* cref) {
 void capture_init(homfe_ctx* c, cudaStream_t s) {
   const int64_t n = c->nvec();
   HB_CUDA(cudaMemsetAsync(c->d_x, 0, n * sizeof(double), s));
+  if (c->fused) {
+    fused_forward(c->ff, c->spp, c->d_r, nullptr, nullptr, c->d_partials, s);
+    launch_pcg_init(c->d_st, c->d_partials, c->d_hist, s);
+    fused_inverse(c->ff, c->d_p, nullptr, nullptr, nullptr, 1, s);  // p = z_0
+    return;
+  }
   precond_apply(c, c->d_r, c->d_z, nullptr, c->d_partials, s);
   launch_pcg_init(c->d_st, c->d_partials, c->d_hist, s);
   HB_CUDA(cudaMemcpyAsync(c->d_p, c->d_z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -220,6 +236,17 @@ void capture_tail(homfe_ctx* c, cudaStream_t s) {
 
 void body_sequence(homfe_ctx* c, cudaStream_t s, bool cond, cudaGraphConditionalHandle h) {
   const int64_t n = c->nvec();
+  if (c->fused) {
+    // K p (+ p.Ap) -> alpha -> [r -= alpha Ap, F r, K^-1, F^-1 pencils, r.z]
+    // -> beta -> [F^-1 planes, x += alpha p, p = z + beta p]
+    apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s);
+    launch_pcg_alpha(c->d_st, c->d_partials, s);
+    fused_forward(c->ff, c->spp, c->d_r, c->d_ap, c->d_st, c->d_partials, s);
+    if (cond) launch_pcg_beta_cond(c->d_st, c->d_partials, c->d_hist, h, s);
+    else launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
+    fused_inverse(c->ff, c->d_p, c->d_x, nullptr, c->d_st, 0, s);
+    return;
+  }
   apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s);
   launch_pcg_alpha(c->d_st, c->d_partials, s);
   launch_update_xr(c->d_x, c->d_r, c->d_p, c->d_ap, n, c->d_st, s);
@@ -231,10 +258,11 @@ void body_sequence(homfe_ctx* c, cudaStream_t s, bool cond, cudaGraphConditional
   else launch_update_p(c->d_p, c->d_z, n, c->d_st, s);
 }
 
-void write_state(homfe_ctx* c, double eta, int it_max) {
+void write_state(homfe_ctx* c, double eta, int it_max, int active = 0) {
   std::memset(c->h_st, 0, sizeof(PcgState));
   c->h_st->eta = eta;
   c->h_st->it_max = it_max;
+  c->h_st->active = active;
   HB_CUDA(cudaMemcpyAsync(c->d_st, c->h_st, sizeof(PcgState), cudaMemcpyHostToDevice, c->stream));
 }
 
@@ -367,7 +395,7 @@ PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history) {
   HB_CUDA(cudaMemcpy(hist.data(), c->d_hist, hist.size() * sizeof(double), cudaMemcpyDeviceToHost));
   res.last_history = hist.back();
   if (h_history) std::copy(hist.begin(), hist.end(), h_history);
-  const int body_kernels = 8;
+  const int body_kernels = c->fused ? 6 : 8;
   c->launches += (int64_t)res.iterations * body_kernels + 8;
   return res;
 }
@@ -708,6 +736,40 @@ int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out) {
         p.tab[a] = ctx->d_tab[a];
       }
       if (const char* env = std::getenv("HOMFE_NO_WHILE_GRAPH")) ctx->use_while = env[0] == '0';
+      const char* fenv = std::getenv("HOMFE_FUSED_FFT");
+      if (fused_fft_eligible(g) && !(fenv && fenv[0] == '0')) {
+        const int n1 = g.n1, n0 = g.n0;
+        // twiddles: N <= 256 in the four-step layout tw[k2 * (N/16) + n1] =
+        // W_N^{n1 k2}; N = 512 as the plain table W_N^k (fft.cuh)
+        auto table = [](int n, std::vector<double2>& out) {
+          if (n <= 256) {
+            const int A = n / 16;
+            for (int k2 = 0; k2 < 16; ++k2)
+              for (int n1 = 0; n1 < A; ++n1) {
+                const double t = -2.0 * M_PI * (double)(n1 * k2) / (double)n;
+                out.push_back(make_double2(std::cos(t), std::sin(t)));
+              }
+          } else {
+            for (int k = 0; k < n; ++k) {
+              const double t = -2.0 * M_PI * (double)k / (double)n;
+              out.push_back(make_double2(std::cos(t), std::sin(t)));
+            }
+          }
+        };
+        std::vector<double2> tw;
+        table(n1, tw);
+        table(n0, tw);
+        ctx->d_tw = dalloc<double2>(tw.size());
+        HB_CUDA(cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        ctx->ff.n0 = n0;
+        ctx->ff.np_plane = n1;
+        ctx->ff.c = c;
+        ctx->ff.np = g.np;
+        ctx->ff.T = ctx->d_spec;
+        ctx->ff.tw_plane = ctx->d_tw;
+        ctx->ff.tw0 = ctx->d_tw + n1;
+        ctx->fused = true;
+      }
     } catch (...) {
       homfe_gpu_destroy(ctx);
       throw;
@@ -729,6 +791,7 @@ int homfe_gpu_destroy(homfe_ctx* c) {
   for (auto* t : c->d_tab)
     if (t) cudaFree(t);
   if (c->d_spec) cudaFree(c->d_spec);
+  if (c->d_tw) cudaFree(c->d_tw);
   if (c->d_phase) cudaFree(c->d_phase);
   if (c->d_st) cudaFree(c->d_st);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -921,7 +984,7 @@ int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
     cudaStream_t s = c->stream;
     // live, never-finishing state with alpha = beta = 0: full memory traffic,
     // unchanged values
-    write_state(c, 0.0, 1 << 30);
+    write_state(c, 0.0, 1 << 30, 1);
     sync(c);
     cudaEvent_t a, b;
     HB_CUDA(cudaEventCreate(&a));
@@ -937,6 +1000,22 @@ int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
       return (double)t / reps;
     };
     ms[0] = timeit([&] { apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s); });
+    if (c->fused) {
+      // pass 1 (r update + forward plane FFTs), pass 2 (pencils + solve)
+      ms[1] = timeit([&] { fused_forward(c->ff, c->spp, c->d_r, c->d_ap, c->d_st, nullptr, s, 1); });
+      ms[2] = -1.0;
+      ms[3] = timeit([&] { fused_forward(c->ff, c->spp, c->d_r, c->d_ap, c->d_st, c->d_partials, s, 2); });
+      ms[4] = -1.0;
+      ms[5] = timeit([&] { fused_inverse(c->ff, c->d_p, c->d_x, nullptr, c->d_st, 0, s); });
+      ms[6] = timeit([&] {
+        launch_pcg_alpha(c->d_st, c->d_partials, s);
+        launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
+      });
+      ms[7] = ms[0] + ms[1] + ms[3] + ms[5] + ms[6];
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+      return;
+    }
     ms[1] = timeit([&] { launch_update_xr(c->d_x, c->d_r, c->d_p, c->d_ap, n, c->d_st, s); });
     ms[2] = timeit([&] { fft_forward(c, c->d_r, s); });
     ms[3] = timeit([&] { launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s); });

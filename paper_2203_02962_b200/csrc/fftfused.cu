@@ -1,0 +1,516 @@
+// fftfused.cu -- the preconditioner M^-1 = F^-1 K_ref_hat^+ F of one PCG
+// iteration as three streaming passes, fused with the PCG vector updates.
+//
+// The reference calls FFTW r2c/c2r per component and runs the per-frequency
+// block multiply and the axpys as separate sweeps (precond.cpp:126-162,
+// solver.cpp:80-92). cuFFT needs three HBM passes per 3-D transform; with the
+// pointwise solve and the two update kernels that is 10 passes over c fields
+// per iteration. Here:
+//
+//   pass 1  k_plane_fwd  one thread-block cluster per (component, x0-plane):
+//           r <- r - alpha Ap (written back), 2-D r2c FFT of the plane
+//           (row FFTs in each CTA's shared memory, column FFTs over DSMEM),
+//           half spectrum T written once;
+//   pass 2  k_pencil     per (k1, k2-tile): 1-D FFT along axis 0 for all c
+//           components, z_hat = K_ref_hat(xi)^+ r_hat / N_p with the analytic
+//           symbol, r.z by Parseval, inverse 1-D FFT, T written back;
+//   pass 3  k_plane_inv  one cluster per (component, plane): inverse 2-D
+//           c2r FFT, then x <- x + alpha p and p <- z + beta p (z is never
+//           stored).
+//
+// Per component and voxel this moves 32 + 16 + 40 = 88 bytes, against 8
+// streaming passes (~216 bytes) for cuFFT + separate kernels.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "fft.cuh"
+#include "kernels.cuh"
+#include "spectral.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace hb {
+
+namespace {
+
+using fft::cadd;
+using fft::cmul;
+using fft::conj;
+using fft::csub;
+
+constexpr int kThreads = 256;
+
+enum { kModePcg = 0, kModePlain = 1, kModeInit = 2, kModeZ = 3 };
+
+struct PlaneArgs {
+  int n0;              // planes per component (axis 0)
+  int64_t np;          // pixels per component
+  double* r;           // pass 1 input (updated in PCG mode)
+  const double* ap;    // pass 1, PCG mode
+  double2* T;          // [c][n0][NP][NP/2+1] half spectrum (no axis-0 FFT)
+  double* p;           // pass 3
+  double* x;           // pass 3, PCG mode
+  double* z;           // pass 3, z mode
+  const double2* tw;   // W_NP table
+  const PcgState* st;  // PCG mode
+  int mode;
+};
+
+template <int NP>
+constexpr int tpf() {
+  return NP / 16;
+}
+
+// Plane kernels: one cluster of CL = NP/32 CTAs per (component, plane), each
+// CTA NP threads = 16 transform groups of TPF = NP/16 threads, 32 rows.
+// Column slots: NP/2 per plane, 16 per CTA; slot 0 of rank 0 pairs the two
+// real columns k2 = 0 and k2 = NP/2 in one complex transform.
+template <int NP>
+constexpr int rows_slots() {
+  constexpr int P = NP / 2 + 1;
+  return 32 * P > 16 * (NP + 1) ? 32 * P : 16 * (NP + 1);
+}
+
+template <int NP>
+__global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
+  constexpr int P = NP / 2 + 1;
+  constexpr int CL = NP / 32;
+  constexpr int TPF = tpf<NP>();
+  constexpr int H = NP / 2;
+  constexpr int PT = 32 * H / NP;  // double2 per thread in the row block (= 16)
+  if (a.mode == kModePcg && !a.st->active) return;
+  extern __shared__ double2 sm[];
+  double2* rows = sm;                      // 32 x P (row phase) / 16 x (NP+1) (column phase)
+  double2* tws = rows + rows_slots<NP>();  // NP
+  __shared__ __align__(8) uint64_t bar;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int cid = blockIdx.x / CL;
+  const int comp = cid / a.n0, i0 = cid % a.n0;
+  const int tid = threadIdx.x, g = tid / TPF, t = tid % TPF;
+  const int64_t plane = (int64_t)comp * a.np + (int64_t)i0 * NP * NP + (int64_t)rank * 32 * NP;
+  constexpr uint32_t ROWB = NP * sizeof(double);
+  const bool pcg = a.mode == kModePcg;
+  if (tid == 0) {
+    fft::mbar_init(&bar, 1);
+    fft::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    fft::mbar_expect_tx(&bar, 32 * ROWB);
+    for (int y = 0; y < 32; ++y) fft::bulk_g2s(rows + y * P, a.r + plane + (int64_t)y * NP, ROWB, &bar);
+  }
+  for (int i = tid; i < NP; i += NP) tws[i] = a.tw[i];
+  double2 apv[PT];
+  if (pcg) {
+    const double2* ap2 = reinterpret_cast<const double2*>(a.ap + plane);
+#pragma unroll
+    for (int i = 0; i < PT; ++i) apv[i] = ap2[tid + i * NP];
+  }
+  fft::mbar_wait(&bar, 0);
+  if (pcg) {
+    const double alpha = a.st->alpha;
+#pragma unroll
+    for (int i = 0; i < PT; ++i) {
+      const int idx = tid + i * NP, row = idx / H, c2 = idx % H;
+      double2 v = rows[row * P + c2];
+      v.x = fma(-alpha, apv[i].x, v.x);
+      v.y = fma(-alpha, apv[i].y, v.y);
+      rows[row * P + c2] = v;
+    }
+    __syncthreads();
+    // r written back by TMA bulk stores (async proxy: no generic stores left
+    // in flight at the cluster barriers below)
+    if (tid == 0) {
+      fft::fence_proxy_async();
+      for (int y = 0; y < 32; ++y) fft::bulk_s2g(a.r + plane + (int64_t)y * NP, rows + y * P, ROWB);
+      fft::bulk_commit();
+      fft::bulk_wait_read();
+    }
+  }
+  __syncthreads();
+  // row r2c: group g transforms the row pair (2g, 2g+1) in place
+  {
+    double2* buf = rows + (2 * g) * P;
+    const double* xa = reinterpret_cast<const double*>(rows + (2 * g) * P);
+    const double* xb = reinterpret_cast<const double*>(rows + (2 * g + 1) * P);
+    double2 v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = make_double2(xa[t + i * TPF], xb[t + i * TPF]);
+    fft::group_sync();
+    fft::fft4step_regs<NP, false>(v, buf, t, tws);
+    constexpr int KN = (P + TPF - 1) / TPF;
+    double2 za[KN], zb[KN];
+#pragma unroll
+    for (int i = 0; i < KN; ++i) {
+      const int k = t + i * TPF;
+      if (k < P) {
+        const double2 zk = buf[k % NP], zm = conj(buf[(NP - k) % NP]);
+        const double2 s = cadd(zk, zm), d = csub(zk, zm);
+        za[i] = make_double2(0.5 * s.x, 0.5 * s.y);
+        zb[i] = make_double2(0.5 * d.y, -0.5 * d.x);  // -i/2 * d
+      }
+    }
+    fft::group_sync();
+#pragma unroll
+    for (int i = 0; i < KN; ++i) {
+      const int k = t + i * TPF;
+      if (k < P) {
+        buf[k] = za[i];
+        buf[P + k] = zb[i];
+      }
+    }
+  }
+  cluster.sync();
+  // gather this CTA's 16 column slots over DSMEM straight into registers
+  const int slot = rank * 16 + g;
+  double2 v[16];
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) {
+    const int y = t + TPF * n2;
+    const double2* src = cluster.map_shared_rank(rows, y >> 5) + (y & 31) * P;
+    if (slot == 0) v[n2] = make_double2(src[0].x, src[NP / 2].x);
+    else v[n2] = src[slot];
+  }
+  cluster.sync();  // every remote read done: local rows become column buffers
+  double2* cbuf = rows + g * (NP + 1);
+  fft::fft4step_regs<NP, false>(v, cbuf, t, tws);
+  __syncthreads();
+  double2* Tp = a.T + ((int64_t)comp * a.n0 + i0) * NP * P;
+  const int first = rank == 0 ? 1 : 0;
+  const int ncol = 16 - first;
+  for (int idx = tid; idx < ncol * NP; idx += NP) {
+    const int k1 = idx / ncol, j = idx % ncol + first;
+    Tp[(int64_t)k1 * P + rank * 16 + j] = rows[j * (NP + 1) + k1];
+  }
+  if (rank == 0 && g == 0) {
+    // split the paired real columns k2 = 0 and k2 = NP/2
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int k = t + i * TPF;
+      const double2 zk = cbuf[k], zm = conj(cbuf[(NP - k) % NP]);
+      const double2 s = cadd(zk, zm), d = csub(zk, zm);
+      Tp[(int64_t)k * P] = make_double2(0.5 * s.x, 0.5 * s.y);
+      Tp[(int64_t)k * P + NP / 2] = make_double2(0.5 * d.y, -0.5 * d.x);
+    }
+  }
+}
+
+template <int NP>
+__global__ void __launch_bounds__(NP, 2) k_plane_inv(const PlaneArgs a) {
+  constexpr int P = NP / 2 + 1;
+  constexpr int CL = NP / 32;
+  constexpr int TPF = tpf<NP>();
+  constexpr int H = NP / 2;
+  constexpr int PT = 32 * H / NP;
+  if (a.mode == kModePcg && !a.st->active) return;
+  extern __shared__ double2 sm[];
+  double2* rows = sm;
+  double2* tws = rows + rows_slots<NP>();
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int cid = blockIdx.x / CL;
+  const int comp = cid / a.n0, i0 = cid % a.n0;
+  const int tid = threadIdx.x, g = tid / TPF, t = tid % TPF;
+  for (int i = tid; i < NP; i += NP) tws[i] = a.tw[i];
+  const int slot = rank * 16 + g;
+  const double2* Tp = a.T + ((int64_t)comp * a.n0 + i0) * NP * P;
+  // column slot inputs k1 = t + TPF n2 (neighbouring groups share sectors)
+  double2 v[16];
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) {
+    const int k = t + TPF * n2;
+    if (slot == 0) {
+      const double2 A = Tp[(int64_t)k * P], B = Tp[(int64_t)k * P + NP / 2];
+      v[n2] = make_double2(A.x - B.y, A.y + B.x);  // A + i B
+    } else {
+      v[n2] = Tp[(int64_t)k * P + slot];
+    }
+  }
+  __syncthreads();
+  double2* cbuf = rows + g * (NP + 1);
+  fft::fft4step_regs<NP, true>(v, cbuf, t, tws);
+  double2 w[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) w[i] = cbuf[t + TPF * i];
+  cluster.sync();  // all column results in registers: regions become row storage
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int y = t + TPF * i;
+    double2* dst = cluster.map_shared_rank(rows, y >> 5) + (y & 31) * P;
+    if (slot == 0) {
+      dst[0] = make_double2(w[i].x, 0.0);
+      dst[NP / 2] = make_double2(w[i].y, 0.0);
+    } else {
+      dst[slot] = w[i];
+    }
+  }
+  cluster.sync();
+  // inverse row c2r: group g, rows (2g, 2g+1): Z = A + i B, z = IFFT(Z)
+  {
+    double2* buf = rows + (2 * g) * P;
+    const double2* A = rows + (2 * g) * P;
+    const double2* B = rows + (2 * g + 1) * P;
+    double2 u[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int n = t + i * TPF;
+      const int k = n <= NP / 2 ? n : NP - n;
+      double2 av = A[k], bv = B[k];
+      if (k == 0 || k == NP / 2) {
+        av.y = 0.0;
+        bv.y = 0.0;
+      }
+      u[i] = n <= NP / 2 ? make_double2(av.x - bv.y, av.y + bv.x) : make_double2(av.x + bv.y, bv.x - av.y);
+    }
+    fft::group_sync();
+    fft::fft4step_regs<NP, true>(u, buf, t, tws);
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)comp * a.np + (int64_t)i0 * NP * NP + (int64_t)rank * 32 * NP;
+  auto zval = [&](int idx) {
+    const int row = idx / H, c2 = idx % H;
+    const double2* zb = rows + (row & ~1) * P + 2 * c2;
+    const double2 z0 = zb[0], z1 = zb[1];
+    return (row & 1) ? make_double2(z0.y, z1.y) : make_double2(z0.x, z1.x);
+  };
+  if (a.mode == kModePcg) {
+    double2* p2 = reinterpret_cast<double2*>(a.p + plane);
+    double2* x2 = reinterpret_cast<double2*>(a.x + plane);
+    double2 pv[PT], xv[PT];
+#pragma unroll
+    for (int i = 0; i < PT; ++i) {
+      pv[i] = p2[tid + i * NP];
+      xv[i] = x2[tid + i * NP];
+    }
+    const double alpha = a.st->alpha, beta = a.st->beta;
+    const int conv = a.st->converged;
+#pragma unroll
+    for (int i = 0; i < PT; ++i) {
+      const int idx = tid + i * NP;
+      x2[idx] = make_double2(fma(alpha, pv[i].x, xv[i].x), fma(alpha, pv[i].y, xv[i].y));
+      if (!conv) {
+        const double2 zv = zval(idx);
+        p2[idx] = make_double2(fma(beta, pv[i].x, zv.x), fma(beta, pv[i].y, zv.y));
+      }
+    }
+  } else {
+    double2* out = reinterpret_cast<double2*>((a.mode == kModeInit ? a.p : a.z) + plane);
+#pragma unroll
+    for (int i = 0; i < PT; ++i) out[tid + i * NP] = zval(tid + i * NP);
+  }
+}
+
+struct PencilArgs {
+  int n0, n1;              // n1 = NP (plane size), T rows per plane
+  int P;                   // NP/2 + 1
+  int ntk;                 // k2 tiles per k1
+  double2* T;
+  const double2* tw;       // W_N0 table
+  const PcgState* st;      // nullable
+  double* partials;        // nullable (Parseval r.z)
+  int nred;
+};
+
+constexpr int kBK = 8;
+
+template <int N0, int C>
+__global__ void __launch_bounds__(kThreads, 2) k_pencil(const __grid_constant__ SpecParams sp, const PencilArgs a) {
+  constexpr int TPF = tpf<N0>();
+  constexpr int G = kThreads / TPF;
+  constexpr int NPC = C * kBK;  // pencils per tile
+  static_assert(NPC % (32 / TPF > 0 ? 32 / TPF : 1) == 0, "pencil count must fill warps");
+  if (a.st && !a.st->active) return;
+  extern __shared__ double2 sm[];
+  constexpr int LD = N0 + 1;       // padded pencil stride (conflict-free transposes)
+  double2* buf = sm;               // [C][kBK][LD]
+  double2* tws = buf + NPC * LD;   // N0
+  const int tid = threadIdx.x, g = tid / TPF, t = tid % TPF;
+  for (int i = tid; i < N0; i += kThreads) tws[i] = a.tw[i];
+  const int P = a.P;
+  const int64_t cstride = (int64_t)a.n0 * a.n1 * P;
+  double rz = 0.0;
+  const int ntiles = a.n1 * a.ntk;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int k1 = tile / a.ntk, c0 = (tile % a.ntk) * kBK;
+    const int nc = min(kBK, P - c0);
+    __syncthreads();
+#pragma unroll 8
+    for (int idx = tid; idx < C * N0 * kBK; idx += kThreads) {
+      const int j = idx % kBK, i0 = (idx / kBK) % N0, comp = idx / (kBK * N0);
+      double2 v = make_double2(0.0, 0.0);
+      if (j < nc) v = a.T[comp * cstride + ((int64_t)i0 * a.n1 + k1) * P + c0 + j];
+      buf[(comp * kBK + j) * LD + i0] = v;
+    }
+    __syncthreads();
+    for (int pc = g; pc < NPC; pc += G) fft::fft<N0, false>(buf + pc * LD, t, tws);
+    __syncthreads();
+    for (int e = tid; e < N0 * kBK; e += kThreads) {
+      const int j = e / N0, k0 = e % N0;
+      if (j >= nc) continue;
+      const int k2 = c0 + j;
+      double2 r[C], z[C];
+#pragma unroll
+      for (int i = 0; i < C; ++i) r[i] = buf[(i * kBK + j) * LD + k0];
+      if (k0 == 0 && k1 == 0 && k2 == 0) {
+#pragma unroll
+        for (int i = 0; i < C; ++i) z[i] = make_double2(0.0, 0.0);
+      } else {
+        const int f[3] = {k0, k1, k2};
+        double M[3][3], K[3][3], I[3][3];
+        spec::gram<3>(sp, f, M);
+        spec::symbol<3, C>(sp, M, K);
+        spec::sym_inverse<C>(K, I);
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          double zr = 0.0, zi = 0.0;
+#pragma unroll
+          for (int jj = 0; jj < C; ++jj) {
+            zr = fma(I[i][jj], r[jj].x, zr);
+            zi = fma(I[i][jj], r[jj].y, zi);
+          }
+          z[i] = make_double2(zr * sp.inv_np, zi * sp.inv_np);
+        }
+        const double wgt = (k2 == 0 || 2 * k2 == a.n1) ? 1.0 : 2.0;
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < C; ++i) s += r[i].x * z[i].x + r[i].y * z[i].y;
+        rz = fma(wgt, s, rz);
+      }
+#pragma unroll
+      for (int i = 0; i < C; ++i) buf[(i * kBK + j) * LD + k0] = z[i];
+    }
+    __syncthreads();
+    for (int pc = g; pc < NPC; pc += G) fft::fft<N0, true>(buf + pc * LD, t, tws);
+    __syncthreads();
+    for (int idx = tid; idx < C * N0 * kBK; idx += kThreads) {
+      const int j = idx % kBK, i0 = (idx / kBK) % N0, comp = idx / (kBK * N0);
+      if (j < nc) a.T[comp * cstride + ((int64_t)i0 * a.n1 + k1) * P + c0 + j] = buf[(comp * kBK + j) * LD + i0];
+    }
+  }
+  if (a.partials) {
+    __shared__ double red[32];
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rz += __shfl_xor_sync(0xffffffffu, rz, o);
+    if (lane == 0) red[warp] = rz;
+    __syncthreads();
+    if (warp == 0) {
+      double s2 = lane < (kThreads / 32) ? red[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (lane == 0) a.partials[blockIdx.x] = s2;
+    }
+    if (blockIdx.x == 0)
+      for (int i = gridDim.x + tid; i < a.nred; i += kThreads) a.partials[i] = 0.0;
+  }
+}
+
+template <class K>
+void launch_cluster(K kernel, int grid, int block, int cl, size_t smem, cudaStream_t s, const PlaneArgs& a) {
+  HB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HB_CUDA(cudaLaunchKernelEx(&cfg, kernel, a));
+}
+
+template <int NP>
+void run_planes(const FusedFft& f, bool inverse, const PlaneArgs& a, cudaStream_t s) {
+  constexpr int CL = NP / 32;
+  const size_t smem = sizeof(double2) * ((size_t)rows_slots<NP>() + NP);
+  const int grid = CL * f.n0 * f.c;
+  if (inverse) launch_cluster(k_plane_inv<NP>, grid, NP, CL, smem, s, a);
+  else launch_cluster(k_plane_fwd<NP>, grid, NP, CL, smem, s, a);
+}
+
+template <int N0>
+void run_pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st, double* partials, cudaStream_t s) {
+  PencilArgs a;
+  a.n0 = f.n0;
+  a.n1 = f.np_plane;
+  a.P = f.np_plane / 2 + 1;
+  a.ntk = (a.P + kBK - 1) / kBK;
+  a.T = f.T;
+  a.tw = f.tw0;
+  a.st = st;
+  a.partials = partials;
+  a.nred = kRedBlocks;
+  const int ntiles = a.n1 * a.ntk;
+  const int grid = ntiles < kRedBlocks ? ntiles : kRedBlocks;
+  const size_t smem = sizeof(double2) * ((size_t)f.c * kBK * (N0 + 1) + N0);
+  if (f.c == 3) {
+    HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_pencil<N0, 3><<<grid, kThreads, smem, s>>>(sp, a);
+  } else {
+    HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_pencil<N0, 1><<<grid, kThreads, smem, s>>>(sp, a);
+  }
+  HB_CUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+bool fused_fft_eligible(const Grid& g) {
+  if (g.d != 3 || (g.c != 1 && g.c != 3)) return false;
+  if (g.n1 != g.n2 || (g.n2 != 128 && g.n2 != 256)) return false;
+  if (g.n0 != 64 && g.n0 != 128 && g.n0 != 256 && g.n0 != 512) return false;
+  return true;
+}
+
+static void planes(const FusedFft& f, bool inverse, const PlaneArgs& a, cudaStream_t s) {
+  if (f.np_plane == 256) run_planes<256>(f, inverse, a, s);
+  else run_planes<128>(f, inverse, a, s);
+}
+
+static void pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st, double* partials, cudaStream_t s) {
+  switch (f.n0) {
+    case 64: run_pencils<64>(f, sp, st, partials, s); break;
+    case 128: run_pencils<128>(f, sp, st, partials, s); break;
+    case 256: run_pencils<256>(f, sp, st, partials, s); break;
+    default: run_pencils<512>(f, sp, st, partials, s); break;
+  }
+}
+
+// PCG iteration part: r -= alpha Ap; z = M^-1 r (with r.z partials).
+void fused_forward(const FusedFft& f, const SpecParams& sp, double* r, const double* ap, const PcgState* st,
+                   double* partials, cudaStream_t s, int which) {
+  PlaneArgs a = {};
+  a.n0 = f.n0;
+  a.np = f.np;
+  a.r = r;
+  a.ap = ap;
+  a.T = f.T;
+  a.tw = f.tw_plane;
+  a.st = st;
+  a.mode = ap ? kModePcg : kModePlain;
+  if (which & 1) planes(f, false, a, s);
+  if (which & 2) pencils(f, sp, st, partials, s);
+}
+
+// x += alpha p; p = z + beta p   (st != nullptr), or p = z (init), or z out.
+void fused_inverse(const FusedFft& f, double* p, double* x, double* z, const PcgState* st, int init,
+                   cudaStream_t s) {
+  PlaneArgs a = {};
+  a.n0 = f.n0;
+  a.np = f.np;
+  a.T = f.T;
+  a.tw = f.tw_plane;
+  a.p = p;
+  a.x = x;
+  a.z = z;
+  a.st = st;
+  a.mode = st ? kModePcg : (init ? kModeInit : kModeZ);
+  planes(f, true, a, s);
+}
+
+}  // namespace hb

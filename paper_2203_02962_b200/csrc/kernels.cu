@@ -402,22 +402,27 @@ __global__ void k_pcg_init(PcgState* st, const double* partials, int nblocks, do
 
 // alpha = rz / p.Ap, abort on non-positive curvature (solver.cpp:74-80).
 __global__ void k_pcg_alpha(PcgState* st, const double* partials, int nblocks) {
-  if (st->done) return;
+  if (st->done) {
+    if (threadIdx.x == 0) st->active = 0;
+    return;
+  }
   const double pap = block_total(partials, nblocks);
   if (threadIdx.x == 0) {
     st->pap = pap;
     if (!(pap > 0.0)) {
       st->status = 4;
       st->done = 1;
+      st->active = 0;
     } else {
       st->alpha = st->rz / pap;
+      st->active = 1;
     }
   }
 }
 
 __global__ void k_update_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                             const double* __restrict__ ap, int64_t n, const PcgState* st) {
-  if (st->done) return;
+  if (!st->active) return;
   const double alpha = st->alpha;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     x[i] = fma(alpha, p[i], x[i]);
@@ -427,7 +432,7 @@ __global__ void k_update_xr(double* __restrict__ x, double* __restrict__ r, cons
 
 // rz_next, history, stopping test, beta (solver.cpp:84-93).
 __global__ void k_pcg_beta(PcgState* st, const double* partials, int nblocks, double* hist) {
-  if (st->done) return;
+  if (!st->active) return;
   const double s = block_total(partials, nblocks);
   if (threadIdx.x == 0) {
     const double rzn = fmax(s, 0.0);
@@ -442,6 +447,31 @@ __global__ void k_pcg_beta(PcgState* st, const double* partials, int nblocks, do
       st->rz = rzn;
       if (it >= st->it_max) st->done = 1;
     }
+  }
+}
+
+// beta kernel that also drives the device WHILE loop of the fused path.
+__global__ void k_pcg_beta_cond(PcgState* st, const double* partials, int nblocks, double* hist,
+                                cudaGraphConditionalHandle h) {
+  if (!st->active) {
+    if (threadIdx.x == 0) cudaGraphSetConditional(h, 0u);
+    return;
+  }
+  const double s = block_total(partials, nblocks);
+  if (threadIdx.x == 0) {
+    const double rzn = fmax(s, 0.0);
+    const int it = st->it + 1;
+    st->it = it;
+    hist[it] = sqrt(rzn);
+    if (sqrt(rzn) <= st->eta * st->norm0) {
+      st->converged = 1;
+      st->done = 1;
+    } else {
+      st->beta = rzn / st->rz;
+      st->rz = rzn;
+      if (it >= st->it_max) st->done = 1;
+    }
+    cudaGraphSetConditional(h, st->done ? 0u : 1u);
   }
 }
 
@@ -588,6 +618,11 @@ void launch_update_xr(double* x, double* r, const double* p, const double* ap, i
 }
 void launch_pcg_beta(PcgState* st, const double* partials, double* hist, cudaStream_t s) {
   k_pcg_beta<<<1, 1024, 0, s>>>(st, partials, kRedBlocks, hist);
+  HB_CUDA(cudaGetLastError());
+}
+void launch_pcg_beta_cond(PcgState* st, const double* partials, double* hist, cudaGraphConditionalHandle h,
+                          cudaStream_t s) {
+  k_pcg_beta_cond<<<1, 1024, 0, s>>>(st, partials, kRedBlocks, hist, h);
   HB_CUDA(cudaGetLastError());
 }
 void launch_update_p(double* p, const double* z, int64_t n, const PcgState* st, cudaStream_t s) {

@@ -82,6 +82,23 @@ struct SpecParams {
 };
 void launch_spectral(const SpecParams& p, double2* spec, const PcgState* st, double* partials,
                      cudaStream_t s);
+
+// Fused three-pass preconditioner (fftfused.cu): 3-D grids with square
+// 128^2 / 256^2 planes. T has the cuFFT D2Z layout [c][n0][n1][n2/2+1].
+struct FusedFft {
+  int n0, np_plane, c;
+  int64_t np;                 // pixels per component
+  double2* T;
+  const double2* tw_plane;    // W_{n1} table
+  const double2* tw0;         // W_{n0} table
+};
+bool fused_fft_eligible(const Grid& g);
+void fused_forward(const FusedFft& f, const SpecParams& sp, double* r, const double* ap, const PcgState* st,
+                   double* partials, cudaStream_t s, int which = 3);
+void fused_inverse(const FusedFft& f, double* p, double* x, double* z, const PcgState* st, int init,
+                   cudaStream_t s);
+void launch_pcg_beta_cond(PcgState* st, const double* partials, double* hist, cudaGraphConditionalHandle h,
+                          cudaStream_t s);
 void launch_symbol_check(const SpecParams& p, double* partials, cudaStream_t s);
 void launch_symbol_dump(const SpecParams& p, double2* blocks, cudaStream_t s);
 
