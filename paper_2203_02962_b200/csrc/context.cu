@@ -102,6 +102,7 @@ struct homfe_ctx {
   bool fused = false;
   FusedFft ff{};
   double2* d_tw = nullptr;          // W_{n1} then W_{n0}
+  double2* d_spec2 = nullptr;       // second spectrum buffer of the fused passes
   // reference
   SpecParams spp{};
   bool have_ref = false;
@@ -199,6 +200,37 @@ void set_reference(homfe_ctx* c, const double* cref) {
       for (int l = 0; l < d; ++l) p.A[j * d + l] = cref[l * d + j];
   } else {
     mandel_to_tensor(cref, d, p.A);
+  }
+  // isotropic reference: closed-form symbol (spectral.cuh)
+  {
+    p.iso = 0;
+    auto C = [&](int i, int j) { return cref[j * m + i]; };
+    if (c->g.c == 1) {
+      bool ok = true;
+      for (int i = 0; i < d; ++i)
+        for (int j = 0; j < d; ++j)
+          if (C(i, j) != (i == j ? C(0, 0) : 0.0)) ok = false;
+      if (ok) {
+        p.iso = 1;
+        p.mu = C(0, 0);
+      }
+    } else {
+      const double lam = C(0, 1), twomu = m == 6 ? C(3, 3) : C(2, 2);
+      const double tol = 8e-16 * (std::fabs(lam) + std::fabs(twomu));
+      bool ok = true;
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+          const bool nn = i < d && j < d;
+          const double want = nn ? (i == j ? lam + twomu : lam) : (i == j ? twomu : 0.0);
+          if (std::fabs(C(i, j) - want) > tol) ok = false;
+        }
+      if (ok) {
+        p.iso = 1;
+        p.lam = lam;
+        p.mu = 0.5 * twomu;
+      }
+    }
+    if (const char* e = std::getenv("HOMFE_ISO_SYMBOL")) if (e[0] == '0') p.iso = 0;
   }
   c->c_ref.assign(cref, cref + m * m);
   destroy_graphs(c);  // spectral kernel nodes hold the symbol parameters by value
@@ -696,7 +728,11 @@ int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out) {
       ctx->d_ap = dalloc<double>(nv);
       ctx->d_z = dalloc<double>(nv);
       ctx->d_u = dalloc<double>(nv);
-      ctx->d_spec = dalloc<double2>((size_t)c * ctx->nf);
+      // spectrum scratch: cuFFT layout, or the tile-major layout of the fused
+      // passes (16-column blocks, fftfused.cu) when that is larger
+      const int64_t nb8 = ((int64_t)(g.n2 / 2 + 1) + 15) / 16 * 16;
+      const int64_t fused_sz = d == 3 ? (int64_t)c * g.n0 * g.n1 * nb8 : 0;
+      ctx->d_spec = dalloc<double2>(std::max<int64_t>((int64_t)c * ctx->nf, fused_sz));
       ctx->d_phase = dalloc<uint8_t>(g.np);
       ctx->d_partials = dalloc<double>((size_t)kRedBlocks * 8);
       ctx->d_scal = dalloc<double>(64);
@@ -766,9 +802,12 @@ int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out) {
         ctx->ff.c = c;
         ctx->ff.np = g.np;
         ctx->ff.T = ctx->d_spec;
+        ctx->d_spec2 = dalloc<double2>((size_t)c * g.n0 * g.n1 * (((g.n2 / 2 + 1) + 15) / 16 * 16));
+        ctx->ff.T2 = ctx->d_spec2;
         ctx->ff.tw_plane = ctx->d_tw;
         ctx->ff.tw0 = ctx->d_tw + n1;
         ctx->fused = true;
+        if (const char* dbg = std::getenv("HOMFE_FFT_DBG")) ctx->ff.dbg = std::atoi(dbg);
       }
     } catch (...) {
       homfe_gpu_destroy(ctx);
@@ -792,6 +831,7 @@ int homfe_gpu_destroy(homfe_ctx* c) {
     if (t) cudaFree(t);
   if (c->d_spec) cudaFree(c->d_spec);
   if (c->d_tw) cudaFree(c->d_tw);
+  if (c->d_spec2) cudaFree(c->d_spec2);
   if (c->d_phase) cudaFree(c->d_phase);
   if (c->d_st) cudaFree(c->d_st);
   if (c->h_st) cudaFreeHost(c->h_st);

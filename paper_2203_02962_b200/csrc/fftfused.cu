@@ -47,18 +47,39 @@ struct PlaneArgs {
   int64_t np;          // pixels per component
   double* r;           // pass 1 input (updated in PCG mode)
   const double* ap;    // pass 1, PCG mode
-  double2* T;          // [c][n0][NP][NP/2+1] half spectrum (no axis-0 FFT)
+  double2* T;          // pass 1 -> 2, tile-major (t_index)
+  double2* T2;         // pass 2 -> 3, plane-major (t2_index)
   double* p;           // pass 3
   double* x;           // pass 3, PCG mode
   double* z;           // pass 3, z mode
   const double2* tw;   // W_NP table
   const PcgState* st;  // PCG mode
   int mode;
+  int dbg;             // profiling only: bit mask of skipped phases
 };
 
 template <int NP>
 constexpr int tpf() {
   return NP / 16;
+}
+
+// Intermediate spectrum layout (tile-major, 16 columns per 256-byte chunk):
+//   T[comp][k1][k2 / 16][i0][k2 % 16]
+// a pass-1/3 CTA (one plane i0, 16 columns) moves one 256-byte chunk per k1;
+// a pass-2 pencil block (all i0 of 16 columns) is one contiguous 64 KB tile.
+constexpr int kTB = 16;
+__host__ __device__ constexpr int t_blocks(int np_plane) { return (np_plane / 2 + 1 + kTB - 1) / kTB; }
+__device__ __forceinline__ int64_t t_index(int comp, int k1, int k2, int i0, int n0, int n1) {
+  const int nb = t_blocks(n1);
+  return (((int64_t)comp * n1 + k1) * nb + (k2 / kTB)) * ((int64_t)n0 * kTB) + (int64_t)i0 * kTB + (k2 % kTB);
+}
+// Pass-2 output / pass-3 input: plane-major with a 16-aligned row pitch,
+//   T2[comp][i0][k1][k2]  (pitch nb * 16), so pass 3 reads its plane
+// contiguously; the scattered side of both transposes is a write (merged in
+// the write-back L2).
+__device__ __forceinline__ int64_t t2_index(int comp, int k1, int k2, int i0, int n0, int n1) {
+  const int pitch = t_blocks(n1) * kTB;
+  return (((int64_t)comp * n0 + i0) * n1 + k1) * pitch + k2;
 }
 
 // Plane kernels: one cluster of CL = NP/32 CTAs per (component, plane), each
@@ -130,7 +151,7 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
   }
   __syncthreads();
   // row r2c: group g transforms the row pair (2g, 2g+1) in place
-  {
+  if (!(a.dbg & 1)) {
     double2* buf = rows + (2 * g) * P;
     const double* xa = reinterpret_cast<const double*>(rows + (2 * g) * P);
     const double* xb = reinterpret_cast<const double*>(rows + (2 * g + 1) * P);
@@ -162,26 +183,37 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
     }
   }
   cluster.sync();
-  // gather this CTA's 16 column slots over DSMEM straight into registers
-  const int slot = rank * 16 + g;
+  // gather this CTA's 16 column slots over DSMEM: warp w reads the rows of
+  // CTA w, each half-warp one row's 16 contiguous columns (256 B)
+  const int lane = tid & 31, warp = tid >> 5;
+  const int jc = lane & 15, yo = lane >> 4;
+  constexpr int NW = NP / 32;  // warps per CTA == CTAs per cluster
+  static_assert(NW == CL, "one warp per remote CTA");
   double2 v[16];
+  {
+    const double2* src = (a.dbg & 2) ? rows : cluster.map_shared_rank(rows, warp);
+    const int col = rank * 16 + jc;
 #pragma unroll
-  for (int n2 = 0; n2 < 16; ++n2) {
-    const int y = t + TPF * n2;
-    const double2* src = cluster.map_shared_rank(rows, y >> 5) + (y & 31) * P;
-    if (slot == 0) v[n2] = make_double2(src[0].x, src[NP / 2].x);
-    else v[n2] = src[slot];
+    for (int i = 0; i < 16; ++i) {
+      const double2* row = src + (2 * i + yo) * P;
+      if (col == 0) v[i] = make_double2(row[0].x, row[NP / 2].x);
+      else v[i] = row[col];
+    }
   }
   cluster.sync();  // every remote read done: local rows become column buffers
-  double2* cbuf = rows + g * (NP + 1);
-  fft::fft4step_regs<NP, false>(v, cbuf, t, tws);
+  // transpose into padded column buffers: slot jc, position y = 32 warp + 2 i + yo
+#pragma unroll
+  for (int i = 0; i < 16; ++i) rows[jc * (NP + 1) + 32 * warp + 2 * i + yo] = v[i];
   __syncthreads();
-  double2* Tp = a.T + ((int64_t)comp * a.n0 + i0) * NP * P;
+  double2* cbuf = rows + g * (NP + 1);
+  if (!(a.dbg & 4)) fft::fft4step<NP, false>(cbuf, t, tws);
+  __syncthreads();
+  if (a.dbg & 8) return;
   const int first = rank == 0 ? 1 : 0;
   const int ncol = 16 - first;
   for (int idx = tid; idx < ncol * NP; idx += NP) {
     const int k1 = idx / ncol, j = idx % ncol + first;
-    Tp[(int64_t)k1 * P + rank * 16 + j] = rows[j * (NP + 1) + k1];
+    a.T[t_index(comp, k1, rank * 16 + j, i0, a.n0, NP)] = rows[j * (NP + 1) + k1];
   }
   if (rank == 0 && g == 0) {
     // split the paired real columns k2 = 0 and k2 = NP/2
@@ -190,8 +222,8 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
       const int k = t + i * TPF;
       const double2 zk = cbuf[k], zm = conj(cbuf[(NP - k) % NP]);
       const double2 s = cadd(zk, zm), d = csub(zk, zm);
-      Tp[(int64_t)k * P] = make_double2(0.5 * s.x, 0.5 * s.y);
-      Tp[(int64_t)k * P + NP / 2] = make_double2(0.5 * d.y, -0.5 * d.x);
+      a.T[t_index(comp, k, 0, i0, a.n0, NP)] = make_double2(0.5 * s.x, 0.5 * s.y);
+      a.T[t_index(comp, k, NP / 2, i0, a.n0, NP)] = make_double2(0.5 * d.y, -0.5 * d.x);
     }
   }
 }
@@ -213,36 +245,48 @@ __global__ void __launch_bounds__(NP, 2) k_plane_inv(const PlaneArgs a) {
   const int comp = cid / a.n0, i0 = cid % a.n0;
   const int tid = threadIdx.x, g = tid / TPF, t = tid % TPF;
   for (int i = tid; i < NP; i += NP) tws[i] = a.tw[i];
-  const int slot = rank * 16 + g;
-  const double2* Tp = a.T + ((int64_t)comp * a.n0 + i0) * NP * P;
-  // column slot inputs k1 = t + TPF n2 (neighbouring groups share sectors)
-  double2 v[16];
+  // coalesced column loads: warp w takes k1 rows [32w, 32w+32), each
+  // half-warp one row's 16 contiguous columns; transposed into padded buffers
+  const int lane = tid & 31, warp = tid >> 5;
+  const int jc = lane & 15, yo = lane >> 4;
+  {
+    const int col = rank * 16 + jc;
+    double2 v[16];
 #pragma unroll
-  for (int n2 = 0; n2 < 16; ++n2) {
-    const int k = t + TPF * n2;
-    if (slot == 0) {
-      const double2 A = Tp[(int64_t)k * P], B = Tp[(int64_t)k * P + NP / 2];
-      v[n2] = make_double2(A.x - B.y, A.y + B.x);  // A + i B
-    } else {
-      v[n2] = Tp[(int64_t)k * P + slot];
+    for (int i = 0; i < 16; ++i) {
+      const int k = 32 * warp + 2 * i + yo;
+      if (col == 0) {
+        const double2 A = a.T2[t2_index(comp, k, 0, i0, a.n0, NP)];
+        const double2 B = a.T2[t2_index(comp, k, NP / 2, i0, a.n0, NP)];
+        v[i] = make_double2(A.x - B.y, A.y + B.x);  // A + i B
+      } else {
+        v[i] = a.T2[t2_index(comp, k, col, i0, a.n0, NP)];
+      }
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) rows[jc * (NP + 1) + 32 * warp + 2 * i + yo] = v[i];
   }
   __syncthreads();
   double2* cbuf = rows + g * (NP + 1);
-  fft::fft4step_regs<NP, true>(v, cbuf, t, tws);
+  fft::fft4step<NP, true>(cbuf, t, tws);
+  __syncthreads();
+  // read back transposed: warp w takes rows [32w, 32w+32) of the 16 slots
   double2 w[16];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) w[i] = cbuf[t + TPF * i];
+  for (int i = 0; i < 16; ++i) w[i] = rows[jc * (NP + 1) + 32 * warp + 2 * i + yo];
   cluster.sync();  // all column results in registers: regions become row storage
+  {
+    double2* dst = cluster.map_shared_rank(rows, warp);
+    const int col = rank * 16 + jc;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int y = t + TPF * i;
-    double2* dst = cluster.map_shared_rank(rows, y >> 5) + (y & 31) * P;
-    if (slot == 0) {
-      dst[0] = make_double2(w[i].x, 0.0);
-      dst[NP / 2] = make_double2(w[i].y, 0.0);
-    } else {
-      dst[slot] = w[i];
+    for (int i = 0; i < 16; ++i) {
+      double2* row = dst + (2 * i + yo) * P;
+      if (col == 0) {
+        row[0] = make_double2(w[i].x, 0.0);
+        row[NP / 2] = make_double2(w[i].y, 0.0);
+      } else {
+        row[col] = w[i];
+      }
     }
   }
   cluster.sync();
@@ -306,68 +350,105 @@ struct PencilArgs {
   int P;                   // NP/2 + 1
   int ntk;                 // k2 tiles per k1
   double2* T;
-  const double2* tw;       // W_N0 table
+  double2* T2;
+  const double2* tw;       // W_N0 four-step table
   const PcgState* st;      // nullable
   double* partials;        // nullable (Parseval r.z)
   int nred;
+  int dbg;
 };
 
-constexpr int kBK = 8;
+template <int C>
+constexpr int pencil_bk() {
+  return C == 3 ? 4 : 16;
+}
 
+// One transform group (TPF threads) per pencil (component, column): the
+// step-1 inputs i0 = t + TPF n2 are loaded straight into registers (adjacent
+// columns of neighbouring groups share 32-byte sectors), transformed, solved
+// per frequency with all C components, inverse transformed and stored.
 template <int N0, int C>
-__global__ void __launch_bounds__(kThreads, 2) k_pencil(const __grid_constant__ SpecParams sp, const PencilArgs a) {
+__global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), 2)
+    k_pencil(const __grid_constant__ SpecParams sp, const PencilArgs a) {
   constexpr int TPF = tpf<N0>();
-  constexpr int G = kThreads / TPF;
-  constexpr int NPC = C * kBK;  // pencils per tile
-  static_assert(NPC % (32 / TPF > 0 ? 32 / TPF : 1) == 0, "pencil count must fill warps");
+  constexpr int BK = pencil_bk<C>();
+  constexpr int NT = C * BK * TPF;
   if (a.st && !a.st->active) return;
   extern __shared__ double2 sm[];
-  constexpr int LD = N0 + 1;       // padded pencil stride (conflict-free transposes)
-  double2* buf = sm;               // [C][kBK][LD]
-  double2* tws = buf + NPC * LD;   // N0
+  double2* buf = sm;              // [C][BK][N0]
+  double2* tws = buf + C * BK * N0;
   const int tid = threadIdx.x, g = tid / TPF, t = tid % TPF;
-  for (int i = tid; i < N0; i += kThreads) tws[i] = a.tw[i];
+  const int j = g % BK, comp = g / BK;
+  for (int i = tid; i < N0; i += NT) tws[i] = a.tw[i];
   const int P = a.P;
-  const int64_t cstride = (int64_t)a.n0 * a.n1 * P;
+  double2* pb = buf + g * N0;
+  // per-column symbol factors (hex, k0-independent parts) and the axis-0 table
+  __shared__ double colf[BK][6];
+  __shared__ double3 ax0[N0];
+  for (int i = tid; i < N0; i += NT) {
+    const double4 tv = sp.tab[0][i];
+    ax0[i] = make_double3(tv.x, tv.z, 2.0 - (4.0 / 3.0) * tv.z * tv.z);  // sin, sin(t/2), S2
+  }
   double rz = 0.0;
   const int ntiles = a.n1 * a.ntk;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int k1 = tile / a.ntk, c0 = (tile % a.ntk) * kBK;
-    const int nc = min(kBK, P - c0);
-    __syncthreads();
-#pragma unroll 8
-    for (int idx = tid; idx < C * N0 * kBK; idx += kThreads) {
-      const int j = idx % kBK, i0 = (idx / kBK) % N0, comp = idx / (kBK * N0);
-      double2 v = make_double2(0.0, 0.0);
-      if (j < nc) v = a.T[comp * cstride + ((int64_t)i0 * a.n1 + k1) * P + c0 + j];
-      buf[(comp * kBK + j) * LD + i0] = v;
+    const int k1 = tile / a.ntk, c0 = (tile % a.ntk) * BK;
+    const bool live = c0 + j < P;
+    const double2* src = a.T + t_index(comp, k1, c0 + j, 0, a.n0, a.n1);
+    double2 v[16];
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2)
+      v[n2] = (live && !(a.dbg & 64)) ? src[(t + TPF * n2) * kTB] : make_double2(0.0, 0.0);
+    __syncthreads();  // tws ready / previous tile's buffers free
+    if (sp.kind == 3 && tid < BK) {
+      // M(k0) = diag(cf0 sh0^2, cf1 S2_0, cf2 S2_0) + offdiag(cf3 sn0, cf4 sn0, cf5 S2_0)
+      const int k2 = min(c0 + tid, P - 1);
+      const double4 t1 = sp.tab[1][k1], t2 = sp.tab[2][k2];
+      const double S21 = 2.0 - (4.0 / 3.0) * t1.z * t1.z, S22 = 2.0 - (4.0 / 3.0) * t2.z * t2.z;
+      const double w = sp.w, h0 = sp.h[0], h1 = sp.h[1], h2 = sp.h[2];
+      colf[tid][0] = 8.0 * w / (h0 * h0) * S21 * S22;
+      colf[tid][1] = 8.0 * w * t1.z * t1.z / (h1 * h1) * S22;
+      colf[tid][2] = 8.0 * w * t2.z * t2.z / (h2 * h2) * S21;
+      colf[tid][3] = 4.0 * w * t1.x / (h0 * h1) * S22;
+      colf[tid][4] = 4.0 * w * t2.x / (h0 * h2) * S21;
+      colf[tid][5] = 4.0 * w * t1.x * t2.x / (h1 * h2);
     }
+    if (!(a.dbg & 32)) fft::fft4step_regs<N0, false>(v, pb, t, tws);
     __syncthreads();
-    for (int pc = g; pc < NPC; pc += G) fft::fft<N0, false>(buf + pc * LD, t, tws);
-    __syncthreads();
-    for (int e = tid; e < N0 * kBK; e += kThreads) {
-      const int j = e / N0, k0 = e % N0;
-      if (j >= nc) continue;
-      const int k2 = c0 + j;
+    for (int e = tid; e < N0 * BK && !(a.dbg & 16); e += NT) {
+      const int jj = e / N0, k0 = e % N0;
+      const int k2 = c0 + jj;
+      if (k2 >= P) continue;
       double2 r[C], z[C];
 #pragma unroll
-      for (int i = 0; i < C; ++i) r[i] = buf[(i * kBK + j) * LD + k0];
+      for (int i = 0; i < C; ++i) r[i] = buf[(i * BK + jj) * N0 + k0];
       if (k0 == 0 && k1 == 0 && k2 == 0) {
 #pragma unroll
         for (int i = 0; i < C; ++i) z[i] = make_double2(0.0, 0.0);
       } else {
-        const int f[3] = {k0, k1, k2};
         double M[3][3], K[3][3], I[3][3];
-        spec::gram<3>(sp, f, M);
+        if (sp.kind == 3) {
+          const double3 t0 = ax0[k0];
+          const double* cf = colf[jj];
+          M[0][0] = cf[0] * t0.y * t0.y;
+          M[1][1] = cf[1] * t0.z;
+          M[2][2] = cf[2] * t0.z;
+          M[0][1] = M[1][0] = cf[3] * t0.x;
+          M[0][2] = M[2][0] = cf[4] * t0.x;
+          M[1][2] = M[2][1] = cf[5] * t0.z;
+        } else {
+          const int f[3] = {k0, k1, k2};
+          spec::gram<3>(sp, f, M);
+        }
         spec::symbol<3, C>(sp, M, K);
         spec::sym_inverse<C>(K, I);
 #pragma unroll
         for (int i = 0; i < C; ++i) {
           double zr = 0.0, zi = 0.0;
 #pragma unroll
-          for (int jj = 0; jj < C; ++jj) {
-            zr = fma(I[i][jj], r[jj].x, zr);
-            zi = fma(I[i][jj], r[jj].y, zi);
+          for (int jj2 = 0; jj2 < C; ++jj2) {
+            zr = fma(I[i][jj2], r[jj2].x, zr);
+            zi = fma(I[i][jj2], r[jj2].y, zi);
           }
           z[i] = make_double2(zr * sp.inv_np, zi * sp.inv_np);
         }
@@ -378,31 +459,32 @@ __global__ void __launch_bounds__(kThreads, 2) k_pencil(const __grid_constant__ 
         rz = fma(wgt, s, rz);
       }
 #pragma unroll
-      for (int i = 0; i < C; ++i) buf[(i * kBK + j) * LD + k0] = z[i];
+      for (int i = 0; i < C; ++i) buf[(i * BK + jj) * N0 + k0] = z[i];
     }
     __syncthreads();
-    for (int pc = g; pc < NPC; pc += G) fft::fft<N0, true>(buf + pc * LD, t, tws);
-    __syncthreads();
-    for (int idx = tid; idx < C * N0 * kBK; idx += kThreads) {
-      const int j = idx % kBK, i0 = (idx / kBK) % N0, comp = idx / (kBK * N0);
-      if (j < nc) a.T[comp * cstride + ((int64_t)i0 * a.n1 + k1) * P + c0 + j] = buf[(comp * kBK + j) * LD + i0];
+    if (!(a.dbg & 32)) fft::fft4step<N0, true>(pb, t, tws);
+    if (live && !(a.dbg & 64)) {
+#pragma unroll
+      for (int n = 0; n < 16; ++n) a.T2[t2_index(comp, k1, c0 + j, t + TPF * n, a.n0, a.n1)] = pb[t + TPF * n];
     }
   }
   if (a.partials) {
     __shared__ double red[32];
     const int lane = tid & 31, warp = tid >> 5;
+    constexpr int NWP = (NT + 31) / 32;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) rz += __shfl_xor_sync(0xffffffffu, rz, o);
+    __syncthreads();
     if (lane == 0) red[warp] = rz;
     __syncthreads();
     if (warp == 0) {
-      double s2 = lane < (kThreads / 32) ? red[lane] : 0.0;
+      double s2 = lane < NWP ? red[lane] : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
       if (lane == 0) a.partials[blockIdx.x] = s2;
     }
     if (blockIdx.x == 0)
-      for (int i = gridDim.x + tid; i < a.nred; i += kThreads) a.partials[i] = 0.0;
+      for (int i = gridDim.x + tid; i < a.nred; i += NT) a.partials[i] = 0.0;
   }
 }
 
@@ -433,29 +515,34 @@ void run_planes(const FusedFft& f, bool inverse, const PlaneArgs& a, cudaStream_
   else launch_cluster(k_plane_fwd<NP>, grid, NP, CL, smem, s, a);
 }
 
-template <int N0>
-void run_pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st, double* partials, cudaStream_t s) {
+template <int N0, int C>
+void run_pencils_c(const FusedFft& f, const SpecParams& sp, const PcgState* st, double* partials, cudaStream_t s) {
+  constexpr int BK = pencil_bk<C>();
+  constexpr int NT = C * BK * (N0 / 16);
   PencilArgs a;
   a.n0 = f.n0;
   a.n1 = f.np_plane;
   a.P = f.np_plane / 2 + 1;
-  a.ntk = (a.P + kBK - 1) / kBK;
+  a.ntk = (a.P + BK - 1) / BK;
   a.T = f.T;
+  a.T2 = f.T2;
   a.tw = f.tw0;
   a.st = st;
   a.partials = partials;
   a.nred = kRedBlocks;
+  a.dbg = f.dbg;
   const int ntiles = a.n1 * a.ntk;
   const int grid = ntiles < kRedBlocks ? ntiles : kRedBlocks;
-  const size_t smem = sizeof(double2) * ((size_t)f.c * kBK * (N0 + 1) + N0);
-  if (f.c == 3) {
-    HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_pencil<N0, 3><<<grid, kThreads, smem, s>>>(sp, a);
-  } else {
-    HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_pencil<N0, 1><<<grid, kThreads, smem, s>>>(sp, a);
-  }
+  const size_t smem = sizeof(double2) * ((size_t)C * BK * N0 + N0);
+  HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_pencil<N0, C><<<grid, NT, smem, s>>>(sp, a);
   HB_CUDA(cudaGetLastError());
+}
+
+template <int N0>
+void run_pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st, double* partials, cudaStream_t s) {
+  if (f.c == 3) run_pencils_c<N0, 3>(f, sp, st, partials, s);
+  else run_pencils_c<N0, 1>(f, sp, st, partials, s);
 }
 
 }  // namespace
@@ -463,7 +550,7 @@ void run_pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st, do
 bool fused_fft_eligible(const Grid& g) {
   if (g.d != 3 || (g.c != 1 && g.c != 3)) return false;
   if (g.n1 != g.n2 || (g.n2 != 128 && g.n2 != 256)) return false;
-  if (g.n0 != 64 && g.n0 != 128 && g.n0 != 256 && g.n0 != 512) return false;
+  if (g.n0 != 64 && g.n0 != 128 && g.n0 != 256) return false;
   return true;
 }
 
@@ -476,8 +563,7 @@ static void pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st,
   switch (f.n0) {
     case 64: run_pencils<64>(f, sp, st, partials, s); break;
     case 128: run_pencils<128>(f, sp, st, partials, s); break;
-    case 256: run_pencils<256>(f, sp, st, partials, s); break;
-    default: run_pencils<512>(f, sp, st, partials, s); break;
+    default: run_pencils<256>(f, sp, st, partials, s); break;
   }
 }
 
@@ -490,9 +576,11 @@ void fused_forward(const FusedFft& f, const SpecParams& sp, double* r, const dou
   a.r = r;
   a.ap = ap;
   a.T = f.T;
+  a.T2 = f.T2;
   a.tw = f.tw_plane;
   a.st = st;
   a.mode = ap ? kModePcg : kModePlain;
+  a.dbg = f.dbg;
   if (which & 1) planes(f, false, a, s);
   if (which & 2) pencils(f, sp, st, partials, s);
 }
@@ -504,6 +592,7 @@ void fused_inverse(const FusedFft& f, double* p, double* x, double* z, const Pcg
   a.n0 = f.n0;
   a.np = f.np;
   a.T = f.T;
+  a.T2 = f.T2;
   a.tw = f.tw_plane;
   a.p = p;
   a.x = x;

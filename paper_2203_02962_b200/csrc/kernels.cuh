@@ -78,6 +78,8 @@ struct SpecParams {
   double w, inv_np;
   double h[3];
   double A[81];         // c = d: tensor A_ijkl; c = 1: C_ref (d x d) in A[0..d*d)
+  int iso;              // C_ref isotropic: K_hat = (lam + mu) M + mu tr(M) I (c = d) / kappa tr(M)
+  double lam, mu;       // isotropic reference moduli (mu = kappa for c = 1)
   const double4* tab[3];  // per axis: (sin, cos, sin(t/2), cos(t/2))
 };
 void launch_spectral(const SpecParams& p, double2* spec, const PcgState* st, double* partials,
@@ -88,9 +90,11 @@ void launch_spectral(const SpecParams& p, double2* spec, const PcgState* st, dou
 struct FusedFft {
   int n0, np_plane, c;
   int64_t np;                 // pixels per component
-  double2* T;
+  double2* T;                 // tile-major pass-1 output
+  double2* T2;                // plane-major pass-2 output
   const double2* tw_plane;    // W_{n1} table
   const double2* tw0;         // W_{n0} table
+  int dbg;                    // profiling: skipped phases (HOMFE_FFT_DBG)
 };
 bool fused_fft_eligible(const Grid& g);
 void fused_forward(const FusedFft& f, const SpecParams& sp, double* r, const double* ap, const PcgState* st,

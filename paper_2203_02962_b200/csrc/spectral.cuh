@@ -57,6 +57,22 @@ __device__ __forceinline__ void gram(const SpecParams& p, const int (&f)[3], dou
 // K_hat (C x C symmetric) from M and the reference tangent.
 template <int D, int C>
 __device__ __forceinline__ void symbol(const SpecParams& p, const double (&M)[3][3], double (&K)[3][3]) {
+  if (p.iso) {
+    // isotropic C_ref: A_ijkl = lam d_ij d_kl + mu (d_ik d_jl + d_il d_jk)
+    double tr = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) tr += M[j][j];
+    if (C == 1) {
+      K[0][0] = p.mu * tr;
+    } else {
+      const double lm = p.lam + p.mu, mt = p.mu * tr;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int k = 0; k < D; ++k) K[i][k] = lm * M[i][k] + (i == k ? mt : 0.0);
+    }
+    return;
+  }
   if (C == 1) {
     double s = 0.0;
 #pragma unroll

@@ -385,3 +385,21 @@ def test_hex_fast_path_matches_oracle(hb, oracle_mod, dims, c, iso, monkeypatch)
     g2 = hb.Grid(dims, [1.0, 1.0, 1.0], "trilinear-hex")
     slow = hb.apply_operator(g2, tangent, u).ravel()
     assert np.abs(fast - slow).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("dims,stencil,c", [((12, 10), "two-triangles", 2), ((8, 6, 10), "trilinear-hex", 3),
+                                            ((8, 6, 10), "trilinear-hex", 1), ((9, 7), "bilinear-quad", 1)])
+def test_isotropic_symbol_matches_general(hb, oracle_mod, dims, stencil, c, monkeypatch):
+    """Closed-form isotropic K_ref_hat = (lam+mu) M + mu tr(M) I against the
+    general tensor contraction and the oracle's assembled blocks."""
+    d = len(dims)
+    cref = hb.isotropic_stiffness(1.7, 0.9, d) if c > 1 else 2.5 * np.eye(d)
+    g = hb.Grid(dims, [1.0] * d, stencil)
+    iso = hb.assemble_preconditioner(g, cref, c).symbol()
+    monkeypatch.setenv("HOMFE_ISO_SYMBOL", "0")
+    g2 = hb.Grid(dims, [1.0] * d, stencil)
+    gen = hb.assemble_preconditioner(g2, cref, c).symbol()
+    assert np.abs(iso - gen).max() <= 1e-14 * np.abs(gen).max()
+    og = oracle_mod.Grid(dims, [1.0] * d, stencil)
+    ref = oracle_mod.Preconditioner(og, cref, c, invert=False).blocks()
+    assert np.abs(iso - ref).max() < 1e-11 * np.abs(ref).max()
