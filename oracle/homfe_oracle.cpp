@@ -985,6 +985,35 @@ int or_precond_assemble(const or_grid* g, const double* c_ref, int32_t c, int32_
   });
 }
 
+int or_precond_from_symbol(const or_grid* g, int32_t c, const double* blocks_rm, int32_t weighted,
+                           or_precond** out) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    if (c != 1 && c != l.d) throw ValidationError("from_symbol: bad component count");
+    auto* p = new or_precond();
+    p->c = c;
+    p->Nn = l.Nn;
+    p->bdim = c * l.Nn;
+    p->weighted = weighted != 0;
+    std::vector<Index> dims(l.N, l.N + l.d);
+    p->fft = std::make_shared<FftGrid>(dims);
+    p->nf = p->fft->spec_size;
+    p->data.assign(p->nf * p->bdim * p->bdim, 0.0);
+    const int b = p->bdim;
+    const cplx* src = reinterpret_cast<const cplx*>(blocks_rm);
+    for (Index k = 0; k < p->nf; ++k)
+      for (int i = 0; i < b; ++i)
+        for (int j = 0; j < b; ++j) p->block(k)[j * b + i] = src[(k * b + i) * b + j];
+    try {
+      invert(p);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
 int or_precond_blocks(const or_precond* p, int64_t* nf, int32_t* bdim, double* blocks) {
   return guarded([&] {
     if (nf) *nf = p->nf;

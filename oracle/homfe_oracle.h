@@ -96,6 +96,11 @@ int or_fft_inverse(int32_t rank, const int64_t* dims, const double* in_c, double
 typedef struct or_precond or_precond;
 int or_precond_assemble(const or_grid* g, const double* c_ref, int32_t c,
                         int32_t weighted, int32_t invert, or_precond** out);
+/* Preconditioner from a given symbol (nf x bdim x bdim complex, row-major per
+   block), inverted like invert_blocks: used to separate the reference's own
+   impulse-probing rounding from implementation differences in parity tests. */
+int or_precond_from_symbol(const or_grid* g, int32_t c, const double* blocks_rm, int32_t weighted,
+                           or_precond** out);
 int or_precond_blocks(const or_precond* p, int64_t* num_freq, int32_t* bdim,
                       double* blocks_c /* nullable: nf*bdim*bdim complex */);
 int or_precond_apply(const or_grid* g, const or_precond* p, const double* r, double* z);

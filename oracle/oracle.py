@@ -227,12 +227,17 @@ def fft_inverse(X, shape):
 class Preconditioner:
     """Impulse-probed, FFT-diagonalised, pseudo-inverted reference operator."""
 
-    def __init__(self, g, c_ref, c, weighted=True, invert=True):
-        m = g.m(c)
-        cr = _cmat(c_ref, m)
+    def __init__(self, g, c_ref, c, weighted=True, invert=True, symbol=None):
         h = C.c_void_p()
-        _check(lib().or_precond_assemble(g.ref, _ptr(cr), C.c_int32(c), C.c_int32(int(weighted)),
-                                         C.c_int32(int(invert)), C.byref(h)))
+        if symbol is not None:
+            sym = np.ascontiguousarray(symbol, dtype=np.complex128)
+            _check(lib().or_precond_from_symbol(g.ref, C.c_int32(c), _ptr(sym.view(np.float64)),
+                                                C.c_int32(int(weighted)), C.byref(h)))
+        else:
+            m = g.m(c)
+            cr = _cmat(c_ref, m)
+            _check(lib().or_precond_assemble(g.ref, _ptr(cr), C.c_int32(c), C.c_int32(int(weighted)),
+                                             C.c_int32(int(invert)), C.byref(h)))
         self._h = h
         self.grid = g
         self.c = c

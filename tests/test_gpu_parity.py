@@ -277,21 +277,25 @@ def test_newton_matches_oracle(hb, oracle_mod, name, dims, stencil, thermal):
         assert abs(k_g - k_o) <= 1, (name, kw, k_g, k_o)
         assert got["report"]["newton_steps"] == len(ref["steps"])
         if k_g == k_o:
-            # fixed-k parity: 1e-10, or 30x the oracle-vs-oracle noise floor
-            # where the reference's own FFT-probed blocks
-            # (rounding ~1e-14 at low frequency) are amplified by the Krylov
-            # process beyond it
-            floor = _noise_floor(oracle_mod, dims, stencil, thermal, cm, ph, e, kw, k_o)
-            tol = max(1e-10, 30 * floor)
+            # Fixed-k parity: 1e-10 relative, unless the problem itself is more
+            # sensitive. The reference probes K_ref_hat by FFTs of impulse
+            # responses (precond.cpp:44-85), rounding ~eps/theta^2 at low
+            # frequencies; the oracle run with the exact symbol instead
+            # measures how far two valid fp64 implementations drift apart at
+            # this iterate (noise floor). Allow 5x that.
+            x_exact, x_probed = _oracle_exact_and_probed(hb, oracle_mod, dims, stencil, thermal, cm, ph, e, kw, k_o)
+            floor = _rel(x_probed, x_exact)
+            tol = max(1e-10, 5 * floor)
+            assert _rel(got["u"], x_exact) <= tol, (name, kw, floor)
         else:
             tol = 10 * kw["eta_cg"]
         assert _rel(got["u"], ref["u"]) <= tol, (name, kw)
-        assert _rel(got["average_stress"], ref["average_stress"]) <= tol, (name, kw)
+        assert _rel(got["average_stress"], ref["average_stress"]) <= max(tol, 1e-10), (name, kw)
 
 
-def _noise_floor(oracle_mod, dims, stencil, thermal, cm, ph, e, kw, k):
-    """Oracle vs oracle at k iterations with the right-hand side perturbed at
-    the GPU-vs-oracle operator difference (2e-14 relative)."""
+def _oracle_exact_and_probed(hb, oracle_mod, dims, stencil, thermal, cm, ph, e, kw, k):
+    """Oracle PCG at k iterations with (a) the analytic symbol exported by the
+    GPU library and (b) the reference's impulse-probed blocks."""
     og = oracle_mod.Grid(dims, [1.0] * len(dims), stencil)
     c = 1 if thermal else len(dims)
     nq = og.quads_per_pixel
@@ -303,11 +307,13 @@ def _noise_floor(oracle_mod, dims, stencil, thermal, cm, ph, e, kw, k):
         cref = kw["reference_scale"] * np.eye(cm.shape[1])
     else:
         cref = (np.bincount(ph, minlength=len(cm))[:, None, None] * cm).sum(0) / ph.size
-    pre = oracle_mod.Preconditioner(og, cref, c)
-    x0 = oracle_mod.pcg(og, c, cm, ph, pre, b, 0.0, k)["x"]
-    rng = np.random.default_rng(1)
-    x1 = oracle_mod.pcg(og, c, cm, ph, pre, b * (1 + 2e-14 * rng.standard_normal(b.size)), 0.0, k)["x"]
-    return _rel(x1, x0)
+    g = hb.Grid(dims, [1.0] * len(dims), stencil)
+    sym = hb.assemble_preconditioner(g, cref, c).symbol()
+    exact = oracle_mod.Preconditioner(og, None, c, symbol=sym)
+    probed = oracle_mod.Preconditioner(og, cref, c)
+    x_exact = oracle_mod.pcg(og, c, cm, ph, exact, b, 0.0, k)["x"]
+    x_probed = oracle_mod.pcg(og, c, cm, ph, probed, b, 0.0, k)["x"]
+    return x_exact, x_probed
 
 
 def test_uniform_material_no_fluctuation(hb):
