@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libhomfe_gpu.so")
+LIB_PATH = os.environ.get("HOMFE_LIB") or os.path.join(HERE, "_lib", "libhomfe_gpu.so")
 
 OK, VALIDATION, NONCONVERGED, NUMERICAL, DEVICE = 0, 2, 3, 4, 5
 

@@ -31,39 +31,42 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def _compile(src, verbose):
-    obj = os.path.join(OBJ_DIR, os.path.splitext(src)[0] + ".o")
+def _compile(src, verbose, obj_dir=None, defines=()):
+    obj = os.path.join(obj_dir or OBJ_DIR, os.path.splitext(src)[0] + ".o")
     deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + [
         os.path.join(HERE, "..", "include", "homfe_gpu.h")]
     if not _stale(obj, deps):
         return obj, ""
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(verbose=False, force=False):
-    os.makedirs(OBJ_DIR, exist_ok=True)
+def build(verbose=False, force=False, lib=None, defines=()):
+    """Compile and link. `lib`/`defines` build a tuning variant elsewhere."""
+    lib = lib or LIB
+    obj_dir = OBJ_DIR if lib == LIB else os.path.join(os.path.dirname(lib), "obj")
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = [s for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
     if force:
-        for f in os.listdir(OBJ_DIR):
-            os.remove(os.path.join(OBJ_DIR, f))
+        for f in os.listdir(obj_dir):
+            os.remove(os.path.join(obj_dir, f))
     with cf.ThreadPoolExecutor(max_workers=len(srcs)) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose), srcs))
+        results = list(ex.map(lambda s: _compile(s, verbose, obj_dir, defines), srcs))
     objs = [o for o, _ in results]
     if verbose:
         for (_, log), s in zip(results, srcs):
             if log:
                 print(f"--- ptxas {s}\n{log}", file=sys.stderr)
-    if _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcufft",
+    if _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcufft",
                "-Xlinker", f"-rpath,{CUDA}/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -368,7 +368,10 @@ constexpr int pencil_bk() {
 // columns of neighbouring groups share 32-byte sectors), transformed, solved
 // per frequency with all C components, inverse transformed and stored.
 template <int N0, int C>
-__global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), 2)
+#ifndef HB_PENCIL_MINB
+#define HB_PENCIL_MINB 2
+#endif
+__global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB)
     k_pencil(const __grid_constant__ SpecParams sp, const PencilArgs a) {
   constexpr int TPF = tpf<N0>();
   constexpr int BK = pencil_bk<C>();

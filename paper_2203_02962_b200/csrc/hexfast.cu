@@ -33,6 +33,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "kernels.cuh"
@@ -41,8 +43,6 @@ namespace hb {
 
 namespace {
 
-constexpr int kTY = 8;
-constexpr int kTZ = 16;
 
 // Per-phase material table layout (doubles):
 //   ISO:      [3 classes][3] = f*lambda, f*2mu, f*mu   (elastic)
@@ -156,7 +156,7 @@ struct HexArgs {
   int tiles_y, tiles_z;
 };
 
-template <int C, bool ISO>
+template <int C, bool ISO, int kTY, int kTZ>
 __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
   if (a.st && a.st->done) return;
   constexpr int MS = mat_stride<C, ISO>();
@@ -305,9 +305,26 @@ __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
 
 }  // namespace
 
+// Tile (rows y per thread, planes z per tile): a larger tile recomputes
+// fewer warm-up elements ((1 + 1/TY)(1 + 1/TZ)) but yields fewer blocks.
+static void hex_tile(const Grid& g, int& ty, int& tz) {
+  ty = 8;
+  tz = 16;
+  if (const char* e = std::getenv("HOMFE_HEX_TILE")) {
+    int a = 0, b = 0;
+    if (std::sscanf(e, "%dx%d", &a, &b) == 2) {
+      ty = a;
+      tz = b;
+    }
+  }
+  (void)g;
+}
+
 bool hex_fast_eligible(const Grid& g) {
   if (g.d != 3 || g.kind != 3 || (g.c != 1 && g.c != 3)) return false;
-  if (g.n2 % 32 != 0 || g.n2 > 256 || g.n1 % kTY != 0 || g.n0 % kTZ != 0) return false;
+  int ty, tz;
+  hex_tile(g, ty, tz);
+  if (g.n2 % 32 != 0 || g.n2 > 256 || g.n1 % ty != 0 || g.n0 % tz != 0) return false;
   if (g.h[0] != g.h[1] || g.h[1] != g.h[2]) return false;
   return true;
 }
@@ -380,6 +397,8 @@ void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, boo
   a.n0 = g.n0;
   a.n1 = g.n1;
   a.n2 = g.n2;
+  int kTY, kTZ;
+  hex_tile(g, kTY, kTZ);
   a.tiles_y = g.n1 / kTY;
   a.tiles_z = g.n0 / kTZ;
   const int ntiles = a.tiles_y * a.tiles_z;
@@ -388,10 +407,20 @@ void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, boo
   const int ms = iso ? (g.c == 3 ? 9 : 3) : (g.c == 3 ? 108 : 27);
   const size_t smem = sizeof(double) * ((size_t)kTY * g.c * g.n2 + 2 * nw * 4 * g.c + (size_t)ea.n_phases * ms +
                                         (size_t)ea.n_phases * 8 * g.c);
-#define HB_HEX(C, ISO)                                                                              \
+#define HB_HEX_T(C, ISO, TY, TZ)                                                                    \
   do {                                                                                              \
-    HB_CUDA(cudaFuncSetAttribute(k_hex_fast<C, ISO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_hex_fast<C, ISO><<<grid, g.n2, smem, s>>>(a);                                                 \
+    HB_CUDA(cudaFuncSetAttribute(k_hex_fast<C, ISO, TY, TZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_hex_fast<C, ISO, TY, TZ><<<grid, g.n2, smem, s>>>(a);                                         \
+  } while (0)
+#define HB_HEX(C, ISO)                                                        \
+  do {                                                                        \
+    if (kTY == 8 && kTZ == 16) HB_HEX_T(C, ISO, 8, 16);                       \
+    else if (kTY == 16 && kTZ == 16) HB_HEX_T(C, ISO, 16, 16);                \
+    else if (kTY == 8 && kTZ == 32) HB_HEX_T(C, ISO, 8, 32);                  \
+    else if (kTY == 16 && kTZ == 8) HB_HEX_T(C, ISO, 16, 8);                  \
+    else if (kTY == 4 && kTZ == 32) HB_HEX_T(C, ISO, 4, 32);                  \
+    else if (kTY == 32 && kTZ == 8) HB_HEX_T(C, ISO, 32, 8);                  \
+    else throw ValidationError("hexfast: unsupported tile");                  \
   } while (0)
   if (g.c == 3) {
     if (iso) HB_HEX(3, true);
@@ -401,6 +430,7 @@ void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, boo
     else HB_HEX(1, false);
   }
 #undef HB_HEX
+#undef HB_HEX_T
   HB_CUDA(cudaGetLastError());
 }
 
