@@ -409,3 +409,22 @@ def test_isotropic_symbol_matches_general(hb, oracle_mod, dims, stencil, c, monk
     og = oracle_mod.Grid(dims, [1.0] * d, stencil)
     ref = oracle_mod.Preconditioner(og, cref, c, invert=False).blocks()
     assert np.abs(iso - ref).max() < 1e-11 * np.abs(ref).max()
+
+
+def test_cpp_drop_in_example_runs(hb):
+    """examples/solve_c1.cpp through include/homfe/gpu.hpp: run_load_program,
+    warm starts, ValidationError mapping."""
+    import os
+    import subprocess
+    import tempfile
+    from paper_2203_02962_b200 import _native
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.dirname(_native.LIB_PATH)
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "solve_c1")
+        subprocess.run(["g++", "-std=c++17", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "examples", "solve_c1.cpp"), "-o", exe, "-L", lib_dir, "-lhomfe_gpu",
+                        f"-Wl,-rpath,{lib_dir}"], check=True)
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("converged 1") == 2 and "ValidationError" in r.stdout

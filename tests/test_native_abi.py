@@ -86,3 +86,16 @@ def test_config_inputs_are_deterministic():
     assert 0.30 <= c2.mean() < 0.33
     grf = inputs.grf_threshold((32, 32, 32), 4.0, 11)
     assert grf.mean() == pytest.approx(0.5, abs=1e-6)
+
+
+def test_cpp_shim_compiles_and_links(tmp_path):
+    """include/homfe/gpu.hpp (the reference-facing C++ API) builds against the
+    C ABI library with g++ alone."""
+    import subprocess
+    from paper_2203_02962_b200 import _native
+    lib_dir = os.path.dirname(_native.LIB_PATH)
+    out = tmp_path / "solve_c1"
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "solve_c1.cpp"), "-o", str(out), "-L", lib_dir, "-lhomfe_gpu",
+                    f"-Wl,-rpath,{lib_dir}"], check=True)
+    assert out.exists()
