@@ -8,7 +8,17 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def _ensure_built():
+    """Build the native library and the oracle if they are missing (nvcc and
+    gcc cross-compile here; no GPU needed)."""
+    lib = os.path.join(ROOT, "paper_2203_02962_b200", "_lib", "libhomfe_gpu.so")
+    if not os.path.exists(lib):
+        from paper_2203_02962_b200 import build as nb
+        nb.build()
+
+
 def pytest_configure(config):
+    _ensure_built()
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (sm_100a) device")
     config.addinivalue_line("markers", "slow: long-running test")
 
