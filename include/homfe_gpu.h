@@ -102,6 +102,19 @@ const char* homfe_gpu_last_error(void);
 int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out);
 int homfe_gpu_destroy(homfe_ctx* ctx);
 
+/* Slab decomposition along axis 0 (the reference is
+   single-process, SPEC.md:204 sketches only a partition contract). `desc` is
+   the GLOBAL grid; rank r of `world` owns planes [r n0/world, (r+1) n0/world).
+   One process per GPU; `nccl_id` (128 bytes from homfe_nccl_unique_id on
+   rank 0, broadcast by the caller) initialises the NCCL communicator used for
+   halo planes, the FFT transposes and scalar all-reductions. Afterwards every
+   host-buffer entry point (set_material, solve, apply_K, apply_minv, pcg)
+   takes and returns this rank's slab; scalars (<sigma>, iteration counts) are
+   global. 3-d trilinear-hex grids with 128^2 / 256^2 planes. */
+int homfe_nccl_unique_id(void* out128);
+int homfe_gpu_create_dist(const homfe_grid_desc* desc, int32_t rank, int32_t world, const void* nccl_id,
+                          homfe_ctx** out);
+
 /* MaterialMap for linear models (material.hpp:100-118): per-phase m x m
    column-major tangents (conductivity d x d, or Mandel stiffness) and the
    uint8 phase of every pixel. Validates like MaterialMap::validate

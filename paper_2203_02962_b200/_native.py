@@ -70,6 +70,8 @@ def _load():
         "homfe_gpu_sizes": (C.c_int, [vp, P(i64), P(i64), P(i32), P(i64)]),
         "homfe_random_uniform": (C.c_int, [C.c_uint64, i64, d, d, P(d)]),
         "homfe_gpu_kernel_times": (C.c_int, [vp, i32, P(d)]),
+        "homfe_nccl_unique_id": (C.c_int, [vp]),
+        "homfe_gpu_create_dist": (C.c_int, [P(GridDesc), i32, i32, vp, P(vp)]),
         "homfe_random_normal": (C.c_int, [C.c_uint64, i64, P(d)]),
     }
     for name, (res, args) in sig.items():
@@ -86,4 +88,5 @@ EXPORTED = ("homfe_gpu_last_error", "homfe_isotropic_stiffness", "homfe_gpu_crea
             "homfe_gpu_solve_device", "homfe_gpu_apply_K", "homfe_gpu_set_reference", "homfe_gpu_apply_minv",
             "homfe_gpu_reference_blocks", "homfe_gpu_gradient", "homfe_gpu_divergence",
             "homfe_gpu_volume_average", "homfe_gpu_pcg", "homfe_gpu_index_maps", "homfe_gpu_sizes",
-            "homfe_random_uniform", "homfe_random_normal", "homfe_gpu_kernel_times")
+            "homfe_random_uniform", "homfe_random_normal", "homfe_gpu_kernel_times",
+            "homfe_nccl_unique_id", "homfe_gpu_create_dist")

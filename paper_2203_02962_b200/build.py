@@ -61,7 +61,7 @@ def build(verbose=False, force=False, lib=None, defines=()):
             if log:
                 print(f"--- ptxas {s}\n{log}", file=sys.stderr)
     if _stale(lib, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcufft",
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcufft", "-lnccl",
                "-Xlinker", f"-rpath,{CUDA}/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

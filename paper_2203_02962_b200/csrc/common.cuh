@@ -57,6 +57,11 @@ struct Grid {
   int64_t np;   // pixels == nodes (one node type per pixel)
   double h[3];
   double cell_volume;
+  // slab decomposition along axis 0 (dist = 1): n0 / np are the LOCAL plane
+  // and pixel counts of this rank; the global grid has n0g planes.
+  int dist;
+  int n0g, z0, rank, world;
+  int64_t npg;
 };
 
 // PCG scalars resident on the device (solver.cpp:62-94).

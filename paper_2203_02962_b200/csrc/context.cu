@@ -8,6 +8,7 @@
 // on the device until the stopping test of solver.cpp:88-91 fires, so the
 // host never synchronises inside a solve.
 #include <cufft.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <random>
@@ -30,6 +31,12 @@ thread_local std::string g_err;
 struct CufftError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+
+#define HB_NCCL(expr)                                                                   \
+  do {                                                                                  \
+    ncclResult_t _r = (expr);                                                           \
+    if (_r != ncclSuccess) throw CudaError(std::string(#expr) + ": " + ncclGetErrorString(_r)); \
+  } while (0)
 
 #define HB_CUFFT(expr)                                                                  \
   do {                                                                                  \
@@ -121,9 +128,19 @@ struct homfe_ctx {
   double graph_eta = -1.0;
   int graph_itmax = -1;
   bool use_while = true;
+  bool body_eager = false;
   cudaGraphExec_t body_exec = nullptr;  // fallback: one iteration per launch
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   int64_t launches = 0;
+  // slab decomposition (homfe_gpu_create_dist): NCCL communicator, halo planes
+  bool dist = false;
+  ncclComm_t comm = nullptr;
+  double* d_hlo = nullptr;          // plane z0-1 of the vector being stenciled, [c][plane]
+  double* d_hhi = nullptr;          // plane z0+nz
+  uint8_t* d_ph_lo = nullptr;       // phase plane z0-1
+  double* d_red = nullptr;          // globally reduced scalars
+  double2* d_spec_r = nullptr;      // all-to-all receive buffers of the fused passes
+  double2* d_spec2_r = nullptr;
 
   int64_t nvec() const { return (int64_t)g.c * g.np; }
 };
@@ -141,8 +158,57 @@ void destroy_graphs(homfe_ctx* c) {
 
 void sync(homfe_ctx* c) { HB_CUDA(cudaStreamSynchronize(c->stream)); }
 
+// ---- slab-mode exchanges (NCCL over NVLink / NVSwitch) --------------------
+// halo planes of a component-planar vector: my first plane goes to the
+// previous rank (its upper halo), my last plane to the next rank (its lower
+// halo); periodic ring, so world == 1 exchanges with itself.
+void exchange_halo(homfe_ctx* c, const double* v, cudaStream_t s) {
+  const Grid& g = c->g;
+  const int prev = (g.rank - 1 + g.world) % g.world, next = (g.rank + 1) % g.world;
+  const size_t plane = (size_t)g.n1 * g.n2;
+  HB_NCCL(ncclGroupStart());
+  for (int k = 0; k < g.c; ++k) {
+    const double* base = v + (int64_t)k * g.np;
+    HB_NCCL(ncclSend(base, plane, ncclDouble, prev, c->comm, s));
+    HB_NCCL(ncclSend(base + (int64_t)(g.n0 - 1) * plane, plane, ncclDouble, next, c->comm, s));
+    HB_NCCL(ncclRecv(c->d_hhi + k * plane, plane, ncclDouble, next, c->comm, s));
+    HB_NCCL(ncclRecv(c->d_hlo + k * plane, plane, ncclDouble, prev, c->comm, s));
+  }
+  HB_NCCL(ncclGroupEnd());
+}
+
+// swap peer chunks of a fused-pass spectrum (planes <-> k1 rows)
+void all_to_all(homfe_ctx* c, const double2* send, double2* recv, int64_t chunk, cudaStream_t s) {
+  if (c->g.world == 1) {
+    if (send != recv)
+      HB_CUDA(cudaMemcpyAsync(recv, send, chunk * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  HB_NCCL(ncclGroupStart());
+  for (int q = 0; q < c->g.world; ++q) {
+    HB_NCCL(ncclSend(send + q * chunk, 2 * chunk, ncclDouble, q, c->comm, s));
+    HB_NCCL(ncclRecv(recv + q * chunk, 2 * chunk, ncclDouble, q, c->comm, s));
+  }
+  HB_NCCL(ncclGroupEnd());
+}
+
+// partials -> d_red[slot..slot+n): fixed-order local sum, then a sum over
+// ranks (NCCL's fixed ring/tree order: identical on every rank and run).
+double* reduce_global(homfe_ctx* c, int nvals, int slot, cudaStream_t s) {
+  launch_final_sum(c->d_partials, kRedBlocks, nvals, c->d_red + slot, s);
+  HB_NCCL(ncclAllReduce(c->d_red + slot, c->d_red + slot, nvals, ncclDouble, ncclSum, c->comm, s));
+  return c->d_red + slot;
+}
+
 // Deterministic reduction of kRedBlocks partials (nvals each) to host.
 void reduce_to_host(homfe_ctx* c, int nvals, double* out) {
+  if (c->dist) {
+    reduce_global(c, nvals, 0, c->stream);
+    HB_CUDA(cudaMemcpyAsync(c->h_scal, c->d_red, nvals * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    std::memcpy(out, c->h_scal, nvals * sizeof(double));
+    return;
+  }
   launch_final_sum(c->d_partials, kRedBlocks, nvals, c->d_scal, c->stream);
   HB_CUDA(cudaMemcpyAsync(c->h_scal, c->d_scal, nvals * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
@@ -163,9 +229,12 @@ void fft_inverse(homfe_ctx* c, double* out, cudaStream_t s) {
 void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st, double* partials,
                    cudaStream_t s) {
   if (c->fused) {
-    fused_forward(c->ff, c->spp, const_cast<double*>(r), nullptr, nullptr, partials, s);
+    fused_forward(c->ff, c->spp, const_cast<double*>(r), nullptr, nullptr, partials, s, 1);
+    all_to_all(c, c->ff.T, c->ff.Trecv, c->ff.chunk_t(), s);
+    fused_forward(c->ff, c->spp, const_cast<double*>(r), nullptr, nullptr, partials, s, 2);
+    all_to_all(c, c->ff.T2, c->ff.T2recv, c->ff.chunk_t2(), s);
     fused_inverse(c->ff, nullptr, nullptr, z, nullptr, 0, s);
-    c->launches += 2;
+    c->launches += 3;
     return;
   }
   fft_forward(c, r, s);
@@ -176,7 +245,8 @@ void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st,
 
 void apply_K(homfe_ctx* c, const double* u, double* out, const double* fe, double scale, double* partials,
              const PcgState* st, cudaStream_t s) {
-  ElemArgs a{u, out, c->d_phase, c->d_ke, c->n_phases, fe, scale, partials, st};
+  if (c->dist) exchange_halo(c, u, s);
+  ElemArgs a{u, c->d_hlo, c->d_hhi, c->d_ph_lo, out, c->d_phase, c->d_ke, c->n_phases, fe, scale, partials, st};
   if (c->hex_fast) launch_hex_fast(c->g, a, c->d_hexmat, c->hex_iso, s);
   else launch_apply_elem(c->g, a, s);
   c->launches += 1;
@@ -249,8 +319,12 @@ void capture_init(homfe_ctx* c, cudaStream_t s) {
   const int64_t n = c->nvec();
   HB_CUDA(cudaMemsetAsync(c->d_x, 0, n * sizeof(double), s));
   if (c->fused) {
-    fused_forward(c->ff, c->spp, c->d_r, nullptr, nullptr, c->d_partials, s);
-    launch_pcg_init(c->d_st, c->d_partials, c->d_hist, s);
+    fused_forward(c->ff, c->spp, c->d_r, nullptr, nullptr, c->d_partials, s, 1);
+    all_to_all(c, c->ff.T, c->ff.Trecv, c->ff.chunk_t(), s);
+    fused_forward(c->ff, c->spp, c->d_r, nullptr, nullptr, c->d_partials, s, 2);
+    if (c->dist) launch_pcg_init(c->d_st, reduce_global(c, 1, 1, s), c->d_hist, s, 1);
+    else launch_pcg_init(c->d_st, c->d_partials, c->d_hist, s);
+    all_to_all(c, c->ff.T2, c->ff.T2recv, c->ff.chunk_t2(), s);
     fused_inverse(c->ff, c->d_p, nullptr, nullptr, nullptr, 1, s);  // p = z_0
     return;
   }
@@ -259,23 +333,36 @@ void capture_init(homfe_ctx* c, cudaStream_t s) {
   HB_CUDA(cudaMemcpyAsync(c->d_p, c->d_z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
+void remove_means_on(homfe_ctx* c, double* v, cudaStream_t s) {
+  launch_comp_sums(v, c->g.c, c->g.np, c->d_partials, s);
+  if (c->dist) {
+    launch_sub_means(v, c->g.c, c->g.np, reduce_global(c, c->g.c, 4, s), s, (double)c->g.npg);
+  } else {
+    launch_final_sum(c->d_partials, kRedBlocks, c->g.c, c->d_scal, s);
+    launch_sub_means(v, c->g.c, c->g.np, c->d_scal, s);
+  }
+}
+
 void capture_tail(homfe_ctx* c, cudaStream_t s) {
   // x.remove_component_means() (solver.cpp:95)
-  launch_comp_sums(c->d_x, c->g.c, c->g.np, c->d_partials, s);
-  launch_final_sum(c->d_partials, kRedBlocks, c->g.c, c->d_scal, s);
-  launch_sub_means(c->d_x, c->g.c, c->g.np, c->d_scal, s);
+  remove_means_on(c, c->d_x, s);
 }
 
 void body_sequence(homfe_ctx* c, cudaStream_t s, bool cond, cudaGraphConditionalHandle h) {
   const int64_t n = c->nvec();
   if (c->fused) {
-    // K p (+ p.Ap) -> alpha -> [r -= alpha Ap, F r, K^-1, F^-1 pencils, r.z]
-    // -> beta -> [F^-1 planes, x += alpha p, p = z + beta p]
+    // K p (+ p.Ap) -> alpha -> [r -= alpha Ap, F_planes r] -> a2a -> [F_0, K^-1,
+    // F_0^-1, r.z] -> beta -> a2a -> [F_planes^-1, x += alpha p, p = z + beta p]
     apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s);
-    launch_pcg_alpha(c->d_st, c->d_partials, s);
-    fused_forward(c->ff, c->spp, c->d_r, c->d_ap, c->d_st, c->d_partials, s);
-    if (cond) launch_pcg_beta_cond(c->d_st, c->d_partials, c->d_hist, h, s);
+    if (c->dist) launch_pcg_alpha(c->d_st, reduce_global(c, 1, 2, s), s, 1);
+    else launch_pcg_alpha(c->d_st, c->d_partials, s);
+    fused_forward(c->ff, c->spp, c->d_r, c->d_ap, c->d_st, c->d_partials, s, 1);
+    all_to_all(c, c->ff.T, c->ff.Trecv, c->ff.chunk_t(), s);
+    fused_forward(c->ff, c->spp, c->d_r, c->d_ap, c->d_st, c->d_partials, s, 2);
+    if (c->dist) launch_pcg_beta(c->d_st, reduce_global(c, 1, 3, s), c->d_hist, s, 1);
+    else if (cond) launch_pcg_beta_cond(c->d_st, c->d_partials, c->d_hist, h, s);
     else launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
+    all_to_all(c, c->ff.T2, c->ff.T2recv, c->ff.chunk_t2(), s);
     fused_inverse(c->ff, c->d_p, c->d_x, nullptr, c->d_st, 0, s);
     return;
   }
@@ -398,14 +485,23 @@ PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history) {
     HB_CUDA(cudaGraphLaunch(c->pcg_exec, c->stream));
   } else {
     capture_init(c, c->stream);
-    if (!c->body_exec) build_body_graph(c);
+    if (!c->body_exec && !c->body_eager) {
+      try {
+        build_body_graph(c);
+      } catch (const std::exception&) {
+        c->body_eager = true;  // e.g. collectives that cannot be captured
+        cudaGetLastError();
+      }
+    }
     HB_CUDA(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     int launched = 0;
     int batch = 1;
     while (!c->h_st->done && launched < it_max) {
-      for (int i = 0; i < batch && launched < it_max; ++i, ++launched)
-        HB_CUDA(cudaGraphLaunch(c->body_exec, c->stream));
+      for (int i = 0; i < batch && launched < it_max; ++i, ++launched) {
+        if (c->body_exec) HB_CUDA(cudaGraphLaunch(c->body_exec, c->stream));
+        else body_sequence(c, c->stream, false, 0);
+      }
       HB_CUDA(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
       sync(c);
       batch = std::min(batch * 2, 16);
@@ -433,7 +529,8 @@ PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history) {
 }
 
 double quad_norm(homfe_ctx* c, const double* u, const double* d_e) {
-  QuadArgs a{u, d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
+  if (c->dist && u) exchange_halo(c, u, c->stream);
+  QuadArgs a{u, c->d_hhi, d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
   launch_quad(c->g, c->sp, kQuadNorm2, a, c->stream);
   c->launches += 2;
   double v = 0.0;
@@ -450,9 +547,7 @@ double vec_dot(homfe_ctx* c, const double* a, const double* b) {
 }
 
 void remove_means(homfe_ctx* c, double* v) {
-  launch_comp_sums(v, c->g.c, c->g.np, c->d_partials, c->stream);
-  launch_final_sum(c->d_partials, kRedBlocks, c->g.c, c->d_scal, c->stream);
-  launch_sub_means(v, c->g.c, c->g.np, c->d_scal, c->stream);
+  remove_means_on(c, v, c->stream);
   c->launches += 3;
 }
 
@@ -470,6 +565,15 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
   }
   std::vector<int64_t> counts(256, 0);
   for (int64_t p = 0; p < c->g.np; ++p) counts[hp[p]] += 1;
+  if (c->dist) {
+    // global phase counts (volume-mean reference) over the slabs
+    std::vector<double> cd(counts.begin(), counts.end());
+    HB_CUDA(cudaMemcpy(c->d_red, cd.data(), 256 * sizeof(double), cudaMemcpyHostToDevice));
+    HB_NCCL(ncclAllReduce(c->d_red, c->d_red, 256, ncclDouble, ncclSum, c->comm, c->stream));
+    HB_CUDA(cudaMemcpyAsync(cd.data(), c->d_red, 256 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    for (int v = 0; v < 256; ++v) counts[v] = (int64_t)cd[v];
+  }
   for (int v = n_phases; v < 256; ++v)
     if (counts[v]) throw ValidationError("materials: phase id " + std::to_string(v) + " missing from catalog");
   counts.resize(n_phases);
@@ -478,6 +582,16 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
   c->catalog.assign(tangents, tangents + n_phases * m * m);
   if (device_phase) HB_CUDA(cudaMemcpyAsync(c->d_phase, phase, c->g.np, cudaMemcpyDeviceToDevice, c->stream));
   else HB_CUDA(cudaMemcpyAsync(c->d_phase, phase, c->g.np, cudaMemcpyHostToDevice, c->stream));
+  if (c->dist) {
+    // phase plane z0-1 (previous rank's last plane), for the warm-up elements
+    const Grid& g = c->g;
+    const int prev = (g.rank - 1 + g.world) % g.world, next = (g.rank + 1) % g.world;
+    const size_t plane = (size_t)g.n1 * g.n2;
+    HB_NCCL(ncclGroupStart());
+    HB_NCCL(ncclSend(c->d_phase + (int64_t)(g.n0 - 1) * plane, plane, ncclUint8, next, c->comm, c->stream));
+    HB_NCCL(ncclRecv(c->d_ph_lo, plane, ncclUint8, prev, c->comm, c->stream));
+    HB_NCCL(ncclGroupEnd());
+  }
   const int ne = c->ne;
   std::vector<double> ke((size_t)n_phases * ne * ne);
   for (int ph = 0; ph < n_phases; ++ph) element_matrix(c->sp, c->g.d, c->g.c, tangents + ph * m * m, &ke[(size_t)ph * ne * ne]);
@@ -495,7 +609,7 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
   c->d_hexmat = nullptr;
   c->hex_fast = false;
   const char* env = std::getenv("HOMFE_HEX_FAST");
-  if (hex_fast_eligible(c->g) && !(env && env[0] == '0')) {
+  if (hex_fast_eligible(c->g) && (c->dist || !(env && env[0] == '0'))) {
     std::vector<double> iso, gen;
     c->hex_iso = hex_fast_tables(c->g, n_phases, tangents, iso, gen);
     const std::vector<double>& t = c->hex_iso ? iso : gen;
@@ -637,7 +751,8 @@ void newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* a
     }
   }
   // <sigma> = (1/|Y|) sum_q w C (e + D u)   (solver.cpp:321-324)
-  QuadArgs qa{c->d_u, c->d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
+  if (c->dist) exchange_halo(c, c->d_u, c->stream);
+  QuadArgs qa{c->d_u, c->d_hhi, c->d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
   launch_quad(c->g, c->sp, kQuadStress, qa, c->stream);
   c->launches += 2;
   double avg[6];
@@ -682,138 +797,216 @@ int homfe_random_normal(uint64_t seed, int64_t n, double* out) {
   });
 }
 
-int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out) {
-  return guarded([&] {
-    if (!desc || !out) throw ValidationError("create: null argument");
-    const int d = desc->dim;
-    if (d != 2 && d != 3) throw ValidationError("cell: dimension must be 2 or 3, got " + std::to_string(d));
-    for (int a = 0; a < d; ++a) {
-      if (desc->dims[a] < 2)
-        throw ValidationError("cell.dims[" + std::to_string(a) + "]: must be >= 2, got " + std::to_string(desc->dims[a]));
-      if (!(desc->lengths[a] > 0.0)) throw ValidationError("cell.lengths[" + std::to_string(a) + "]: must be > 0");
-      if (desc->dims[a] > (1 << 24)) throw ValidationError("cell: dimension too large");
+}  // extern "C"
+
+namespace {
+
+// Shared constructor. world == 0: single device (periodic grid on one GPU);
+// world >= 1: slab `rank` of `world` along axis 0 with NCCL exchanges.
+homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const void* nccl_id) {
+  if (!desc) throw ValidationError("create: null argument");
+  const int d = desc->dim;
+  if (d != 2 && d != 3) throw ValidationError("cell: dimension must be 2 or 3, got " + std::to_string(d));
+  for (int a = 0; a < d; ++a) {
+    if (desc->dims[a] < 2)
+      throw ValidationError("cell.dims[" + std::to_string(a) + "]: must be >= 2, got " + std::to_string(desc->dims[a]));
+    if (!(desc->lengths[a] > 0.0)) throw ValidationError("cell.lengths[" + std::to_string(a) + "]: must be > 0");
+    if (desc->dims[a] > (1 << 24)) throw ValidationError("cell: dimension too large");
+  }
+  const int c = desc->components;
+  if (c != 1 && c != d) throw ValidationError("nodal field shape does not match layout");
+  const bool dist = world >= 1;
+  const int G = dist ? world : 1;
+  if (dist) {
+    if (rank < 0 || rank >= world) throw ValidationError("slab: rank out of range");
+    if (d != 3 || desc->stencil != HOMFE_TRILINEAR_HEX)
+      throw ValidationError("slab mode: 3-d trilinear-hex grids only");
+    if (desc->dims[0] % world != 0 || desc->dims[1] % world != 0)
+      throw ValidationError("slab mode: dims[0] and dims[1] must be divisible by the number of ranks");
+    if (!nccl_id) throw ValidationError("slab mode: missing NCCL unique id");
+  }
+  auto* ctx = new homfe_ctx();
+  try {
+    ctx->device = desc->device;
+    HB_CUDA(cudaSetDevice(ctx->device));
+    Grid& g = ctx->g;
+    g.d = d;
+    g.c = c;
+    g.m = c == 1 ? d : mandel_dim(d);
+    g.kind = desc->stencil;
+    g.n0g = (int)desc->dims[0];
+    g.n0 = g.n0g / G;
+    g.n1 = (int)desc->dims[1];
+    g.n2 = d == 3 ? (int)desc->dims[2] : 1;
+    g.np = (int64_t)g.n0 * g.n1 * g.n2;
+    g.npg = (int64_t)g.n0g * g.n1 * g.n2;
+    g.dist = dist ? 1 : 0;
+    g.rank = dist ? rank : 0;
+    g.world = G;
+    g.z0 = g.rank * g.n0;
+    g.cell_volume = 1.0;
+    for (int a = 0; a < 3; ++a) g.h[a] = a < d ? desc->lengths[a] / (double)desc->dims[a] : 1.0;
+    for (int a = 0; a < d; ++a) g.cell_volume *= desc->lengths[a];
+    if ((int64_t)c * g.np >= (int64_t)1 << 31) throw ValidationError("cell: grid too large for one device");
+    ctx->dist = dist;
+    ctx->sp = make_stencil(g.kind, d, g.h);
+    ctx->nl = ctx->sp.noff;
+    ctx->ne = ctx->nl * c;
+    const int nh = (d == 3 ? g.n2 : g.n1) / 2 + 1;
+    ctx->nf = (d == 3 ? (int64_t)g.n0g * g.n1 : (int64_t)g.n0g) * nh;  // global spectrum
+    HB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    HB_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
+    HB_CUDA(cudaEventCreate(&ctx->ev0));
+    HB_CUDA(cudaEventCreate(&ctx->ev1));
+    if (dist) {
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      HB_NCCL(ncclCommInitRank(&ctx->comm, world, id, rank));
+      const size_t plane = (size_t)g.n1 * g.n2;
+      ctx->d_hlo = dalloc<double>(c * plane);
+      ctx->d_hhi = dalloc<double>(c * plane);
+      ctx->d_ph_lo = dalloc<uint8_t>(plane);
+      ctx->use_while = false;  // host-driven iterations around the collectives
     }
-    const int c = desc->components;
-    if (c != 1 && c != d) throw ValidationError("nodal field shape does not match layout");
-    auto* ctx = new homfe_ctx();
-    try {
-      ctx->device = desc->device;
-      HB_CUDA(cudaSetDevice(ctx->device));
-      Grid& g = ctx->g;
-      g.d = d;
-      g.c = c;
-      g.m = c == 1 ? d : mandel_dim(d);
-      g.kind = desc->stencil;
-      g.n0 = (int)desc->dims[0];
-      g.n1 = (int)desc->dims[1];
-      g.n2 = d == 3 ? (int)desc->dims[2] : 1;
-      g.np = (int64_t)g.n0 * g.n1 * g.n2;
-      g.cell_volume = 1.0;
-      for (int a = 0; a < 3; ++a) g.h[a] = a < d ? desc->lengths[a] / (double)desc->dims[a] : 1.0;
-      for (int a = 0; a < d; ++a) g.cell_volume *= desc->lengths[a];
-      if ((int64_t)c * g.np >= (int64_t)1 << 31) throw ValidationError("cell: grid too large for one device");
-      ctx->sp = make_stencil(g.kind, d, g.h);
-      ctx->nl = ctx->sp.noff;
-      ctx->ne = ctx->nl * c;
-      const int nh = (d == 3 ? g.n2 : g.n1) / 2 + 1;
-      ctx->nf = (d == 3 ? (int64_t)g.n0 * g.n1 : (int64_t)g.n0) * nh;
-      HB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-      HB_CUDA(cudaStreamCreateWithFlags(&ctx->stream2, cudaStreamNonBlocking));
-      HB_CUDA(cudaEventCreate(&ctx->ev0));
-      HB_CUDA(cudaEventCreate(&ctx->ev1));
-      const int64_t nv = ctx->nvec();
-      ctx->d_x = dalloc<double>(nv);
-      ctx->d_r = dalloc<double>(nv);
-      ctx->d_p = dalloc<double>(nv);
-      ctx->d_ap = dalloc<double>(nv);
-      ctx->d_z = dalloc<double>(nv);
-      ctx->d_u = dalloc<double>(nv);
-      // spectrum scratch: cuFFT layout, or the tile-major layout of the fused
-      // passes (16-column blocks, fftfused.cu) when that is larger
-      const int64_t nb8 = ((int64_t)(g.n2 / 2 + 1) + 15) / 16 * 16;
-      const int64_t fused_sz = d == 3 ? (int64_t)c * g.n0 * g.n1 * nb8 : 0;
-      ctx->d_spec = dalloc<double2>(std::max<int64_t>((int64_t)c * ctx->nf, fused_sz));
-      ctx->d_phase = dalloc<uint8_t>(g.np);
-      ctx->d_partials = dalloc<double>((size_t)kRedBlocks * 8);
-      ctx->d_scal = dalloc<double>(64);
-      ctx->d_e = dalloc<double>(8);
-      ctx->d_st = dalloc<PcgState>(1);
-      HB_CUDA(cudaMallocHost(&ctx->h_st, sizeof(PcgState)));
-      HB_CUDA(cudaMallocHost(&ctx->h_scal, 64 * sizeof(double)));
-      HB_CUDA(cudaMemset(ctx->d_u, 0, nv * sizeof(double)));
+    const int64_t nv = ctx->nvec();
+    ctx->d_x = dalloc<double>(nv);
+    ctx->d_r = dalloc<double>(nv);
+    ctx->d_p = dalloc<double>(nv);
+    ctx->d_ap = dalloc<double>(nv);
+    ctx->d_z = dalloc<double>(nv);
+    ctx->d_u = dalloc<double>(nv);
+    // spectrum scratch: cuFFT layout, or the tile-major layout of the fused
+    // passes (16-column blocks, fftfused.cu) when that is larger
+    const int64_t pitch = ((int64_t)(g.n2 / 2 + 1) + 15) / 16 * 16;
+    const int64_t fused_sz = d == 3 ? (int64_t)c * g.n0 * g.n1 * pitch : 0;
+    ctx->d_spec = dalloc<double2>(std::max<int64_t>(dist ? 0 : (int64_t)c * ctx->nf, fused_sz));
+    ctx->d_phase = dalloc<uint8_t>(g.np);
+    ctx->d_partials = dalloc<double>((size_t)kRedBlocks * 8);
+    ctx->d_scal = dalloc<double>(64);
+    ctx->d_red = dalloc<double>(256);
+    ctx->d_e = dalloc<double>(8);
+    ctx->d_st = dalloc<PcgState>(1);
+    HB_CUDA(cudaMallocHost(&ctx->h_st, sizeof(PcgState)));
+    HB_CUDA(cudaMallocHost(&ctx->h_scal, 256 * sizeof(double)));
+    HB_CUDA(cudaMemset(ctx->d_u, 0, nv * sizeof(double)));
+    if (!dist) {
       // cuFFT plans: batched over the c components (component-planar fields)
       int nn[3] = {g.n0, g.n1, g.n2};
       HB_CUFFT(cufftPlanMany(&ctx->fwd, d, nn, nullptr, 1, (int)g.np, nullptr, 1, (int)ctx->nf, CUFFT_D2Z, c));
       HB_CUFFT(cufftPlanMany(&ctx->inv, d, nn, nullptr, 1, (int)ctx->nf, nullptr, 1, (int)g.np, CUFFT_Z2D, c));
-      // per-axis phase tables for the analytic symbol
-      SpecParams& p = ctx->spp;
-      std::memset(&p, 0, sizeof(p));
-      p.kind = g.kind;
-      p.d = d;
-      p.c = c;
-      p.n0 = g.n0;
-      p.n1 = g.n1;
-      p.n2 = g.n2;
-      p.nh = nh;
-      p.nf = ctx->nf;
-      p.w = ctx->sp.w[0];
-      p.inv_np = 1.0 / (double)g.np;
-      for (int a = 0; a < 3; ++a) p.h[a] = g.h[a];
-      for (int a = 0; a < d; ++a) {
-        const int nfull = a == 0 ? g.n0 : (a == 1 ? g.n1 : g.n2);
-        const int len = a == d - 1 ? nh : nfull;
-        std::vector<double4> tab(len);
-        for (int k = 0; k < len; ++k) {
-          const double t = 2.0 * M_PI * (double)k / (double)nfull;
-          tab[k] = make_double4(std::sin(t), std::cos(t), std::sin(0.5 * t), std::cos(0.5 * t));
-        }
-        ctx->d_tab[a] = dalloc<double4>(len);
-        HB_CUDA(cudaMemcpy(ctx->d_tab[a], tab.data(), len * sizeof(double4), cudaMemcpyHostToDevice));
-        p.tab[a] = ctx->d_tab[a];
+    }
+    // per-axis phase tables for the analytic symbol (global grid)
+    SpecParams& p = ctx->spp;
+    std::memset(&p, 0, sizeof(p));
+    p.kind = g.kind;
+    p.d = d;
+    p.c = c;
+    p.n0 = g.n0g;
+    p.n1 = g.n1;
+    p.n2 = g.n2;
+    p.nh = nh;
+    p.nf = ctx->nf;
+    p.w = ctx->sp.w[0];
+    p.inv_np = 1.0 / (double)g.npg;
+    for (int a = 0; a < 3; ++a) p.h[a] = g.h[a];
+    for (int a = 0; a < d; ++a) {
+      const int nfull = a == 0 ? g.n0g : (a == 1 ? g.n1 : g.n2);
+      const int len = a == d - 1 ? nh : nfull;
+      std::vector<double4> tab(len);
+      for (int k = 0; k < len; ++k) {
+        const double t = 2.0 * M_PI * (double)k / (double)nfull;
+        tab[k] = make_double4(std::sin(t), std::cos(t), std::sin(0.5 * t), std::cos(0.5 * t));
       }
-      if (const char* env = std::getenv("HOMFE_NO_WHILE_GRAPH")) ctx->use_while = env[0] == '0';
-      const char* fenv = std::getenv("HOMFE_FUSED_FFT");
-      if (fused_fft_eligible(g) && !(fenv && fenv[0] == '0')) {
-        const int n1 = g.n1, n0 = g.n0;
-        // twiddles: N <= 256 in the four-step layout tw[k2 * (N/16) + n1] =
-        // W_N^{n1 k2}; N = 512 as the plain table W_N^k (fft.cuh)
-        auto table = [](int n, std::vector<double2>& out) {
-          if (n <= 256) {
-            const int A = n / 16;
-            for (int k2 = 0; k2 < 16; ++k2)
-              for (int n1 = 0; n1 < A; ++n1) {
-                const double t = -2.0 * M_PI * (double)(n1 * k2) / (double)n;
-                out.push_back(make_double2(std::cos(t), std::sin(t)));
-              }
-          } else {
-            for (int k = 0; k < n; ++k) {
-              const double t = -2.0 * M_PI * (double)k / (double)n;
+      ctx->d_tab[a] = dalloc<double4>(len);
+      HB_CUDA(cudaMemcpy(ctx->d_tab[a], tab.data(), len * sizeof(double4), cudaMemcpyHostToDevice));
+      p.tab[a] = ctx->d_tab[a];
+    }
+    if (const char* env = std::getenv("HOMFE_NO_WHILE_GRAPH")) ctx->use_while = ctx->use_while && env[0] == '0';
+    const char* fenv = std::getenv("HOMFE_FUSED_FFT");
+    const bool fused_ok = fused_fft_eligible(g) && g.n1 % G == 0;
+    if (dist && !fused_ok) throw ValidationError("slab mode: plane size must be 128 or 256 and n0 in {64,128,256}");
+    if (fused_ok && (dist || !(fenv && fenv[0] == '0'))) {
+      const int n1 = g.n1, n0 = g.n0g;
+      // twiddles: N <= 256 in the four-step layout tw[k2 * (N/16) + n1] =
+      // W_N^{n1 k2}; N = 512 as the plain table W_N^k (fft.cuh)
+      auto table = [](int n, std::vector<double2>& out) {
+        if (n <= 256) {
+          const int A = n / 16;
+          for (int k2 = 0; k2 < 16; ++k2)
+            for (int n1 = 0; n1 < A; ++n1) {
+              const double t = -2.0 * M_PI * (double)(n1 * k2) / (double)n;
               out.push_back(make_double2(std::cos(t), std::sin(t)));
             }
+        } else {
+          for (int k = 0; k < n; ++k) {
+            const double t = -2.0 * M_PI * (double)k / (double)n;
+            out.push_back(make_double2(std::cos(t), std::sin(t)));
           }
-        };
-        std::vector<double2> tw;
-        table(n1, tw);
-        table(n0, tw);
-        ctx->d_tw = dalloc<double2>(tw.size());
-        HB_CUDA(cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
-        ctx->ff.n0 = n0;
-        ctx->ff.np_plane = n1;
-        ctx->ff.c = c;
-        ctx->ff.np = g.np;
-        ctx->ff.T = ctx->d_spec;
-        ctx->d_spec2 = dalloc<double2>((size_t)c * g.n0 * g.n1 * (((g.n2 / 2 + 1) + 15) / 16 * 16));
-        ctx->ff.T2 = ctx->d_spec2;
-        ctx->ff.tw_plane = ctx->d_tw;
-        ctx->ff.tw0 = ctx->d_tw + n1;
-        ctx->fused = true;
-        if (const char* dbg = std::getenv("HOMFE_FFT_DBG")) ctx->ff.dbg = std::atoi(dbg);
+        }
+      };
+      std::vector<double2> tw;
+      table(n1, tw);
+      table(n0, tw);
+      ctx->d_tw = dalloc<double2>(tw.size());
+      HB_CUDA(cudaMemcpy(ctx->d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+      FusedFft& f = ctx->ff;
+      f.n0 = g.n0;
+      f.np_plane = n1;
+      f.c = c;
+      f.np = g.np;
+      f.n0g = g.n0g;
+      f.rank = g.rank;
+      f.world = G;
+      f.n1l = n1 / G;
+      f.T = ctx->d_spec;
+      ctx->d_spec2 = dalloc<double2>(fused_sz);
+      f.T2 = ctx->d_spec2;
+      if (G > 1) {
+        ctx->d_spec_r = dalloc<double2>(fused_sz);
+        ctx->d_spec2_r = dalloc<double2>(fused_sz);
+        f.Trecv = ctx->d_spec_r;
+        f.T2recv = ctx->d_spec2_r;
+      } else {
+        f.Trecv = f.T;
+        f.T2recv = f.T2;
       }
-    } catch (...) {
-      homfe_gpu_destroy(ctx);
-      throw;
+      f.tw_plane = ctx->d_tw;
+      f.tw0 = ctx->d_tw + n1;
+      ctx->fused = true;
+      if (const char* dbg = std::getenv("HOMFE_FFT_DBG")) f.dbg = std::atoi(dbg);
     }
-    *out = ctx;
+  } catch (...) {
+    homfe_gpu_destroy(ctx);
+    throw;
+  }
+  return ctx;
+}
+
+}  // namespace
+
+extern "C" {
+
+int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("create: null argument");
+    *out = create_impl(desc, 0, 0, nullptr);
+  });
+}
+
+int homfe_nccl_unique_id(void* out) {
+  return guarded([&] {
+    ncclUniqueId id;
+    HB_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+  });
+}
+
+int homfe_gpu_create_dist(const homfe_grid_desc* desc, int32_t rank, int32_t world, const void* nccl_id,
+                          homfe_ctx** out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("create: null argument");
+    if (world < 1) throw ValidationError("slab mode: world must be >= 1");
+    *out = create_impl(desc, rank, world, nccl_id);
   });
 }
 
@@ -832,6 +1025,13 @@ int homfe_gpu_destroy(homfe_ctx* c) {
   if (c->d_spec) cudaFree(c->d_spec);
   if (c->d_tw) cudaFree(c->d_tw);
   if (c->d_spec2) cudaFree(c->d_spec2);
+  if (c->d_spec_r) cudaFree(c->d_spec_r);
+  if (c->d_spec2_r) cudaFree(c->d_spec2_r);
+  if (c->d_hlo) cudaFree(c->d_hlo);
+  if (c->d_hhi) cudaFree(c->d_hhi);
+  if (c->d_ph_lo) cudaFree(c->d_ph_lo);
+  if (c->d_red) cudaFree(c->d_red);
+  if (c->comm) ncclCommDestroy(c->comm);
   if (c->d_phase) cudaFree(c->d_phase);
   if (c->d_st) cudaFree(c->d_st);
   if (c->h_st) cudaFreeHost(c->h_st);
@@ -931,6 +1131,10 @@ int homfe_gpu_apply_minv(homfe_ctx* c, const double* r, double* z) {
 }
 
 int homfe_gpu_reference_blocks(homfe_ctx* c, double* blocks) {
+  if (c && c->dist) {
+    g_err = "not available in slab mode (use a single-device context)";
+    return HOMFE_VALIDATION;
+  }
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_reference(c);
@@ -949,12 +1153,16 @@ static double* quad_buffer(homfe_ctx* c) {
 }
 
 int homfe_gpu_gradient(homfe_ctx* c, const double* u, double* grad) {
+  if (c && c->dist) {
+    g_err = "not available in slab mode (use a single-device context)";
+    return HOMFE_VALIDATION;
+  }
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     const int64_t n = c->nvec();
     double* q = quad_buffer(c);
     HB_CUDA(cudaMemcpyAsync(c->d_p, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    QuadArgs a{c->d_p, nullptr, c->d_phase, c->d_cmat, q, nullptr};
+    QuadArgs a{c->d_p, nullptr, nullptr, c->d_phase, c->d_cmat, q, nullptr};
     launch_quad(c->g, c->sp, kQuadGrad, a, c->stream);
     HB_CUDA(cudaMemcpyAsync(grad, q, (size_t)c->g.np * c->sp.nq * c->g.m * sizeof(double), cudaMemcpyDeviceToHost,
                             c->stream));
@@ -963,6 +1171,10 @@ int homfe_gpu_gradient(homfe_ctx* c, const double* u, double* grad) {
 }
 
 int homfe_gpu_divergence(homfe_ctx* c, const double* s, int32_t weighted, double* out) {
+  if (c && c->dist) {
+    g_err = "not available in slab mode (use a single-device context)";
+    return HOMFE_VALIDATION;
+  }
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     const int64_t n = c->nvec();
@@ -976,6 +1188,10 @@ int homfe_gpu_divergence(homfe_ctx* c, const double* s, int32_t weighted, double
 }
 
 int homfe_gpu_volume_average(homfe_ctx* c, const double* s, double* out) {
+  if (c && c->dist) {
+    g_err = "not available in slab mode (use a single-device context)";
+    return HOMFE_VALIDATION;
+  }
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     double* q = quad_buffer(c);
@@ -1072,6 +1288,10 @@ int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
 }
 
 int homfe_gpu_index_maps(homfe_ctx* c, int64_t* strides3, int64_t* nbr, int32_t* n_off) {
+  if (c && c->dist) {
+    g_err = "not available in slab mode (use a single-device context)";
+    return HOMFE_VALIDATION;
+  }
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     const Grid& g = c->g;

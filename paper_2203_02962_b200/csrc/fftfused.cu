@@ -42,13 +42,40 @@ constexpr int kThreads = 256;
 
 enum { kModePcg = 0, kModePlain = 1, kModeInit = 2, kModeZ = 3 };
 
+// Intermediate spectra. Rank r of G owns planes [r nzl, (r+1) nzl) and, in
+// pass 2, rows k1 in [r n1l, (r+1) n1l).
+//   pass 1 -> 2: T[peer][c][k1l][k2 / 16][i0l][k2 % 16]   (tile-major)
+//     written by the plane owner with peer = destination (k1 / n1l), read by
+//     the pencil owner with peer = source (i0 / nzl); between the two an
+//     all-to-all swaps peer chunks (G = 1: the same buffer, no exchange).
+//     A pass-1/3 CTA moves one 256-byte chunk per k1; a pass-2 block of 16
+//     columns is one contiguous tile per peer.
+//   pass 2 -> 3: T2[peer][c][i0l][k1l][k2]   (plane-major, 16-aligned pitch)
+//     written by the pencil owner with peer = destination (i0 / nzl), read
+//     by the plane owner with peer = source (k1 / n1l).
+// The scattered side of each transpose is a store (merged in L2).
+constexpr int kTB = 16;
+__host__ __device__ constexpr int t_blocks(int np_plane) { return (np_plane / 2 + 1 + kTB - 1) / kTB; }
+struct TLayout {
+  int nc, n1l, nzl, nb;
+  __device__ __forceinline__ int64_t t(int peer, int comp, int k1l, int k2, int i0l) const {
+    return ((((int64_t)peer * nc + comp) * n1l + k1l) * nb + (k2 / kTB)) * ((int64_t)nzl * kTB) +
+           (int64_t)i0l * kTB + (k2 % kTB);
+  }
+  __device__ __forceinline__ int64_t t2(int peer, int comp, int i0l, int k1l, int k2) const {
+    return ((((int64_t)peer * nc + comp) * nzl + i0l) * n1l + k1l) * (int64_t)(nb * kTB) + k2;
+  }
+};
+
+
 struct PlaneArgs {
-  int n0;              // planes per component (axis 0)
-  int64_t np;          // pixels per component
+  int n0;              // LOCAL planes per component (axis 0)
+  int64_t np;          // LOCAL pixels per component
+  TLayout L;
   double* r;           // pass 1 input (updated in PCG mode)
   const double* ap;    // pass 1, PCG mode
-  double2* T;          // pass 1 -> 2, tile-major (t_index)
-  double2* T2;         // pass 2 -> 3, plane-major (t2_index)
+  double2* T;          // pass 1 output (TLayout::t)
+  double2* T2;         // pass 3 input (TLayout::t2)
   double* p;           // pass 3
   double* x;           // pass 3, PCG mode
   double* z;           // pass 3, z mode
@@ -63,29 +90,6 @@ constexpr int tpf() {
   return NP / 16;
 }
 
-// Intermediate spectrum layout (tile-major, 16 columns per 256-byte chunk):
-//   T[comp][k1][k2 / 16][i0][k2 % 16]
-// a pass-1/3 CTA (one plane i0, 16 columns) moves one 256-byte chunk per k1;
-// a pass-2 pencil block (all i0 of 16 columns) is one contiguous 64 KB tile.
-constexpr int kTB = 16;
-__host__ __device__ constexpr int t_blocks(int np_plane) { return (np_plane / 2 + 1 + kTB - 1) / kTB; }
-__device__ __forceinline__ int64_t t_index(int comp, int k1, int k2, int i0, int n0, int n1) {
-  const int nb = t_blocks(n1);
-  return (((int64_t)comp * n1 + k1) * nb + (k2 / kTB)) * ((int64_t)n0 * kTB) + (int64_t)i0 * kTB + (k2 % kTB);
-}
-// Pass-2 output / pass-3 input: plane-major with a 16-aligned row pitch,
-//   T2[comp][i0][k1][k2]  (pitch nb * 16), so pass 3 reads its plane
-// contiguously; the scattered side of both transposes is a write (merged in
-// the write-back L2).
-__device__ __forceinline__ int64_t t2_index(int comp, int k1, int k2, int i0, int n0, int n1) {
-  const int pitch = t_blocks(n1) * kTB;
-  return (((int64_t)comp * n0 + i0) * n1 + k1) * pitch + k2;
-}
-
-// Plane kernels: one cluster of CL = NP/32 CTAs per (component, plane), each
-// CTA NP threads = 16 transform groups of TPF = NP/16 threads, 32 rows.
-// Column slots: NP/2 per plane, 16 per CTA; slot 0 of rank 0 pairs the two
-// real columns k2 = 0 and k2 = NP/2 in one complex transform.
 template <int NP>
 constexpr int rows_slots() {
   constexpr int P = NP / 2 + 1;
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
   const int ncol = 16 - first;
   for (int idx = tid; idx < ncol * NP; idx += NP) {
     const int k1 = idx / ncol, j = idx % ncol + first;
-    a.T[t_index(comp, k1, rank * 16 + j, i0, a.n0, NP)] = rows[j * (NP + 1) + k1];
+    a.T[a.L.t(k1 / a.L.n1l, comp, k1 % a.L.n1l, rank * 16 + j, i0)] = rows[j * (NP + 1) + k1];
   }
   if (rank == 0 && g == 0) {
     // split the paired real columns k2 = 0 and k2 = NP/2
@@ -222,8 +226,8 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
       const int k = t + i * TPF;
       const double2 zk = cbuf[k], zm = conj(cbuf[(NP - k) % NP]);
       const double2 s = cadd(zk, zm), d = csub(zk, zm);
-      a.T[t_index(comp, k, 0, i0, a.n0, NP)] = make_double2(0.5 * s.x, 0.5 * s.y);
-      a.T[t_index(comp, k, NP / 2, i0, a.n0, NP)] = make_double2(0.5 * d.y, -0.5 * d.x);
+      a.T[a.L.t(k / a.L.n1l, comp, k % a.L.n1l, 0, i0)] = make_double2(0.5 * s.x, 0.5 * s.y);
+      a.T[a.L.t(k / a.L.n1l, comp, k % a.L.n1l, NP / 2, i0)] = make_double2(0.5 * d.y, -0.5 * d.x);
     }
   }
 }
@@ -256,11 +260,11 @@ __global__ void __launch_bounds__(NP, 2) k_plane_inv(const PlaneArgs a) {
     for (int i = 0; i < 16; ++i) {
       const int k = 32 * warp + 2 * i + yo;
       if (col == 0) {
-        const double2 A = a.T2[t2_index(comp, k, 0, i0, a.n0, NP)];
-        const double2 B = a.T2[t2_index(comp, k, NP / 2, i0, a.n0, NP)];
+        const double2 A = a.T2[a.L.t2(k / a.L.n1l, comp, i0, k % a.L.n1l, 0)];
+        const double2 B = a.T2[a.L.t2(k / a.L.n1l, comp, i0, k % a.L.n1l, NP / 2)];
         v[i] = make_double2(A.x - B.y, A.y + B.x);  // A + i B
       } else {
-        v[i] = a.T2[t2_index(comp, k, col, i0, a.n0, NP)];
+        v[i] = a.T2[a.L.t2(k / a.L.n1l, comp, i0, k % a.L.n1l, col)];
       }
     }
 #pragma unroll
@@ -346,7 +350,9 @@ __global__ void __launch_bounds__(NP, 2) k_plane_inv(const PlaneArgs a) {
 }
 
 struct PencilArgs {
-  int n0, n1;              // n1 = NP (plane size), T rows per plane
+  int n0, n1;              // GLOBAL pencil length n0 and plane size n1 (= NP)
+  int k1off;               // global k1 of local row 0 (rank * n1l)
+  TLayout L;
   int P;                   // NP/2 + 1
   int ntk;                 // k2 tiles per k1
   double2* T;
@@ -393,15 +399,18 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     ax0[i] = make_double3(tv.x, tv.z, 2.0 - (4.0 / 3.0) * tv.z * tv.z);  // sin, sin(t/2), S2
   }
   double rz = 0.0;
-  const int ntiles = a.n1 * a.ntk;
+  const int ntiles = a.L.n1l * a.ntk;
+  const int nzl = a.L.nzl;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int k1 = tile / a.ntk, c0 = (tile % a.ntk) * BK;
+    const int k1l = tile / a.ntk, c0 = (tile % a.ntk) * BK;
+    const int k1 = a.k1off + k1l;
     const bool live = c0 + j < P;
-    const double2* src = a.T + t_index(comp, k1, c0 + j, 0, a.n0, a.n1);
     double2 v[16];
 #pragma unroll
-    for (int n2 = 0; n2 < 16; ++n2)
-      v[n2] = (live && !(a.dbg & 64)) ? src[(t + TPF * n2) * kTB] : make_double2(0.0, 0.0);
+    for (int n2 = 0; n2 < 16; ++n2) {
+      const int i0 = t + TPF * n2;
+      v[n2] = (live && !(a.dbg & 64)) ? a.T[a.L.t(i0 / nzl, comp, k1l, c0 + j, i0 % nzl)] : make_double2(0.0, 0.0);
+    }
     __syncthreads();  // tws ready / previous tile's buffers free
     if (sp.kind == 3 && tid < BK) {
       // M(k0) = diag(cf0 sh0^2, cf1 S2_0, cf2 S2_0) + offdiag(cf3 sn0, cf4 sn0, cf5 S2_0)
@@ -468,7 +477,10 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     if (!(a.dbg & 32)) fft::fft4step<N0, true>(pb, t, tws);
     if (live && !(a.dbg & 64)) {
 #pragma unroll
-      for (int n = 0; n < 16; ++n) a.T2[t2_index(comp, k1, c0 + j, t + TPF * n, a.n0, a.n1)] = pb[t + TPF * n];
+      for (int n = 0; n < 16; ++n) {
+        const int i0 = t + TPF * n;
+        a.T2[a.L.t2(i0 / nzl, comp, i0 % nzl, k1l, c0 + j)] = pb[t + TPF * n];
+      }
     }
   }
   if (a.partials) {
@@ -489,6 +501,10 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     if (blockIdx.x == 0)
       for (int i = gridDim.x + tid; i < a.nred; i += NT) a.partials[i] = 0.0;
   }
+}
+
+TLayout layout_of(const FusedFft& f) {
+  return TLayout{f.c, f.n1l, f.n0, t_blocks(f.np_plane)};
 }
 
 template <class K>
@@ -523,18 +539,20 @@ void run_pencils_c(const FusedFft& f, const SpecParams& sp, const PcgState* st, 
   constexpr int BK = pencil_bk<C>();
   constexpr int NT = C * BK * (N0 / 16);
   PencilArgs a;
-  a.n0 = f.n0;
+  a.n0 = f.n0g;
   a.n1 = f.np_plane;
+  a.k1off = f.rank * f.n1l;
+  a.L = layout_of(f);
   a.P = f.np_plane / 2 + 1;
   a.ntk = (a.P + BK - 1) / BK;
-  a.T = f.T;
+  a.T = f.Trecv;
   a.T2 = f.T2;
   a.tw = f.tw0;
   a.st = st;
   a.partials = partials;
   a.nred = kRedBlocks;
   a.dbg = f.dbg;
-  const int ntiles = a.n1 * a.ntk;
+  const int ntiles = a.L.n1l * a.ntk;
   const int grid = ntiles < kRedBlocks ? ntiles : kRedBlocks;
   const size_t smem = sizeof(double2) * ((size_t)C * BK * N0 + N0);
   HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -553,7 +571,8 @@ void run_pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st, do
 bool fused_fft_eligible(const Grid& g) {
   if (g.d != 3 || (g.c != 1 && g.c != 3)) return false;
   if (g.n1 != g.n2 || (g.n2 != 128 && g.n2 != 256)) return false;
-  if (g.n0 != 64 && g.n0 != 128 && g.n0 != 256) return false;
+  const int n0g = g.dist ? g.n0g : g.n0;
+  if (n0g != 64 && n0g != 128 && n0g != 256) return false;
   return true;
 }
 
@@ -563,7 +582,7 @@ static void planes(const FusedFft& f, bool inverse, const PlaneArgs& a, cudaStre
 }
 
 static void pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st, double* partials, cudaStream_t s) {
-  switch (f.n0) {
+  switch (f.n0g) {
     case 64: run_pencils<64>(f, sp, st, partials, s); break;
     case 128: run_pencils<128>(f, sp, st, partials, s); break;
     default: run_pencils<256>(f, sp, st, partials, s); break;
@@ -576,6 +595,7 @@ void fused_forward(const FusedFft& f, const SpecParams& sp, double* r, const dou
   PlaneArgs a = {};
   a.n0 = f.n0;
   a.np = f.np;
+  a.L = layout_of(f);
   a.r = r;
   a.ap = ap;
   a.T = f.T;
@@ -594,8 +614,9 @@ void fused_inverse(const FusedFft& f, double* p, double* x, double* z, const Pcg
   PlaneArgs a = {};
   a.n0 = f.n0;
   a.np = f.np;
+  a.L = layout_of(f);
   a.T = f.T;
-  a.T2 = f.T2;
+  a.T2 = f.T2recv;
   a.tw = f.tw_plane;
   a.p = p;
   a.x = x;

@@ -143,6 +143,9 @@ __device__ __forceinline__ void hex_element(const double (&u)[8][C], const doubl
 
 struct HexArgs {
   const double* u;
+  const double* halo_lo, *halo_hi;  // dist mode: neighbour planes [c][plane]
+  const uint8_t* ph_lo;             // dist mode: phase plane z0-1
+  int dist;
   double* out;
   const uint8_t* phase;
   const double* mat;     // n_phases * mat_stride
@@ -185,9 +188,24 @@ __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
     const int z0 = (tile / a.tiles_y) * kTZ;
     for (int zi = -1; zi < kTZ; ++zi) {
       int z = z0 + zi;
-      z = z < 0 ? z + a.n0 : z;
-      const int z1 = z + 1 == a.n0 ? 0 : z + 1;
-      const double* up[2] = {a.u + (int64_t)z * plane, a.u + (int64_t)z1 * plane};
+      int z1 = z + 1;
+      // plane pointers + component strides: periodic wrap on one device,
+      // halo planes at the slab ends in dist mode
+      const double* up[2];
+      int64_t cs[2];
+      if (a.dist) {
+        up[0] = z < 0 ? a.halo_lo : a.u + (int64_t)z * plane;
+        cs[0] = z < 0 ? plane : np;
+        up[1] = z1 >= a.n0 ? a.halo_hi : a.u + (int64_t)z1 * plane;
+        cs[1] = z1 >= a.n0 ? plane : np;
+      } else {
+        z = z < 0 ? z + a.n0 : z;
+        z1 = z + 1 == a.n0 ? 0 : z + 1;
+        up[0] = a.u + (int64_t)z * plane;
+        up[1] = a.u + (int64_t)z1 * plane;
+        cs[0] = cs[1] = np;
+      }
+      const uint8_t* phz = (a.dist && z < 0) ? a.ph_lo : a.phase + (int64_t)z * plane;
       // row y0 - 1 at planes z, z+1: uc[a][c][k]
       double uc[2][2][C];
       {
@@ -196,8 +214,8 @@ __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
         for (int aa = 0; aa < 2; ++aa)
 #pragma unroll
           for (int k = 0; k < C; ++k) {
-            uc[aa][0][k] = __ldg(up[aa] + k * np + (int64_t)y * nx + x);
-            uc[aa][1][k] = __ldg(up[aa] + k * np + (int64_t)y * nx + xp);
+            uc[aa][0][k] = __ldg(up[aa] + k * cs[aa] + (int64_t)y * nx + x);
+            uc[aa][1][k] = __ldg(up[aa] + k * cs[aa] + (int64_t)y * nx + xp);
           }
       }
       double ycarry[2][C];
@@ -215,8 +233,8 @@ __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
         for (int aa = 0; aa < 2; ++aa)
 #pragma unroll
           for (int k = 0; k < C; ++k) {
-            un[aa][0][k] = __ldg(up[aa] + k * np + (int64_t)y1 * nx + x);
-            un[aa][1][k] = __ldg(up[aa] + k * np + (int64_t)y1 * nx + xp);
+            un[aa][0][k] = __ldg(up[aa] + k * cs[aa] + (int64_t)y1 * nx + x);
+            un[aa][1][k] = __ldg(up[aa] + k * cs[aa] + (int64_t)y1 * nx + xp);
           }
         // corners: loc = (aa*2 + b)*2 + c
         double ue[8][C];
@@ -229,7 +247,7 @@ __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
               ue[(aa * 2 + 0) * 2 + c][k] = uc[aa][c][k];
               ue[(aa * 2 + 1) * 2 + c][k] = un[aa][c][k];
             }
-        const int ph = a.phase[(int64_t)z * plane + (int64_t)y * nx + x];
+        const int ph = phz[(int64_t)y * nx + x];
         double r[8][C];
         hex_element<C, ISO>(ue, mat_s + ph * MS, r);
         if (a.fe) {
@@ -385,6 +403,10 @@ bool hex_fast_tables(const Grid& g, int n_phases, const double* cmats, std::vect
 void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, bool iso, cudaStream_t s) {
   HexArgs a;
   a.u = ea.u;
+  a.halo_lo = ea.halo_lo;
+  a.halo_hi = ea.halo_hi;
+  a.ph_lo = ea.ph_lo;
+  a.dist = g.dist;
   a.out = ea.out;
   a.phase = ea.phase;
   a.mat = d_mat;

@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kBlock) k_quad(const Grid g, const __grid_cons
       c1 = (int)(p % g.n1);
       c0 = (int)(p / g.n1);
     }
-    const int u0 = c0 + 1 == g.n0 ? 0 : c0 + 1;
+    const int u0 = (c0 + 1 == g.n0 && !g.dist) ? 0 : c0 + 1;
     const int u1 = c1 + 1 == g.n1 ? 0 : c1 + 1;
     const int u2 = D == 3 ? (c2 + 1 == g.n2 ? 0 : c2 + 1) : 0;
     double uv[8][3];
@@ -193,6 +193,13 @@ __global__ void __launch_bounds__(kBlock) k_quad(const Grid g, const __grid_cons
       const int i0 = sp.offs[o][0] ? u0 : c0;
       const int i1 = sp.offs[o][1] ? u1 : c1;
       const int i2 = sp.offs[o][2] ? u2 : c2;
+      if (g.dist && i0 == g.n0) {  // plane above the slab: halo
+        const int64_t nd = (int64_t)i1 * g.n2 + i2;
+        const int64_t pl = (int64_t)g.n1 * g.n2;
+#pragma unroll
+        for (int k = 0; k < C; ++k) uv[o][k] = a.u ? a.halo_hi[k * pl + nd] : 0.0;
+        continue;
+      }
       const int64_t nd = D == 3 ? ((int64_t)i0 * g.n1 + i1) * g.n2 + i2 : (int64_t)i0 * g.n1 + i1;
 #pragma unroll
       for (int k = 0; k < C; ++k) uv[o][k] = a.u ? a.u[k * np + nd] : 0.0;
@@ -344,10 +351,10 @@ __global__ void k_comp_sums(const double* __restrict__ a, int64_t np, double* pa
 }
 
 template <int C>
-__global__ void k_sub_means(double* __restrict__ a, int64_t np, const double* __restrict__ sums) {
+__global__ void k_sub_means(double* __restrict__ a, int64_t np, const double* __restrict__ sums, double count) {
   double mean[C];
 #pragma unroll
-  for (int k = 0; k < C; ++k) mean[k] = sums[k] / (double)np;
+  for (int k = 0; k < C; ++k) mean[k] = sums[k] / count;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
 #pragma unroll
     for (int k = 0; k < C; ++k) a[k * np + i] -= mean[k];
@@ -580,11 +587,12 @@ void launch_comp_sums(const double* a, int c, int64_t np, double* partials, cuda
   HB_CUDA(cudaGetLastError());
 }
 
-void launch_sub_means(double* a, int c, int64_t np, const double* sums, cudaStream_t s) {
+void launch_sub_means(double* a, int c, int64_t np, const double* sums, cudaStream_t s, double count) {
   const int blocks = grid_for(np);
-  if (c == 1) k_sub_means<1><<<blocks, kBlock, 0, s>>>(a, np, sums);
-  else if (c == 2) k_sub_means<2><<<blocks, kBlock, 0, s>>>(a, np, sums);
-  else k_sub_means<3><<<blocks, kBlock, 0, s>>>(a, np, sums);
+  if (count <= 0.0) count = (double)np;
+  if (c == 1) k_sub_means<1><<<blocks, kBlock, 0, s>>>(a, np, sums, count);
+  else if (c == 2) k_sub_means<2><<<blocks, kBlock, 0, s>>>(a, np, sums, count);
+  else k_sub_means<3><<<blocks, kBlock, 0, s>>>(a, np, sums, count);
   HB_CUDA(cudaGetLastError());
 }
 
@@ -603,12 +611,12 @@ void launch_scale(double* a, double sc, int64_t n, cudaStream_t s) {
   HB_CUDA(cudaGetLastError());
 }
 
-void launch_pcg_init(PcgState* st, const double* partials, double* hist, cudaStream_t s) {
-  k_pcg_init<<<1, 1024, 0, s>>>(st, partials, kRedBlocks, hist);
+void launch_pcg_init(PcgState* st, const double* partials, double* hist, cudaStream_t s, int nblocks) {
+  k_pcg_init<<<1, 1024, 0, s>>>(st, partials, nblocks, hist);
   HB_CUDA(cudaGetLastError());
 }
-void launch_pcg_alpha(PcgState* st, const double* partials, cudaStream_t s) {
-  k_pcg_alpha<<<1, 1024, 0, s>>>(st, partials, kRedBlocks);
+void launch_pcg_alpha(PcgState* st, const double* partials, cudaStream_t s, int nblocks) {
+  k_pcg_alpha<<<1, 1024, 0, s>>>(st, partials, nblocks);
   HB_CUDA(cudaGetLastError());
 }
 void launch_update_xr(double* x, double* r, const double* p, const double* ap, int64_t n, const PcgState* st,
@@ -616,8 +624,8 @@ void launch_update_xr(double* x, double* r, const double* p, const double* ap, i
   k_update_xr<<<grid_for(n), kBlock, 0, s>>>(x, r, p, ap, n, st);
   HB_CUDA(cudaGetLastError());
 }
-void launch_pcg_beta(PcgState* st, const double* partials, double* hist, cudaStream_t s) {
-  k_pcg_beta<<<1, 1024, 0, s>>>(st, partials, kRedBlocks, hist);
+void launch_pcg_beta(PcgState* st, const double* partials, double* hist, cudaStream_t s, int nblocks) {
+  k_pcg_beta<<<1, 1024, 0, s>>>(st, partials, nblocks, hist);
   HB_CUDA(cudaGetLastError());
 }
 void launch_pcg_beta_cond(PcgState* st, const double* partials, double* hist, cudaGraphConditionalHandle h,

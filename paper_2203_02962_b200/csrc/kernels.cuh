@@ -14,6 +14,9 @@ constexpr int kRedBlocks = 1184;  // 8 x 148 SMs: fixed grid => deterministic su
 
 struct ElemArgs {
   const double* u;
+  const double* halo_lo;  // dist: plane z0-1 of u ([c][plane]); nullable otherwise
+  const double* halo_hi;  // dist: plane z0+nz of u
+  const uint8_t* ph_lo;   // dist: phase plane z0-1
   double* out;
   const uint8_t* phase;
   const double* ke;       // n_phases x NE x NE, row-major
@@ -36,6 +39,7 @@ void launch_hex_fast(const Grid& g, const ElemArgs& a, const double* d_mat, bool
 enum QuadMode { kQuadGrad = 0, kQuadNorm2 = 1, kQuadStress = 2 };
 struct QuadArgs {
   const double* u;        // nullable => zero field
+  const double* halo_hi;  // dist: plane z0+nz of u ([c][plane])
   const double* e;        // nullable => no macroscopic term (device, m doubles)
   const uint8_t* phase;
   const double* cmat;     // n_phases x m x m column-major (stress mode)
@@ -52,17 +56,17 @@ void launch_index_maps(const Grid& g, const StencilParams& sp, int64_t* nbr, cud
 // Vectors / reductions (deterministic: fixed grids, fixed-order finals).
 void launch_dot_partials(const double* a, const double* b, int64_t n, double* partials, cudaStream_t s);
 void launch_comp_sums(const double* a, int c, int64_t np, double* partials, cudaStream_t s);
-void launch_sub_means(double* a, int c, int64_t np, const double* sums, cudaStream_t s);
+void launch_sub_means(double* a, int c, int64_t np, const double* sums, cudaStream_t s, double count = 0.0);
 void launch_final_sum(const double* partials, int nblocks, int nvals, double* out, cudaStream_t s);
 void launch_scale(double* a, double sc, int64_t n, cudaStream_t s);
 void launch_axpy(double* y, double a, const double* x, int64_t n, cudaStream_t s);
 
 // PCG steps (solver.cpp:62-94) with device-resident scalars.
-void launch_pcg_init(PcgState* st, const double* partials, double* hist, cudaStream_t s);
-void launch_pcg_alpha(PcgState* st, const double* partials, cudaStream_t s);
+void launch_pcg_init(PcgState* st, const double* partials, double* hist, cudaStream_t s, int nblocks = kRedBlocks);
+void launch_pcg_alpha(PcgState* st, const double* partials, cudaStream_t s, int nblocks = kRedBlocks);
 void launch_update_xr(double* x, double* r, const double* p, const double* ap, int64_t n,
                       const PcgState* st, cudaStream_t s);
-void launch_pcg_beta(PcgState* st, const double* partials, double* hist, cudaStream_t s);
+void launch_pcg_beta(PcgState* st, const double* partials, double* hist, cudaStream_t s, int nblocks = kRedBlocks);
 void launch_update_p(double* p, const double* z, int64_t n, const PcgState* st, cudaStream_t s);
 void launch_set_while(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s);
 void launch_update_p_cond(double* p, const double* z, int64_t n, const PcgState* st,
@@ -88,13 +92,18 @@ void launch_spectral(const SpecParams& p, double2* spec, const PcgState* st, dou
 // Fused three-pass preconditioner (fftfused.cu): 3-D grids with square
 // 128^2 / 256^2 planes. T has the cuFFT D2Z layout [c][n0][n1][n2/2+1].
 struct FusedFft {
-  int n0, np_plane, c;
-  int64_t np;                 // pixels per component
-  double2* T;                 // tile-major pass-1 output
-  double2* T2;                // plane-major pass-2 output
+  int n0, np_plane, c;        // n0: LOCAL planes (slab), np_plane = n1 = n2
+  int64_t np;                 // LOCAL pixels per component
+  int n0g, rank, world, n1l;  // global planes, slab rank, ranks, k1 rows per rank
+  double2* T;                 // pass-1 output (send side)
+  double2* Trecv;             // pass-2 input (== T when world == 1)
+  double2* T2;                // pass-2 output (send side)
+  double2* T2recv;            // pass-3 input (== T2 when world == 1)
   const double2* tw_plane;    // W_{n1} table
-  const double2* tw0;         // W_{n0} table
+  const double2* tw0;         // W_{n0g} table
   int dbg;                    // profiling: skipped phases (HOMFE_FFT_DBG)
+  int64_t chunk_t() const { return (int64_t)c * n1l * ((np_plane / 2 + 16) / 16) * n0 * 16; }
+  int64_t chunk_t2() const { return (int64_t)c * n0 * n1l * (((np_plane / 2 + 16) / 16) * 16); }
 };
 bool fused_fft_eligible(const Grid& g);
 void fused_forward(const FusedFft& f, const SpecParams& sp, double* r, const double* ap, const PcgState* st,
