@@ -58,6 +58,19 @@ constexpr int kTB = 16;
 __host__ __device__ constexpr int t_blocks(int np_plane) { return (np_plane / 2 + 1 + kTB - 1) / kTB; }
 struct TLayout {
   int nc, n1l, nzl, nb;
+  int sh1, shz;  // log2 n1l, log2 nzl (both powers of two)
+  // global k1 / global i0 -> (peer, local) without divisions
+  __device__ __forceinline__ int p1(int k1) const { return k1 >> sh1; }
+  __device__ __forceinline__ int l1(int k1) const { return k1 & (n1l - 1); }
+  __device__ __forceinline__ int pz(int i0) const { return i0 >> shz; }
+  __device__ __forceinline__ int lz(int i0) const { return i0 & (nzl - 1); }
+  // t(peer(k1), comp, k1l, k2, i0l) = (row1 * nb + k2 / 16) * nzl * 16 + i0l * 16 + k2 % 16
+  __device__ __forceinline__ int row1(int comp, int k1) const { return comp * n1l + k1 + p1(k1) * (nc - 1) * n1l; }
+  // t2(peer(k1), comp, i0l, k1l, k2) = row2 * (nb * 16) + k2
+  __device__ __forceinline__ int row2(int comp, int i0l, int k1) const {
+    const int q = p1(k1);
+    return ((q * nc + comp) * nzl + i0l) * n1l + k1 - q * n1l;
+  }
   __device__ __forceinline__ int64_t t(int peer, int comp, int k1l, int k2, int i0l) const {
     return ((((int64_t)peer * nc + comp) * n1l + k1l) * nb + (k2 / kTB)) * ((int64_t)nzl * kTB) +
            (int64_t)i0l * kTB + (k2 % kTB);
@@ -215,9 +228,12 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
   if (a.dbg & 8) return;
   const int first = rank == 0 ? 1 : 0;
   const int ncol = 16 - first;
+  constexpr int NB = t_blocks(NP);
+  const int64_t zs = (int64_t)a.L.nzl * kTB;
+  double2* tdst = a.T + (int64_t)rank * zs + i0 * kTB;  // k2 / 16 == rank for this CTA's columns
   for (int idx = tid; idx < ncol * NP; idx += NP) {
     const int k1 = idx / ncol, j = idx % ncol + first;
-    a.T[a.L.t(k1 / a.L.n1l, comp, k1 % a.L.n1l, rank * 16 + j, i0)] = rows[j * (NP + 1) + k1];
+    tdst[(int64_t)a.L.row1(comp, k1) * NB * zs + j] = rows[j * (NP + 1) + k1];
   }
   if (rank == 0 && g == 0) {
     // split the paired real columns k2 = 0 and k2 = NP/2
@@ -226,8 +242,8 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
       const int k = t + i * TPF;
       const double2 zk = cbuf[k], zm = conj(cbuf[(NP - k) % NP]);
       const double2 s = cadd(zk, zm), d = csub(zk, zm);
-      a.T[a.L.t(k / a.L.n1l, comp, k % a.L.n1l, 0, i0)] = make_double2(0.5 * s.x, 0.5 * s.y);
-      a.T[a.L.t(k / a.L.n1l, comp, k % a.L.n1l, NP / 2, i0)] = make_double2(0.5 * d.y, -0.5 * d.x);
+      a.T[a.L.t(a.L.p1(k), comp, a.L.l1(k), 0, i0)] = make_double2(0.5 * s.x, 0.5 * s.y);
+      a.T[a.L.t(a.L.p1(k), comp, a.L.l1(k), NP / 2, i0)] = make_double2(0.5 * d.y, -0.5 * d.x);
     }
   }
 }
@@ -255,16 +271,18 @@ __global__ void __launch_bounds__(NP, 2) k_plane_inv(const PlaneArgs a) {
   const int jc = lane & 15, yo = lane >> 4;
   {
     const int col = rank * 16 + jc;
+    constexpr int PITCH = t_blocks(NP) * kTB;
+    // rows k = 32 warp + 2 i + yo share one peer (n1l is a multiple of 32)
+    const double2* src = a.T2 + (int64_t)a.L.row2(comp, i0, 32 * warp + yo) * PITCH + col;
     double2 v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int k = 32 * warp + 2 * i + yo;
       if (col == 0) {
-        const double2 A = a.T2[a.L.t2(k / a.L.n1l, comp, i0, k % a.L.n1l, 0)];
-        const double2 B = a.T2[a.L.t2(k / a.L.n1l, comp, i0, k % a.L.n1l, NP / 2)];
+        const double2 A = src[2 * i * PITCH];
+        const double2 B = src[2 * i * PITCH + NP / 2];
         v[i] = make_double2(A.x - B.y, A.y + B.x);  // A + i B
       } else {
-        v[i] = a.T2[a.L.t2(k / a.L.n1l, comp, i0, k % a.L.n1l, col)];
+        v[i] = src[2 * i * PITCH];
       }
     }
 #pragma unroll
@@ -400,7 +418,6 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
   }
   double rz = 0.0;
   const int ntiles = a.L.n1l * a.ntk;
-  const int nzl = a.L.nzl;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int k1l = tile / a.ntk, c0 = (tile % a.ntk) * BK;
     const int k1 = a.k1off + k1l;
@@ -409,7 +426,7 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
 #pragma unroll
     for (int n2 = 0; n2 < 16; ++n2) {
       const int i0 = t + TPF * n2;
-      v[n2] = (live && !(a.dbg & 64)) ? a.T[a.L.t(i0 / nzl, comp, k1l, c0 + j, i0 % nzl)] : make_double2(0.0, 0.0);
+      v[n2] = (live && !(a.dbg & 64)) ? a.T[a.L.t(a.L.pz(i0), comp, k1l, c0 + j, a.L.lz(i0))] : make_double2(0.0, 0.0);
     }
     __syncthreads();  // tws ready / previous tile's buffers free
     if (sp.kind == 3 && tid < BK) {
@@ -479,7 +496,7 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
 #pragma unroll
       for (int n = 0; n < 16; ++n) {
         const int i0 = t + TPF * n;
-        a.T2[a.L.t2(i0 / nzl, comp, i0 % nzl, k1l, c0 + j)] = pb[t + TPF * n];
+        a.T2[a.L.t2(a.L.pz(i0), comp, a.L.lz(i0), k1l, c0 + j)] = pb[t + TPF * n];
       }
     }
   }
@@ -503,8 +520,15 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
   }
 }
 
+static int ilog2(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  if ((1 << l) != v) throw ValidationError("fused FFT: slab sizes must be powers of two");
+  return l;
+}
+
 TLayout layout_of(const FusedFft& f) {
-  return TLayout{f.c, f.n1l, f.n0, t_blocks(f.np_plane)};
+  return TLayout{f.c, f.n1l, f.n0, t_blocks(f.np_plane), ilog2(f.n1l), ilog2(f.n0)};
 }
 
 template <class K>
@@ -573,6 +597,9 @@ bool fused_fft_eligible(const Grid& g) {
   if (g.n1 != g.n2 || (g.n2 != 128 && g.n2 != 256)) return false;
   const int n0g = g.dist ? g.n0g : g.n0;
   if (n0g != 64 && n0g != 128 && n0g != 256) return false;
+  if (g.dist && ((g.world & (g.world - 1)) != 0 || g.n1 % g.world != 0 || g.n1 / g.world < 32 ||
+                 g.n0 * g.world != n0g))
+    return false;
   return true;
 }
 

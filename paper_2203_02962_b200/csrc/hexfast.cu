@@ -37,6 +37,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "fft.cuh"
 #include "kernels.cuh"
 
 namespace hb {
@@ -119,6 +120,7 @@ __device__ __forceinline__ void hex_element(const double (&u)[8][C], const doubl
   for (int k = 0; k < C; ++k)
 #pragma unroll
     for (int i = 0; i < 8; ++i) R[k][i] = 0.0;
+#define HB_ACC(k, v, t) R[k][v] += (t)
   if constexpr (C == 3) {
     if constexpr (ISO) {
       HB_HEX_MODES_ELASTIC_ISO
@@ -132,6 +134,7 @@ __device__ __forceinline__ void hex_element(const double (&u)[8][C], const doubl
       HB_HEX_MODES_SCALAR_GEN
     }
   }
+#undef HB_ACC
 #pragma unroll
   for (int k = 0; k < C; ++k) {
     double x[8];
@@ -321,7 +324,309 @@ __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
   }
 }
 
+
+// ===========================================================================
+// v2: z-march with TMA-staged rows and shared per-axis transforms.
+//
+// Each block owns a contiguous run of "element rows" r = zb * n1 + y (zb = a
+// block of KZ element planes) and marches z inside a row:
+//  * unit j of a row = plane pz = zb*KZ - 1 + j, node rows y and y+1, all
+//    components (+ the element phase row), bulk-copied by one thread into a
+//    D-deep shared-memory ring (cp.async.bulk + mbarrier);
+//  * forward: the x- and y-stages of the (S, D) transform are done once per
+//    plane and carried in registers to the next element (Lo), so an element
+//    costs 16 instead of 24 adds per component;
+//  * adjoint: z-stage with a register carry of the upper face (zc), then the
+//    x-stage (warp shuffle + one shared-memory hop between warps), then the
+//    y-stage; node row y+1's partial waits in a per-thread shared-memory
+//    buffer (ybuf, KZ x C) for the next element row.
+// The first row of a run and the first element plane of a row are warm-up
+// (recomputed, not stored), so runs are independent and every node is the
+// same fixed-order sum (bitwise reproducible). Runs are balanced over exactly
+// (resident blocks) CTAs.
+// ===========================================================================
+constexpr int kZDepth = 3;
+#ifndef HB_HEXZ_MINB3
+#define HB_HEXZ_MINB3 2
+#endif
+#ifndef HB_HEXZ_KZ3
+#define HB_HEXZ_KZ3 8
+#endif
+
+template <int C>
+__host__ __device__ constexpr int zslot_bytes(int nx) {
+  return 2 * C * nx * 8 + nx;
+}
+
+template <int V>
+__device__ __forceinline__ void acc_fold(double (&A)[4], double (&B)[4], double t) {
+  if constexpr (V < 4) {
+    A[V] += t;
+    B[V] += t;
+  } else {
+    A[V - 4] -= t;
+    B[V - 4] += t;
+  }
+}
+
+struct ZRun {
+  int rows_total;  // n1 * (n0 / KZ)
+  int grid;
+  int list_cap;
+};
+
+template <int C, int KZ>
+__device__ __forceinline__ void z_issue(const HexArgs& a, const int* its, int u, unsigned char* slot,
+                                        uint64_t* bar) {
+  const int nx = a.n2;
+  const int i = u / (KZ + 2), j = u - i * (KZ + 2);
+  const int info = its[i];
+  const int y = info & 0xffff, zb = (info >> 16) & 0x7fff;
+  const int y1 = y + 1 == a.n1 ? 0 : y + 1;
+  const int64_t plane = (int64_t)a.n1 * nx;
+  const int64_t np = plane * a.n0;
+  int pz = zb * KZ - 1 + j;
+  const double* src;
+  int64_t cs;
+  if (a.dist) {
+    src = pz < 0 ? a.halo_lo : (pz >= a.n0 ? a.halo_hi : a.u + (int64_t)pz * plane);
+    cs = (pz < 0 || pz >= a.n0) ? plane : np;
+  } else {
+    pz = pz < 0 ? pz + a.n0 : (pz >= a.n0 ? pz - a.n0 : pz);
+    src = a.u + (int64_t)pz * plane;
+    cs = np;
+  }
+  const uint32_t row_bytes = nx * 8;
+  fft::mbar_expect_tx(bar, 2 * C * row_bytes + (j ? nx : 0));
+  double* dst = reinterpret_cast<double*>(slot);
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    fft::bulk_g2s(dst + (0 * C + k) * nx, src + k * cs + (int64_t)y * nx, row_bytes, bar);
+    fft::bulk_g2s(dst + (1 * C + k) * nx, src + k * cs + (int64_t)y1 * nx, row_bytes, bar);
+  }
+  if (j) {
+    int zp = zb * KZ - 2 + j;  // element plane
+    const uint8_t* ph;
+    if (a.dist && zp < 0) ph = a.ph_lo;
+    else {
+      zp = zp < 0 ? zp + a.n0 : zp;
+      ph = a.phase + (int64_t)zp * plane;
+    }
+    fft::bulk_g2s(slot + 2 * C * row_bytes, ph + (int64_t)y * nx, nx, bar);
+  }
+}
+
+template <int C, bool ISO, int KZ, bool FE>
+__global__ void __launch_bounds__(256, C == 3 ? HB_HEXZ_MINB3 : 2) k_hex_z(const HexArgs a, const ZRun run) {
+  if (a.st && a.st->done) return;
+  constexpr int MS = mat_stride<C, ISO>();
+  constexpr int D = kZDepth;
+  extern __shared__ __align__(16) unsigned char zsm[];
+  const int nx = blockDim.x;  // == n2
+  const int nw = nx >> 5;
+  const int sb = zslot_bytes<C>(nx);
+  unsigned char* ring = zsm;                                        // [D][sb]
+  double* ybuf = reinterpret_cast<double*>(zsm + D * sb);            // [KZ][C][nx]
+  double* lo_s = ybuf + KZ * C * nx;                                 // [C][4][nx]
+  double* edge = lo_s + 4 * C * nx;                                  // [2][nw][C][2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(edge + 2 * nw * C * 2);  // [D]
+  int* its = reinterpret_cast<int*>(full + D);                       // [list_cap]
+  double* mat_s = reinterpret_cast<double*>(its + ((run.list_cap + 1) & ~1));  // optional table copy
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  // this block's run of element rows and its y-iteration list
+  const int r0 = (int)((int64_t)blockIdx.x * run.rows_total / run.grid);
+  const int r1 = (int)((int64_t)(blockIdx.x + 1) * run.rows_total / run.grid);
+  __shared__ int n_its_s;
+  if (tid == 0) {
+    int n = 0;
+    for (int r = r0; r < r1; ++r) {
+      const int zb = r / a.n1, y = r - zb * a.n1;
+      if (r == r0 || y == 0) its[n++] = (y == 0 ? a.n1 - 1 : y - 1) | (zb << 16) | (1 << 31);
+      its[n++] = y | (zb << 16);
+    }
+    n_its_s = n;
+    for (int d = 0; d < D; ++d) fft::mbar_init(&full[d], 1);
+    fft::fence_mbar_init();
+  }
+  const bool mat_in_smem = a.n_phases * MS <= 2048;
+  if (mat_in_smem)
+    for (int i = tid; i < a.n_phases * MS; i += nx) mat_s[i] = a.mat[i];
+  __syncthreads();
+  const double* matp = mat_in_smem ? mat_s : a.mat;
+  const int n_its = n_its_s;
+  const int nunits = n_its * (KZ + 2);
+  if (tid == 0)
+    for (int u = 0; u < D && u < nunits; ++u) z_issue<C, KZ>(a, its, u, ring + u * sb, &full[u]);
+
+  const int x = tid;
+  const int xp = x + 1 == nx ? 0 : x + 1;
+  const int64_t plane = (int64_t)a.n1 * nx;
+  const int64_t np = plane * a.n0;
+  double dotacc = 0.0;
+  double zc[C][4], uprev[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    uprev[k] = 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) zc[k][m] = 0.0;
+  }
+  int u = 0;
+#pragma unroll 1
+  for (int it = 0; it < n_its; ++it) {
+    const int info = its[it];
+    const int y = info & 0xffff, zb = (info >> 16) & 0x7fff;
+    const bool warm = info < 0;
+#pragma unroll 1
+    for (int j = 0; j < KZ + 2; ++j, ++u) {
+      const int slot = u % D;
+      unsigned char* sl = ring + slot * sb;
+      fft::mbar_wait(&full[slot], (u / D) & 1);
+      const double* rows = reinterpret_cast<const double*>(sl);
+      double Up[C][4], ucur[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const double a0 = rows[(0 * C + k) * nx + x], a1 = rows[(0 * C + k) * nx + xp];
+        const double b0 = rows[(1 * C + k) * nx + x], b1 = rows[(1 * C + k) * nx + xp];
+        const double aS = a0 + a1, aD = a1 - a0, bS = b0 + b1, bD = b1 - b0;
+        Up[k][0] = aS + bS;
+        Up[k][1] = aD + bD;
+        Up[k][2] = bS - aS;
+        Up[k][3] = bD - aD;
+        ucur[k] = a0;
+      }
+      const int ph = j ? sl[2 * C * nx * 8 + x] : 0;
+      double nodev[C][2];
+      if (j) {
+        // lower plane's x/y-stage values (stored by the previous step)
+        double V[C][8];
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const double lo = lo_s[(k * 4 + m) * nx + x];
+            V[k][m] = lo + Up[k][m];
+            V[k][4 + m] = Up[k][m] - lo;
+          }
+        // modal residual folded straight into the z-adjoint: A = lower face
+        // (seeded with the previous element's upper face), B = upper face
+        double A[C][4], B[C][4];
+#pragma unroll
+        for (int k = 0; k < C; ++k)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            A[k][m] = zc[k][m];
+            B[k][m] = 0.0;
+          }
+        const double* mat = matp + ph * MS;
+#define HB_ACC(k, v, t) acc_fold<v>(A[k], B[k], (t))
+        if constexpr (C == 3) {
+          if constexpr (ISO) {
+            HB_HEX_MODES_ELASTIC_ISO
+          } else {
+            HB_HEX_MODES_ELASTIC_GEN
+          }
+        } else {
+          if constexpr (ISO) {
+            HB_HEX_MODES_SCALAR_ISO
+          } else {
+            HB_HEX_MODES_SCALAR_GEN
+          }
+        }
+#undef HB_ACC
+        if constexpr (FE) {  // element load, moved to the modal basis (fwd / 8)
+#pragma unroll
+          for (int k = 0; k < C; ++k) {
+            double fx[8], fv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) fx[i] = __ldg(a.fe + ph * 8 * C + i * C + k);
+            modal_fwd(fx, fv);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              A[k][m] += 0.125 * (fv[m] - fv[4 + m]);
+              B[k][m] += 0.125 * (fv[m] + fv[4 + m]);
+            }
+          }
+        }
+        double sp[C][2];
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m) zc[k][m] = B[k][m];
+#pragma unroll
+          for (int ym = 0; ym < 2; ++ym) {
+            const double sm = A[k][ym * 2] - A[k][ym * 2 + 1];
+            sp[k][ym] = A[k][ym * 2] + A[k][ym * 2 + 1];
+            const double recv = __shfl_up_sync(0xffffffffu, sp[k][ym], 1);
+            nodev[k][ym] = lane ? sm + recv : sm;
+          }
+        }
+        if (lane == 31) {
+          double* eg = edge + ((u & 1) * nw + warp) * C * 2;
+#pragma unroll
+          for (int k = 0; k < C; ++k) {
+            eg[k * 2 + 0] = sp[k][0];
+            eg[k * 2 + 1] = sp[k][1];
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < C; ++k)
+#pragma unroll
+        for (int m = 0; m < 4; ++m) lo_s[(k * 4 + m) * nx + x] = Up[k][m];
+      __syncthreads();  // edges visible; ring slot fully read
+      if (tid == 0 && u + D < nunits) z_issue<C, KZ>(a, its, u + D, sl, &full[slot]);
+      if (j >= 2) {
+        const int zi = j - 2;
+        const int z = zb * KZ + zi;
+        const double* eg = edge + ((u & 1) * nw + (warp == 0 ? nw - 1 : warp - 1)) * C * 2;
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          double n0v = nodev[k][0], n1v = nodev[k][1];
+          if (lane == 0) {
+            n0v += eg[k * 2 + 0];
+            n1v += eg[k * 2 + 1];
+          }
+          const double rowy = n0v - n1v, rowy1 = n0v + n1v;
+          double* yb = ybuf + (zi * C + k) * nx + x;
+          if (!warm) {
+            const double val = a.scale * (rowy + *yb);
+            a.out[k * np + (int64_t)z * plane + (int64_t)y * nx + x] = val;
+            dotacc = fma(uprev[k], val, dotacc);
+          }
+          *yb = rowy1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < C; ++k) uprev[k] = ucur[k];
+    }
+  }
+  if (a.partials) {
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dotacc += __shfl_xor_sync(0xffffffffu, dotacc, o);
+    if (lane == 0) red[warp] = dotacc;
+    __syncthreads();
+    if (warp == 0) {
+      double t = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0) a.partials[blockIdx.x] = t;
+    }
+    if (blockIdx.x == 0)
+      for (int i = gridDim.x + tid; i < a.nred; i += nx) a.partials[i] = 0.0;
+  }
+}
 }  // namespace
+
+static int hex_kz(const Grid& g) { return g.c == 3 ? HB_HEXZ_KZ3 : 16; }
+
+static bool hex_v2(const Grid& g) {
+  const char* e = std::getenv("HOMFE_HEX_V1");
+  if (e && e[0] == '1') return false;
+  return g.n0 % hex_kz(g) == 0;
+}
 
 // Tile (rows y per thread, planes z per tile): a larger tile recomputes
 // fewer warm-up elements ((1 + 1/TY)(1 + 1/TZ)) but yields fewer blocks.
@@ -342,7 +647,8 @@ bool hex_fast_eligible(const Grid& g) {
   if (g.d != 3 || g.kind != 3 || (g.c != 1 && g.c != 3)) return false;
   int ty, tz;
   hex_tile(g, ty, tz);
-  if (g.n2 % 32 != 0 || g.n2 > 256 || g.n1 % ty != 0 || g.n0 % tz != 0) return false;
+  if (g.n2 % 32 != 0 || g.n2 > 256) return false;
+  if (!hex_v2(g) && (g.n1 % ty != 0 || g.n0 % tz != 0)) return false;
   if (g.h[0] != g.h[1] || g.h[1] != g.h[2]) return false;
   return true;
 }
@@ -400,6 +706,42 @@ bool hex_fast_tables(const Grid& g, int n_phases, const double* cmats, std::vect
   return all_iso;
 }
 
+template <int C, bool ISO, int KZ, bool FE>
+static void launch_hex_z(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
+  constexpr int MS = mat_stride<C, ISO>();
+  const int nx = g.n2, nw = nx / 32;
+  const int rows_total = g.n1 * (g.n0 / KZ);
+  auto smem_for = [&](int grid) {
+    const int per = (rows_total + grid - 1) / grid;
+    const int cap = 2 * per + 4;
+    size_t b = (size_t)kZDepth * zslot_bytes<C>(nx) + sizeof(double) * ((size_t)KZ * C * nx + 4 * C * nx + 2 * nw * C * 2) +
+               sizeof(uint64_t) * kZDepth + sizeof(int) * ((cap + 1) & ~1);
+    if (n_phases * MS <= 2048) b += sizeof(double) * (size_t)n_phases * MS;
+    return b;
+  };
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    HB_CUDA(cudaGetDevice(&dev));
+    HB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  size_t smem = smem_for(2 * sms);
+  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hex_z<C, ISO, KZ, FE>, nx, smem));
+  if (per_sm < 1) per_sm = 1;
+  int grid = per_sm * sms;
+  if (grid > rows_total) grid = rows_total;
+  if (grid > kRedBlocks) grid = kRedBlocks;
+  smem = smem_for(grid);
+  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ZRun run;
+  run.rows_total = rows_total;
+  run.grid = grid;
+  run.list_cap = 2 * ((rows_total + grid - 1) / grid) + 4;
+  k_hex_z<C, ISO, KZ, FE><<<grid, nx, smem, s>>>(a, run);
+}
+
 void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, bool iso, cudaStream_t s) {
   HexArgs a;
   a.u = ea.u;
@@ -419,6 +761,23 @@ void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, boo
   a.n0 = g.n0;
   a.n1 = g.n1;
   a.n2 = g.n2;
+  if (hex_v2(g)) {
+#define HB_HEXZ(C, ISO, KZ)                                      \
+  do {                                                           \
+    if (a.fe) launch_hex_z<C, ISO, KZ, true>(g, a, ea.n_phases, s); \
+    else launch_hex_z<C, ISO, KZ, false>(g, a, ea.n_phases, s);     \
+  } while (0)
+    if (g.c == 3) {
+      if (iso) HB_HEXZ(3, true, HB_HEXZ_KZ3);
+      else HB_HEXZ(3, false, HB_HEXZ_KZ3);
+    } else {
+      if (iso) HB_HEXZ(1, true, 16);
+      else HB_HEXZ(1, false, 16);
+    }
+#undef HB_HEXZ
+    HB_CUDA(cudaGetLastError());
+    return;
+  }
   int kTY, kTZ;
   hex_tile(g, kTY, kTZ);
   a.tiles_y = g.n1 / kTY;
