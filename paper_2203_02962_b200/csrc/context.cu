@@ -972,6 +972,7 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
       }
       f.tw_plane = ctx->d_tw;
       f.tw0 = ctx->d_tw + n1;
+      fused_make_maps(f);
       ctx->fused = true;
       if (const char* dbg = std::getenv("HOMFE_FFT_DBG")) f.dbg = std::atoi(dbg);
     }

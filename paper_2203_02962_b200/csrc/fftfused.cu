@@ -21,6 +21,7 @@
 // Per component and voxel this moves 32 + 16 + 40 = 88 bytes, against 8
 // streaming passes (~216 bytes) for cuFFT + separate kernels.
 #include <cooperative_groups.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "fft.cuh"
@@ -44,27 +45,29 @@ enum { kModePcg = 0, kModePlain = 1, kModeInit = 2, kModeZ = 3 };
 
 // Intermediate spectra. Rank r of G owns planes [r nzl, (r+1) nzl) and, in
 // pass 2, rows k1 in [r n1l, (r+1) n1l).
-//   pass 1 -> 2: T[peer][c][k1l][k2 / 16][i0l][k2 % 16]   (tile-major)
+//   pass 1 -> 2: T[peer][c][k1l][k2 / 4][i0l][k2 % 4]   (tile-major)
 //     written by the plane owner with peer = destination (k1 / n1l), read by
 //     the pencil owner with peer = source (i0 / nzl); between the two an
 //     all-to-all swaps peer chunks (G = 1: the same buffer, no exchange).
-//     A pass-1/3 CTA moves one 256-byte chunk per k1; a pass-2 block of 16
-//     columns is one contiguous tile per peer.
+//     A pass-1 CTA stores 64-byte pieces; a pass-2 block's 4-column group
+//     is one contiguous run per peer (one TMA bulk copy).
 //   pass 2 -> 3: T2[peer][c][i0l][k1l][k2]   (plane-major, 16-aligned pitch)
 //     written by the pencil owner with peer = destination (i0 / nzl), read
 //     by the plane owner with peer = source (k1 / n1l).
 // The scattered side of each transpose is a store (merged in L2).
-constexpr int kTB = 16;
+constexpr int kTB = 16;  // T2 row pitch granule
+constexpr int kTG = 4;   // T column group: a pencil block's TMA unit
 __host__ __device__ constexpr int t_blocks(int np_plane) { return (np_plane / 2 + 1 + kTB - 1) / kTB; }
+__host__ __device__ constexpr int t_groups(int np_plane) { return (np_plane / 2 + 1 + kTG - 1) / kTG; }
 struct TLayout {
-  int nc, n1l, nzl, nb;
+  int nc, n1l, nzl, nb, ng;  // ng: 4-column groups of T
   int sh1, shz;  // log2 n1l, log2 nzl (both powers of two)
   // global k1 / global i0 -> (peer, local) without divisions
   __device__ __forceinline__ int p1(int k1) const { return k1 >> sh1; }
   __device__ __forceinline__ int l1(int k1) const { return k1 & (n1l - 1); }
   __device__ __forceinline__ int pz(int i0) const { return i0 >> shz; }
   __device__ __forceinline__ int lz(int i0) const { return i0 & (nzl - 1); }
-  // t(peer(k1), comp, k1l, k2, i0l) = (row1 * nb + k2 / 16) * nzl * 16 + i0l * 16 + k2 % 16
+  // t(peer(k1), comp, k1l, k2, i0l) = (row1 * ng + k2 / 4) * nzl * 4 + i0l * 4 + k2 % 4
   __device__ __forceinline__ int row1(int comp, int k1) const { return comp * n1l + k1 + p1(k1) * (nc - 1) * n1l; }
   // t2(peer(k1), comp, i0l, k1l, k2) = row2 * (nb * 16) + k2
   __device__ __forceinline__ int row2(int comp, int i0l, int k1) const {
@@ -72,8 +75,8 @@ struct TLayout {
     return ((q * nc + comp) * nzl + i0l) * n1l + k1 - q * n1l;
   }
   __device__ __forceinline__ int64_t t(int peer, int comp, int k1l, int k2, int i0l) const {
-    return ((((int64_t)peer * nc + comp) * n1l + k1l) * nb + (k2 / kTB)) * ((int64_t)nzl * kTB) +
-           (int64_t)i0l * kTB + (k2 % kTB);
+    return ((((int64_t)peer * nc + comp) * n1l + k1l) * ng + (k2 / kTG)) * ((int64_t)nzl * kTG) +
+           (int64_t)i0l * kTG + (k2 % kTG);
   }
   __device__ __forceinline__ int64_t t2(int peer, int comp, int i0l, int k1l, int k2) const {
     return ((((int64_t)peer * nc + comp) * nzl + i0l) * n1l + k1l) * (int64_t)(nb * kTB) + k2;
@@ -134,19 +137,21 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
     fft::fence_mbar_init();
   }
   __syncthreads();
+  const bool noio = a.dbg & 128;  // profiling: no r / Ap traffic
   if (tid == 0) {
-    fft::mbar_expect_tx(&bar, 32 * ROWB);
-    for (int y = 0; y < 32; ++y) fft::bulk_g2s(rows + y * P, a.r + plane + (int64_t)y * NP, ROWB, &bar);
+    fft::mbar_expect_tx(&bar, noio ? 0 : 32 * ROWB);
+    if (!noio)
+      for (int y = 0; y < 32; ++y) fft::bulk_g2s(rows + y * P, a.r + plane + (int64_t)y * NP, ROWB, &bar);
   }
   for (int i = tid; i < NP; i += NP) tws[i] = a.tw[i];
   double2 apv[PT];
-  if (pcg) {
+  if (pcg && !noio) {
     const double2* ap2 = reinterpret_cast<const double2*>(a.ap + plane);
 #pragma unroll
     for (int i = 0; i < PT; ++i) apv[i] = ap2[tid + i * NP];
   }
   fft::mbar_wait(&bar, 0);
-  if (pcg) {
+  if (pcg && !noio) {
     const double alpha = a.st->alpha;
 #pragma unroll
     for (int i = 0; i < PT; ++i) {
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
     __syncthreads();
     // r written back by TMA bulk stores (async proxy: no generic stores left
     // in flight at the cluster barriers below)
-    if (tid == 0) {
+    if (tid == 0 && !noio) {
       fft::fence_proxy_async();
       for (int y = 0; y < 32; ++y) fft::bulk_s2g(a.r + plane + (int64_t)y * NP, rows + y * P, ROWB);
       fft::bulk_commit();
@@ -228,12 +233,12 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
   if (a.dbg & 8) return;
   const int first = rank == 0 ? 1 : 0;
   const int ncol = 16 - first;
-  constexpr int NB = t_blocks(NP);
-  const int64_t zs = (int64_t)a.L.nzl * kTB;
-  double2* tdst = a.T + (int64_t)rank * zs + i0 * kTB;  // k2 / 16 == rank for this CTA's columns
+  constexpr int NG = t_groups(NP);
+  const int64_t zs = (int64_t)a.L.nzl * kTG;
+  double2* tdst = a.T + (int64_t)(rank * (16 / kTG)) * zs + i0 * kTG;  // this CTA's 16 columns
   for (int idx = tid; idx < ncol * NP; idx += NP) {
     const int k1 = idx / ncol, j = idx % ncol + first;
-    tdst[(int64_t)a.L.row1(comp, k1) * NB * zs + j] = rows[j * (NP + 1) + k1];
+    tdst[(int64_t)a.L.row1(comp, k1) * NG * zs + (j / kTG) * zs + (j % kTG)] = rows[j * (NP + 1) + k1];
   }
   if (rank == 0 && g == 0) {
     // split the paired real columns k2 = 0 and k2 = NP/2
@@ -384,7 +389,7 @@ struct PencilArgs {
 
 template <int C>
 constexpr int pencil_bk() {
-  return C == 3 ? 4 : 16;
+  return C == 3 ? 4 : 8;
 }
 
 // One transform group (TPF threads) per pencil (component, column): the
@@ -396,19 +401,56 @@ template <int N0, int C>
 #define HB_PENCIL_MINB 2
 #endif
 __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB)
-    k_pencil(const __grid_constant__ SpecParams sp, const PencilArgs a) {
+    k_pencil(const __grid_constant__ SpecParams sp, const PencilArgs a, const __grid_constant__ CUtensorMap t2map) {
+  // Persistent blocks; tile = (k1 row, BK columns) for all C components.
+  // Each tile's T data (BK/4 column groups x C components x peers, each a
+  // contiguous run) is bulk-copied (TMA) into one of two stages while the
+  // previous tile is transformed; after the raw reads the stage is reused
+  // as the pencils' FFT / solve buffer.
   constexpr int TPF = tpf<N0>();
   constexpr int BK = pencil_bk<C>();
   constexpr int NT = C * BK * TPF;
+  constexpr int NGB = BK / kTG;  // column groups per tile
+  constexpr int STAGE = C * BK * N0;  // double2 per stage
   if (a.st && !a.st->active) return;
-  extern __shared__ double2 sm[];
-  double2* buf = sm;              // [C][BK][N0]
-  double2* tws = buf + C * BK * N0;
+  extern __shared__ double2 sm_raw[];
+  double2* sm = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(sm_raw) + 127) & ~uintptr_t(127));
+  double2* stage0 = sm;             // [2][C][NGB][N0][kTG]  (128-B aligned: TMA tensor stores)
+  double2* tws = sm + 2 * STAGE;
+  __shared__ __align__(8) uint64_t full[2];
   const int tid = threadIdx.x, g = tid / TPF, t = tid % TPF;
   const int j = g % BK, comp = g / BK;
-  for (int i = tid; i < N0; i += NT) tws[i] = a.tw[i];
   const int P = a.P;
-  double2* pb = buf + g * N0;
+  const int ntiles = a.L.n1l * a.ntk;
+  const int nzl = a.L.nzl;
+  const int world = N0 / nzl;
+  // one tile's bulk copies into stage st
+  auto issue = [&](int tile, int st) {
+    const int k1l = tile / a.ntk, c0 = (tile % a.ntk) * BK;
+    uint32_t bytes = 0;
+    for (int gg = 0; gg < NGB; ++gg)
+      if (c0 / kTG + gg < a.L.ng) bytes += C * world * nzl * kTG * (uint32_t)sizeof(double2);
+    fft::mbar_expect_tx(&full[st], bytes);
+    for (int c = 0; c < C; ++c)
+      for (int gg = 0; gg < NGB; ++gg) {
+        if (c0 / kTG + gg >= a.L.ng) continue;
+        for (int q = 0; q < world; ++q)
+          fft::bulk_g2s(stage0 + st * STAGE + ((c * NGB + gg) * N0 + q * nzl) * kTG,
+                        a.T + a.L.t(q, c, k1l, c0 + gg * kTG, 0), nzl * kTG * (uint32_t)sizeof(double2),
+                        &full[st]);
+      }
+  };
+  if (tid == 0) {
+    fft::mbar_init(&full[0], 1);
+    fft::mbar_init(&full[1], 1);
+    fft::fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if ((int)(blockIdx.x + gridDim.x) < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  for (int i = tid; i < N0; i += NT) tws[i] = a.tw[i];
   // per-column symbol factors (hex, k0-independent parts) and the axis-0 table
   __shared__ double colf[BK][6];
   __shared__ double3 ax0[N0];
@@ -417,18 +459,19 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     ax0[i] = make_double3(tv.x, tv.z, 2.0 - (4.0 / 3.0) * tv.z * tv.z);  // sin, sin(t/2), S2
   }
   double rz = 0.0;
-  const int ntiles = a.L.n1l * a.ntk;
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it & 1;
+    double2* stg = stage0 + st * STAGE;
     const int k1l = tile / a.ntk, c0 = (tile % a.ntk) * BK;
     const int k1 = a.k1off + k1l;
-    const bool live = c0 + j < P;
+    fft::mbar_wait(&full[st], (it >> 1) & 1);
     double2 v[16];
+    {
+      const double2* src = stg + (comp * NGB + j / kTG) * N0 * kTG + (j % kTG);
 #pragma unroll
-    for (int n2 = 0; n2 < 16; ++n2) {
-      const int i0 = t + TPF * n2;
-      v[n2] = (live && !(a.dbg & 64)) ? a.T[a.L.t(a.L.pz(i0), comp, k1l, c0 + j, a.L.lz(i0))] : make_double2(0.0, 0.0);
+      for (int n2 = 0; n2 < 16; ++n2) v[n2] = src[(t + TPF * n2) * kTG];
     }
-    __syncthreads();  // tws ready / previous tile's buffers free
     if (sp.kind == 3 && tid < BK) {
       // M(k0) = diag(cf0 sh0^2, cf1 S2_0, cf2 S2_0) + offdiag(cf3 sn0, cf4 sn0, cf5 S2_0)
       const int k2 = min(c0 + tid, P - 1);
@@ -442,7 +485,13 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
       colf[tid][4] = 4.0 * w * t2.x / (h0 * h2) * S21;
       colf[tid][5] = 4.0 * w * t1.x * t2.x / (h1 * h2);
     }
+    __syncthreads();  // raw stage reads done (stage becomes the FFT buffers); colf, tws ready
+    double2* buf = stg;               // [C][BK][N0]
+    double2* pb = buf + g * N0;
     if (!(a.dbg & 32)) fft::fft4step_regs<N0, false>(v, pb, t, tws);
+    else
+#pragma unroll
+      for (int n2 = 0; n2 < 16; ++n2) pb[t + TPF * n2] = v[n2];
     __syncthreads();
     for (int e = tid; e < N0 * BK && !(a.dbg & 16); e += NT) {
       const int jj = e / N0, k0 = e % N0;
@@ -492,14 +541,40 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     }
     __syncthreads();
     if (!(a.dbg & 32)) fft::fft4step<N0, true>(pb, t, tws);
-    if (live && !(a.dbg & 64)) {
 #pragma unroll
-      for (int n = 0; n < 16; ++n) {
-        const int i0 = t + TPF * n;
-        a.T2[a.L.t2(a.L.pz(i0), comp, a.L.lz(i0), k1l, c0 + j)] = pb[t + TPF * n];
+    for (int n = 0; n < 16; ++n) v[n] = pb[t + TPF * n];
+    __syncthreads();  // every pencil read back: re-lay the stage as [C][group][i0][4]
+    {
+      double2* dst = stg + (comp * NGB + j / kTG) * N0 * kTG + (j % kTG);
+#pragma unroll
+      for (int n = 0; n < 16; ++n) dst[(t + TPF * n) * kTG] = v[n];
+    }
+    fft::fence_proxy_async();  // generic smem writes -> async-proxy (TMA) reads
+    __syncthreads();
+    if (tid == 0) {
+      // T2 is plane-major: each (component, 4-column group) is a box of
+      // 64 bytes x n0 planes, scattered by the TMA engine
+      if (!(a.dbg & 64)) {
+        for (int c = 0; c < C; ++c)
+          for (int gg = 0; gg < NGB; ++gg) {
+            if (c0 / kTG + gg >= a.L.ng) continue;
+            const double2* src = stg + (c * NGB + gg) * N0 * kTG;
+            asm volatile(
+                "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                    reinterpret_cast<uint64_t>(&t2map)),
+                "r"(2 * (c0 + gg * kTG)), "r"(k1l), "r"(0), "r"(c), "r"(0), "r"(fft::smem_u32(src))
+                : "memory");
+          }
+        fft::bulk_commit();
+      }
+      if (tile + 2 * (int)gridDim.x < ntiles) {
+        fft::bulk_wait_read();  // the stores have read the stage
+        issue(tile + 2 * gridDim.x, st);
       }
     }
+    __syncthreads();
   }
+  if (tid == 0) fft::bulk_wait();  // stores complete before the block retires
   if (a.partials) {
     __shared__ double red[32];
     const int lane = tid & 31, warp = tid >> 5;
@@ -528,7 +603,7 @@ static int ilog2(int v) {
 }
 
 TLayout layout_of(const FusedFft& f) {
-  return TLayout{f.c, f.n1l, f.n0, t_blocks(f.np_plane), ilog2(f.n1l), ilog2(f.n0)};
+  return TLayout{f.c, f.n1l, f.n0, t_blocks(f.np_plane), t_groups(f.np_plane), ilog2(f.n1l), ilog2(f.n0)};
 }
 
 template <class K>
@@ -577,10 +652,20 @@ void run_pencils_c(const FusedFft& f, const SpecParams& sp, const PcgState* st, 
   a.nred = kRedBlocks;
   a.dbg = f.dbg;
   const int ntiles = a.L.n1l * a.ntk;
-  const int grid = ntiles < kRedBlocks ? ntiles : kRedBlocks;
-  const size_t smem = sizeof(double2) * ((size_t)C * BK * N0 + N0);
+  const size_t smem = sizeof(double2) * (2 * (size_t)C * BK * N0 + N0) + 128;
   HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_pencil<N0, C><<<grid, NT, smem, s>>>(sp, a);
+  static int grid_cap[2] = {0, 0};  // resident blocks of this instantiation (persistent grid)
+  int& cap = grid_cap[C == 3];
+  if (!cap) {
+    int dev = 0, sms = 0, per = 0;
+    HB_CUDA(cudaGetDevice(&dev));
+    HB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_pencil<N0, C>, NT, smem));
+    cap = sms * (per > 0 ? per : 1);
+  }
+  int grid = ntiles < cap ? ntiles : cap;
+  if (grid > kRedBlocks) grid = kRedBlocks;
+  k_pencil<N0, C><<<grid, NT, smem, s>>>(sp, a, *reinterpret_cast<const CUtensorMap*>(f.t2map));
   HB_CUDA(cudaGetLastError());
 }
 
@@ -591,6 +676,33 @@ void run_pencils(const FusedFft& f, const SpecParams& sp, const PcgState* st, do
 }
 
 }  // namespace
+
+// T2 as a 5-D fp64 tensor {2 pitch, n1l, nzl, c, world} (innermost first);
+// box {8, 1, nzl, 1, world} = one 4-column group of one k1 row over all planes.
+void fused_make_maps(FusedFft& f) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    HB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  const cuuint64_t pitch = (cuuint64_t)t_blocks(f.np_plane) * kTB;  // complex per row
+  const cuuint64_t dims[5] = {2 * pitch, (cuuint64_t)f.n1l, (cuuint64_t)f.n0, (cuuint64_t)f.c, (cuuint64_t)f.world};
+  const cuuint64_t row = pitch * sizeof(double2);
+  const cuuint64_t strides[4] = {row, row * f.n1l, row * f.n1l * f.n0, row * f.n1l * f.n0 * f.c};
+  const cuuint32_t box[5] = {2 * kTG, 1, (cuuint32_t)f.n0, 1, (cuuint32_t)f.world};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(f.t2map);
+  const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, f.T2, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
 
 bool fused_fft_eligible(const Grid& g) {
   if (g.d != 3 || (g.c != 1 && g.c != 3)) return false;

@@ -102,10 +102,12 @@ struct FusedFft {
   const double2* tw_plane;    // W_{n1} table
   const double2* tw0;         // W_{n0g} table
   int dbg;                    // profiling: skipped phases (HOMFE_FFT_DBG)
-  int64_t chunk_t() const { return (int64_t)c * n1l * ((np_plane / 2 + 16) / 16) * n0 * 16; }
+  alignas(64) unsigned char t2map[128];  // CUtensorMap of T2 (pass-2 TMA stores), fused_make_maps
+  int64_t chunk_t() const { return (int64_t)c * n1l * ((np_plane / 2 + 4) / 4) * n0 * 4; }
   int64_t chunk_t2() const { return (int64_t)c * n0 * n1l * (((np_plane / 2 + 16) / 16) * 16); }
 };
 bool fused_fft_eligible(const Grid& g);
+void fused_make_maps(FusedFft& f);  // after T2 is allocated
 void fused_forward(const FusedFft& f, const SpecParams& sp, double* r, const double* ap, const PcgState* st,
                    double* partials, cudaStream_t s, int which = 3);
 void fused_inverse(const FusedFft& f, double* p, double* x, double* z, const PcgState* st, int init,

@@ -41,7 +41,8 @@ class slab_layout:
     """Index maps of the fused passes' exchanged spectra (csrc/fftfused.cu,
     TLayout), restated for host-side tests."""
 
-    TB = 16
+    TB = 16  # T2 row pitch granule
+    TG = 4   # T column group
 
     def __init__(self, c, n0, n1, world):
         self.c, self.n0, self.n1, self.world = c, n0, n1, world
@@ -49,16 +50,17 @@ class slab_layout:
         self.n1l = n1 // world
         self.P = n1 // 2 + 1
         self.nb = (self.P + self.TB - 1) // self.TB
+        self.ng = (self.P + self.TG - 1) // self.TG
 
     def chunk_t(self):
-        return self.c * self.n1l * self.nb * self.nzl * self.TB
+        return self.c * self.n1l * self.ng * self.nzl * self.TG
 
     def chunk_t2(self):
         return self.c * self.nzl * self.n1l * self.nb * self.TB
 
     def t(self, peer, comp, k1l, k2, i0l):
-        return ((((peer * self.c + comp) * self.n1l + k1l) * self.nb + k2 // self.TB) * (self.nzl * self.TB)
-                + i0l * self.TB + k2 % self.TB)
+        return ((((peer * self.c + comp) * self.n1l + k1l) * self.ng + k2 // self.TG) * (self.nzl * self.TG)
+                + i0l * self.TG + k2 % self.TG)
 
     def t2(self, peer, comp, i0l, k1l, k2):
         return (((peer * self.c + comp) * self.nzl + i0l) * self.n1l + k1l) * (self.nb * self.TB) + k2
