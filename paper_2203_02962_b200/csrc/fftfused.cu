@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(NP, 2) k_plane_inv(const PlaneArgs a) {
     const double2 z0 = zb[0], z1 = zb[1];
     return (row & 1) ? make_double2(z0.y, z1.y) : make_double2(z0.x, z1.x);
   };
+  if (a.dbg & 256) return;  // profiling: no p / x traffic
   if (a.mode == kModePcg) {
     double2* p2 = reinterpret_cast<double2*>(a.p + plane);
     double2* x2 = reinterpret_cast<double2*>(a.x + plane);
@@ -762,6 +763,7 @@ void fused_inverse(const FusedFft& f, double* p, double* x, double* z, const Pcg
   a.z = z;
   a.st = st;
   a.mode = st ? kModePcg : (init ? kModeInit : kModeZ);
+  a.dbg = f.dbg;
   planes(f, true, a, s);
 }
 
