@@ -253,8 +253,14 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
   }
 }
 
+#ifndef HB_INV_MINB
+#define HB_INV_MINB 2
+#endif
+#ifndef HB_INV_SPLIT
+#define HB_INV_SPLIT 2
+#endif
 template <int NP>
-__global__ void __launch_bounds__(NP, 2) k_plane_inv(const PlaneArgs a) {
+__global__ void __launch_bounds__(NP, HB_INV_MINB) k_plane_inv(const PlaneArgs a) {
   constexpr int P = NP / 2 + 1;
   constexpr int CL = NP / 32;
   constexpr int TPF = tpf<NP>();
@@ -349,21 +355,25 @@ __global__ void __launch_bounds__(NP, 2) k_plane_inv(const PlaneArgs a) {
   if (a.mode == kModePcg) {
     double2* p2 = reinterpret_cast<double2*>(a.p + plane);
     double2* x2 = reinterpret_cast<double2*>(a.x + plane);
-    double2 pv[PT], xv[PT];
-#pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      pv[i] = p2[tid + i * NP];
-      xv[i] = x2[tid + i * NP];
-    }
     const double alpha = a.st->alpha, beta = a.st->beta;
     const int conv = a.st->converged;
+    constexpr int HP = PT / HB_INV_SPLIT;  // chunks bound the live registers
 #pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      const int idx = tid + i * NP;
-      x2[idx] = make_double2(fma(alpha, pv[i].x, xv[i].x), fma(alpha, pv[i].y, xv[i].y));
-      if (!conv) {
-        const double2 zv = zval(idx);
-        p2[idx] = make_double2(fma(beta, pv[i].x, zv.x), fma(beta, pv[i].y, zv.y));
+    for (int hh = 0; hh < HB_INV_SPLIT; ++hh) {
+      double2 pv[HP], xv[HP];
+#pragma unroll
+      for (int i = 0; i < HP; ++i) {
+        pv[i] = p2[tid + (hh * HP + i) * NP];
+        xv[i] = x2[tid + (hh * HP + i) * NP];
+      }
+#pragma unroll
+      for (int i = 0; i < HP; ++i) {
+        const int idx = tid + (hh * HP + i) * NP;
+        x2[idx] = make_double2(fma(alpha, pv[i].x, xv[i].x), fma(alpha, pv[i].y, xv[i].y));
+        if (!conv) {
+          const double2 zv = zval(idx);
+          p2[idx] = make_double2(fma(beta, pv[i].x, zv.x), fma(beta, pv[i].y, zv.y));
+        }
       }
     }
   } else {
