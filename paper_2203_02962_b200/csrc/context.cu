@@ -530,12 +530,18 @@ PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history) {
 
 double quad_norm(homfe_ctx* c, const double* u, const double* d_e) {
   if (c->dist && u) exchange_halo(c, u, c->stream);
-  QuadArgs a{u, c->d_hhi, d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
-  launch_quad(c->g, c->sp, kQuadNorm2, a, c->stream);
+  double scale = 1.0;
+  if (c->hex_fast && u &&
+      launch_hex_quad(c->g, 0, u, c->d_hhi, d_e, c->d_phase, c->d_cmat, c->d_partials, c->stream)) {
+    scale = c->g.h[0] * c->g.h[0] * c->g.h[0];  // 8 w
+  } else {
+    QuadArgs a{u, c->d_hhi, d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
+    launch_quad(c->g, c->sp, kQuadNorm2, a, c->stream);
+  }
   c->launches += 2;
   double v = 0.0;
   reduce_to_host(c, 1, &v);
-  return std::sqrt(v);
+  return std::sqrt(v * scale);
 }
 
 double vec_dot(homfe_ctx* c, const double* a, const double* b) {
@@ -752,12 +758,18 @@ void newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* a
   }
   // <sigma> = (1/|Y|) sum_q w C (e + D u)   (solver.cpp:321-324)
   if (c->dist) exchange_halo(c, c->d_u, c->stream);
-  QuadArgs qa{c->d_u, c->d_hhi, c->d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
-  launch_quad(c->g, c->sp, kQuadStress, qa, c->stream);
+  double sscale = 1.0;
+  if (c->hex_fast && launch_hex_quad(c->g, 1, c->d_u, c->d_hhi, c->d_e, c->d_phase, c->d_cmat, c->d_partials,
+                                     c->stream)) {
+    sscale = c->g.h[0] * c->g.h[0] * c->g.h[0];
+  } else {
+    QuadArgs qa{c->d_u, c->d_hhi, c->d_e, c->d_phase, c->d_cmat, nullptr, c->d_partials};
+    launch_quad(c->g, c->sp, kQuadStress, qa, c->stream);
+  }
   c->launches += 2;
   double avg[6];
   reduce_to_host(c, m, avg);
-  for (int k = 0; k < m; ++k) avg_out[k] = avg[k] / c->g.cell_volume;
+  for (int k = 0; k < m; ++k) avg_out[k] = avg[k] * sscale / c->g.cell_volume;
   rep->seconds_total = since(t_total);
   rep->kernel_launches = c->launches;
 }

@@ -84,6 +84,36 @@ def gen_scalar(iso):
     return "\n".join(out)
 
 
+def gen_norm(elastic):
+    """sum_q |eps_q + E|^2 / (8 w) over the quad modes (orthogonal patterns):
+    mode m contributes sum_rows (sc * e_row (+ E_row for sss))^2, with
+    sc[2 cls + shear] = per-class mode scale (x sqrt(2)/2 on Mandel shear rows)."""
+    out = []
+    tables = INC3 if elastic else [[(j, 0, v) for (j, v) in inc] for inc in INCS]
+    for md, inc in enumerate(tables):
+        cls = CLASS[md]
+        rows = sorted({e for e, _, _ in inc})
+        out.append(f"  {{  /* mode {MODES[md]} */")
+        for e in rows:
+            terms = [f"V[{k}][{v}]" for (ee, k, v) in inc if ee == e]
+            idx = cls * 2 + (1 if (elastic and e >= 3) else 0)
+            base = f"fma(sc[{idx}], {' + '.join(terms)}, E[{e}])" if md == 0 else f"sc[{idx}] * ({' + '.join(terms)})"
+            out.append(f"    {{ const double t = {base}; nacc = fma(t, t, nacc); }}")
+        out.append("  }")
+    return "\n".join(out)
+
+
+def gen_sss(elastic):
+    """Mandel strain of the constant quad mode plus E (= the element's quad average)."""
+    out = []
+    inc = INC3[0] if elastic else [(j, 0, v) for (j, v) in INCS[0]]
+    for e in sorted({e for e, _, _ in inc}):
+        terms = [f"V[{k}][{v}]" for (ee, k, v) in inc if ee == e]
+        idx = 1 if (elastic and e >= 3) else 0
+        out.append(f"  es[{e}] = fma(sc[{idx}], {' + '.join(terms)}, E[{e}]);")
+    return "\n".join(out)
+
+
 def main():
     here = os.path.dirname(os.path.abspath(__file__))
     parts = ["// GENERATED by gen_hex_modes.py -- do not edit.",
@@ -92,7 +122,9 @@ def main():
              "// t into modal residual (k, v) (defined by the including kernel).",
              "#define HB_HEX_MODES_ELASTIC_ISO \\"]
     for name, body in (("ELASTIC_ISO", gen_elastic(True)), ("ELASTIC_GEN", gen_elastic(False)),
-                       ("SCALAR_ISO", gen_scalar(True)), ("SCALAR_GEN", gen_scalar(False))):
+                       ("SCALAR_ISO", gen_scalar(True)), ("SCALAR_GEN", gen_scalar(False)),
+                       ("NRM_ELASTIC", gen_norm(True)), ("NRM_SCALAR", gen_norm(False)),
+                       ("SSS_ELASTIC", gen_sss(True)), ("SSS_SCALAR", gen_sss(False))):
         if name != "ELASTIC_ISO":
             parts.append(f"#define HB_HEX_MODES_{name} \\")
         lines = body.split("\n")

@@ -618,6 +618,113 @@ __global__ void __launch_bounds__(256, C == 3 ? HB_HEXZ_MINB3 : 2) k_hex_z(const
       for (int i = gridDim.x + tid; i < a.nred; i += nx) a.partials[i] = 0.0;
   }
 }
+
+// ---------------------------------------------------------------------------
+// Quadrature reductions of the Newton shell on the hex fast path
+// (solver.cpp:216-263 norms, :321-324 average stress): in the modal basis the
+// 8 Gauss-point patterns are orthogonal, so
+//   sum_q w |eps_q + E|^2 = 8w sum_modes |s_m e_m (+ E for the constant mode)|^2
+//   sum_q w C (eps_q + E)  = 8w C (s_0 e_sss + E)
+// (s_m = 1/(4h), 1/(4 sqrt3 h), 1/(12h) by class; sqrt(2)/2 on Mandel shear).
+// One element per thread, rows (y, z) strided over a fixed grid; per-block
+// partials (deterministic). Sums are returned without the 8w = h^3 factor.
+struct HexQArgs {
+  const double* u;
+  const double* halo_hi;  // dist: plane n0 of u
+  int dist;
+  const double* e;        // nullable macro strain (Mandel, m)
+  const uint8_t* phase;
+  const double* cmat;     // stress: n_phases x m x m column-major
+  double* partials;       // per block: 1 (norm) or m (stress)
+  double sc[6];
+  int n0, n1, n2;
+};
+
+template <int C, bool STRESS>
+__global__ void __launch_bounds__(256) k_hex_quad(const HexQArgs a) {
+  constexpr int M = C == 3 ? 6 : 3;
+  constexpr int NV = STRESS ? M : 1;
+  const int nx = a.n2;
+  const int64_t plane = (int64_t)a.n1 * nx, np = plane * a.n0;
+  double E[M], sc[6];
+#pragma unroll
+  for (int k = 0; k < M; ++k) E[k] = a.e ? a.e[k] : 0.0;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) sc[k] = a.sc[k];
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  const int nrows = a.n0 * a.n1;
+  for (int r = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < nrows * (nx / 32);
+       r += gridDim.x * (blockDim.x / 32)) {
+    // warp-granular work item: (row, 32-column segment)
+    const int row = r / (nx / 32), seg = r % (nx / 32);
+    const int z = row / a.n1, y = row % a.n1;
+    const int x = seg * 32 + (threadIdx.x & 31);
+    const int xp = x + 1 == nx ? 0 : x + 1, y1 = y + 1 == a.n1 ? 0 : y + 1;
+    const double* p0 = a.u + (int64_t)z * plane;
+    const double* p1;
+    int64_t cs1 = np;
+    if (z + 1 < a.n0) p1 = p0 + plane;
+    else if (a.dist) {
+      p1 = a.halo_hi;
+      cs1 = plane;
+    } else p1 = a.u;
+    double V[C][8];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      double xx[8];
+      xx[0] = __ldg(p0 + k * np + (int64_t)y * nx + x);
+      xx[1] = __ldg(p0 + k * np + (int64_t)y * nx + xp);
+      xx[2] = __ldg(p0 + k * np + (int64_t)y1 * nx + x);
+      xx[3] = __ldg(p0 + k * np + (int64_t)y1 * nx + xp);
+      xx[4] = __ldg(p1 + k * cs1 + (int64_t)y * nx + x);
+      xx[5] = __ldg(p1 + k * cs1 + (int64_t)y * nx + xp);
+      xx[6] = __ldg(p1 + k * cs1 + (int64_t)y1 * nx + x);
+      xx[7] = __ldg(p1 + k * cs1 + (int64_t)y1 * nx + xp);
+      modal_fwd(xx, V[k]);
+    }
+    if constexpr (!STRESS) {
+      double nacc = 0.0;
+      if constexpr (C == 3) {
+        HB_HEX_MODES_NRM_ELASTIC
+      } else {
+        HB_HEX_MODES_NRM_SCALAR
+      }
+      acc[0] += nacc;
+    } else {
+      double es[M];
+      if constexpr (C == 3) {
+        HB_HEX_MODES_SSS_ELASTIC
+      } else {
+        HB_HEX_MODES_SSS_SCALAR
+      }
+      const double* cm = a.cmat + (size_t)a.phase[(int64_t)z * plane + (int64_t)y * nx + x] * M * M;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) t = fma(__ldg(cm + j * M + i), es[j], t);
+        acc[i] += t;
+      }
+    }
+  }
+  __shared__ double red[NV][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double v = acc[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[i][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[threadIdx.x][w];
+    a.partials[(size_t)blockIdx.x * NV + threadIdx.x] = v;
+  }
+}
 }  // namespace
 
 static int hex_kz(const Grid& g) { return g.c == 3 ? HB_HEXZ_KZ3 : 16; }
@@ -813,6 +920,36 @@ void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, boo
 #undef HB_HEX
 #undef HB_HEX_T
   HB_CUDA(cudaGetLastError());
+}
+
+// Newton-shell quadrature sums on the hex fast path; false if not eligible.
+bool launch_hex_quad(const Grid& g, int mode, const double* u, const double* halo_hi, const double* e,
+                     const uint8_t* phase, const double* cmat, double* partials, cudaStream_t s) {
+  if (!hex_fast_eligible(g)) return false;
+  HexQArgs a;
+  a.u = u;
+  a.halo_hi = halo_hi;
+  a.dist = g.dist;
+  a.e = e;
+  a.phase = phase;
+  a.cmat = cmat;
+  a.partials = partials;
+  const double h = g.h[0], r2 = 0.70710678118654752440;
+  const double s0 = 1.0 / (4.0 * h), s1 = 1.0 / (4.0 * std::sqrt(3.0) * h), s2 = 1.0 / (12.0 * h);
+  const double scv[6] = {s0, s0 * r2, s1, s1 * r2, s2, s2 * r2};
+  for (int i = 0; i < 6; ++i) a.sc[i] = scv[i];
+  a.n0 = g.n0;
+  a.n1 = g.n1;
+  a.n2 = g.n2;
+  if (mode == 0) {
+    if (g.c == 3) k_hex_quad<3, false><<<kRedBlocks, 256, 0, s>>>(a);
+    else k_hex_quad<1, false><<<kRedBlocks, 256, 0, s>>>(a);
+  } else {
+    if (g.c == 3) k_hex_quad<3, true><<<kRedBlocks, 256, 0, s>>>(a);
+    else k_hex_quad<1, true><<<kRedBlocks, 256, 0, s>>>(a);
+  }
+  HB_CUDA(cudaGetLastError());
+  return true;
 }
 
 }  // namespace hb

@@ -254,6 +254,9 @@ def _newton_pair(hb, oracle_mod, dims, stencil, thermal, cm, ph, e, **kw):
 @pytest.mark.parametrize("name,dims,stencil,thermal", [("c1-like", (64, 64), "two-triangles", True),
                                                         ("c2-like", (24, 24, 24), "trilinear-hex", True),
                                                         ("c3-like", (16, 16, 16), "trilinear-hex", False),
+                                                        # hex fast path (modal K, TMA z-march, modal norms/stress)
+                                                        ("c3-fast", (16, 16, 32), "trilinear-hex", False),
+                                                        ("c2-fast", (16, 16, 32), "trilinear-hex", True),
                                                         ("c5-like", (96, 96), "two-triangles", True),
                                                         ("elastic-2d", (32, 24), "two-triangles", False)])
 def test_newton_matches_oracle(hb, oracle_mod, name, dims, stencil, thermal):
