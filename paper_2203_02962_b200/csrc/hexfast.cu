@@ -416,13 +416,13 @@ __device__ __forceinline__ void z_issue(const HexArgs& a, const int* its, int u,
   }
 }
 
-template <int C, bool ISO, int KZ, bool FE>
+template <int C, bool ISO, int KZ, bool FE, int NXT>
 __global__ void __launch_bounds__(256, C == 3 ? HB_HEXZ_MINB3 : 2) k_hex_z(const HexArgs a, const ZRun run) {
   if (a.st && a.st->done) return;
   constexpr int MS = mat_stride<C, ISO>();
   constexpr int D = kZDepth;
   extern __shared__ __align__(16) unsigned char zsm[];
-  const int nx = blockDim.x;  // == n2
+  const int nx = NXT ? NXT : blockDim.x;  // == n2 (compile-time for the common sizes: immediate smem offsets)
   const int nw = nx >> 5;
   const int sb = zslot_bytes<C>(nx);
   unsigned char* ring = zsm;                                        // [D][sb]
@@ -813,8 +813,8 @@ bool hex_fast_tables(const Grid& g, int n_phases, const double* cmats, std::vect
   return all_iso;
 }
 
-template <int C, bool ISO, int KZ, bool FE>
-static void launch_hex_z(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
+template <int C, bool ISO, int KZ, bool FE, int NXT>
+static void launch_hex_z_nx(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
   constexpr int MS = mat_stride<C, ISO>();
   const int nx = g.n2, nw = nx / 32;
   const int rows_total = g.n1 * (g.n0 / KZ);
@@ -833,20 +833,27 @@ static void launch_hex_z(const Grid& g, const HexArgs& a, int n_phases, cudaStre
     HB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   size_t smem = smem_for(2 * sms);
-  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hex_z<C, ISO, KZ, FE>, nx, smem));
+  HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hex_z<C, ISO, KZ, FE, NXT>, nx, smem));
   if (per_sm < 1) per_sm = 1;
   int grid = per_sm * sms;
   if (grid > rows_total) grid = rows_total;
   if (grid > kRedBlocks) grid = kRedBlocks;
   smem = smem_for(grid);
-  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ZRun run;
   run.rows_total = rows_total;
   run.grid = grid;
   run.list_cap = 2 * ((rows_total + grid - 1) / grid) + 4;
-  k_hex_z<C, ISO, KZ, FE><<<grid, nx, smem, s>>>(a, run);
+  k_hex_z<C, ISO, KZ, FE, NXT><<<grid, nx, smem, s>>>(a, run);
+}
+
+template <int C, bool ISO, int KZ, bool FE>
+static void launch_hex_z(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
+  if (g.n2 == 256) launch_hex_z_nx<C, ISO, KZ, FE, 256>(g, a, n_phases, s);
+  else if (g.n2 == 128) launch_hex_z_nx<C, ISO, KZ, FE, 128>(g, a, n_phases, s);
+  else launch_hex_z_nx<C, ISO, KZ, FE, 0>(g, a, n_phases, s);
 }
 
 void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, bool iso, cudaStream_t s) {
