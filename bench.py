@@ -204,9 +204,11 @@ def run_gpu(args, rank, world, local_rank):
     hb._check(lib.homfe_gpu_kernel_times(ctx_h, 20, ms.ctypes.data_as(C.POINTER(C.c_double))))
 
     # e2e: host buffers through the C ABI, copies inside the timed region
-    ph_host = np.ascontiguousarray(ph_local, dtype=np.uint8)
+    # pinned host buffers (the contract's H2D/D2H from page-locked memory)
+    ph_host = torch.empty(ph_local.size, dtype=torch.uint8, pin_memory=True).numpy()
+    ph_host[:] = np.ascontiguousarray(ph_local, dtype=np.uint8).ravel()
     cm = np.ascontiguousarray(np.stack(tangents).transpose(0, 2, 1), dtype=np.float64)
-    u_host = np.zeros(cfg.components * n_local)
+    u_host = torch.zeros(cfg.components * n_local, dtype=torch.float64, pin_memory=True).numpy()
     e2e_iters = 0
     torch.cuda.synchronize()
     if world > 1:

@@ -210,6 +210,7 @@ class _Context:
         key = (cm.tobytes(), ph.tobytes()) if ph.size <= 1 << 16 else None
         if key is not None and key == self._material_key:
             return
+        self._material_key = None  # a failed upload leaves the context without a material
         _check(lib.homfe_gpu_set_material(self.h, cm.shape[0], _dp(cm),
                                           ph.ctypes.data_as(C.POINTER(C.c_uint8))))
         self._material_key = key

@@ -562,32 +562,27 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
   if (n_phases < 1) throw ValidationError("materials: catalog is empty");
   if (n_phases > kMaxPhases) throw ValidationError("materials: at most 256 phases");
   for (int ph = 0; ph < n_phases; ++ph) check_spd(tangents + ph * m * m, m, "material");
-  std::vector<uint8_t> host;
-  const uint8_t* hp = phase;
-  if (device_phase) {
-    host.resize(c->g.np);
-    HB_CUDA(cudaMemcpy(host.data(), phase, c->g.np, cudaMemcpyDeviceToHost));
-    hp = host.data();
-  }
-  std::vector<int64_t> counts(256, 0);
-  for (int64_t p = 0; p < c->g.np; ++p) counts[hp[p]] += 1;
-  if (c->dist) {
-    // global phase counts (volume-mean reference) over the slabs
-    std::vector<double> cd(counts.begin(), counts.end());
-    HB_CUDA(cudaMemcpy(c->d_red, cd.data(), 256 * sizeof(double), cudaMemcpyHostToDevice));
-    HB_NCCL(ncclAllReduce(c->d_red, c->d_red, 256, ncclDouble, ncclSum, c->comm, c->stream));
-    HB_CUDA(cudaMemcpyAsync(cd.data(), c->d_red, 256 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    sync(c);
-    for (int v = 0; v < 256; ++v) counts[v] = (int64_t)cd[v];
-  }
-  for (int v = n_phases; v < 256; ++v)
-    if (counts[v]) throw ValidationError("materials: phase id " + std::to_string(v) + " missing from catalog");
-  counts.resize(n_phases);
-  c->counts = counts;
-  c->n_phases = n_phases;
-  c->catalog.assign(tangents, tangents + n_phases * m * m);
+  // phase map upload + per-phase voxel counts on the device (integer atomics:
+  // exact, order-independent)
   if (device_phase) HB_CUDA(cudaMemcpyAsync(c->d_phase, phase, c->g.np, cudaMemcpyDeviceToDevice, c->stream));
   else HB_CUDA(cudaMemcpyAsync(c->d_phase, phase, c->g.np, cudaMemcpyHostToDevice, c->stream));
+  launch_phase_counts(c->d_phase, c->g.np, reinterpret_cast<unsigned long long*>(c->d_red), c->stream);
+  std::vector<int64_t> counts(256, 0);
+  if (c->dist) {
+    // global phase counts (volume-mean reference) over the slabs
+    HB_NCCL(ncclAllReduce(c->d_red, c->d_red, 256, ncclUint64, ncclSum, c->comm, c->stream));
+  }
+  HB_CUDA(cudaMemcpyAsync(counts.data(), c->d_red, 256 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  for (int v = n_phases; v < 256; ++v)
+    if (counts[v]) {
+      c->n_phases = 0;  // the uploaded map is invalid: no material until the next valid call
+      c->catalog.clear();
+      throw ValidationError("materials: phase id " + std::to_string(v) + " missing from catalog");
+    }
+  counts.resize(n_phases);
+  c->counts = counts;
+  c->catalog.assign(tangents, tangents + n_phases * m * m);
   if (c->dist) {
     // phase plane z0-1 (previous rank's last plane), for the warm-up elements
     const Grid& g = c->g;
@@ -598,33 +593,36 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
     HB_NCCL(ncclRecv(c->d_ph_lo, plane, ncclUint8, prev, c->comm, c->stream));
     HB_NCCL(ncclGroupEnd());
   }
+  // per-phase tables in buffers sized for the full catalog (stable pointers:
+  // captured graphs stay valid unless the kernel configuration changes)
   const int ne = c->ne;
   std::vector<double> ke((size_t)n_phases * ne * ne);
   for (int ph = 0; ph < n_phases; ++ph) element_matrix(c->sp, c->g.d, c->g.c, tangents + ph * m * m, &ke[(size_t)ph * ne * ne]);
-  if (c->d_ke) cudaFree(c->d_ke);
-  if (c->d_fe) cudaFree(c->d_fe);
-  if (c->d_cmat) cudaFree(c->d_cmat);
-  c->d_ke = dalloc<double>(ke.size());
-  c->d_fe = dalloc<double>((size_t)n_phases * ne);
-  c->d_cmat = dalloc<double>((size_t)n_phases * m * m);
+  if (!c->d_ke) {
+    c->d_ke = dalloc<double>((size_t)kMaxPhases * ne * ne);
+    c->d_fe = dalloc<double>((size_t)kMaxPhases * ne);
+    c->d_cmat = dalloc<double>((size_t)kMaxPhases * m * m);
+    c->d_hexmat = dalloc<double>((size_t)kMaxPhases * (c->g.c == 3 ? 108 : 27));
+  }
   HB_CUDA(cudaMemcpyAsync(c->d_ke, ke.data(), ke.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   HB_CUDA(cudaMemcpyAsync(c->d_cmat, tangents, (size_t)n_phases * m * m * sizeof(double), cudaMemcpyHostToDevice,
                           c->stream));
   // modal-basis tables of the element-centric hex kernel
-  if (c->d_hexmat) cudaFree(c->d_hexmat);
-  c->d_hexmat = nullptr;
-  c->hex_fast = false;
+  bool hex_fast = false, hex_iso = false;
   const char* env = std::getenv("HOMFE_HEX_FAST");
   if (hex_fast_eligible(c->g) && (c->dist || !(env && env[0] == '0'))) {
     std::vector<double> iso, gen;
-    c->hex_iso = hex_fast_tables(c->g, n_phases, tangents, iso, gen);
-    const std::vector<double>& t = c->hex_iso ? iso : gen;
-    c->d_hexmat = dalloc<double>(t.size());
+    hex_iso = hex_fast_tables(c->g, n_phases, tangents, iso, gen);
+    const std::vector<double>& t = hex_iso ? iso : gen;
     HB_CUDA(cudaMemcpyAsync(c->d_hexmat, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    c->hex_fast = true;
+    hex_fast = true;
   }
   sync(c);
-  destroy_graphs(c);  // graphs capture material pointers
+  if (hex_fast != c->hex_fast || hex_iso != c->hex_iso || n_phases != c->n_phases)
+    destroy_graphs(c);  // graphs capture the kernel variant and the catalog size
+  c->hex_fast = hex_fast;
+  c->hex_iso = hex_iso;
+  c->n_phases = n_phases;
 }
 
 // ReferencePolicy::resolve (solver.cpp:99-118); volume mean from phase counts.

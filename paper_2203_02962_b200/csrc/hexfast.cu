@@ -576,7 +576,8 @@ __global__ void __launch_bounds__(256, C == 3 ? HB_HEXZ_MINB3 : 2) k_hex_z(const
 #pragma unroll
         for (int m = 0; m < 4; ++m) lo_s[(k * 4 + m) * nx + x] = Up[k][m];
       __syncthreads();  // edges visible; ring slot fully read
-      if (tid == 0 && u + D < nunits) z_issue<C, KZ>(a, its, u + D, sl, &full[slot]);
+      // producer role rotates over the warps (spreads the issue cost)
+      if (tid == ((u % nw) << 5) && u + D < nunits) z_issue<C, KZ>(a, its, u + D, sl, &full[slot]);
       if (j >= 2) {
         const int zi = j - 2;
         const int z = zb * KZ + zi;

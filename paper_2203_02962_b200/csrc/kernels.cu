@@ -570,6 +570,35 @@ void launch_quad_wsum(const Grid& g, const StencilParams& sp, const double* sf, 
   HB_CUDA(cudaGetLastError());
 }
 
+// per-phase voxel counts (MaterialMap::validate + volume-mean reference,
+// material.cpp:252-277): shared-memory histogram, exact integer atomics
+__global__ void __launch_bounds__(kBlock) k_phase_counts(const uint8_t* __restrict__ ph, int64_t n,
+                                                          unsigned long long* __restrict__ counts) {
+  __shared__ unsigned int hist[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+  __syncthreads();
+  const int64_t n4 = n / 4;
+  const uchar4* p4 = reinterpret_cast<const uchar4*>(ph);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const uchar4 v = p4[i];
+    atomicAdd(&hist[v.x], 1u);
+    atomicAdd(&hist[v.y], 1u);
+    atomicAdd(&hist[v.z], 1u);
+    atomicAdd(&hist[v.w], 1u);
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&hist[ph[i]], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (hist[i]) atomicAdd(&counts[i], (unsigned long long)hist[i]);
+}
+
+void launch_phase_counts(const uint8_t* ph, int64_t n, unsigned long long* counts, cudaStream_t s) {
+  HB_CUDA(cudaMemsetAsync(counts, 0, 256 * sizeof(unsigned long long), s));
+  k_phase_counts<<<kRedBlocks / 4, kBlock, 0, s>>>(ph, n, counts);
+  HB_CUDA(cudaGetLastError());
+}
+
 void launch_index_maps(const Grid& g, const StencilParams& sp, int64_t* nbr, cudaStream_t s) {
   k_index_maps<<<grid_for(g.np), kBlock, 0, s>>>(g, sp, nbr);
   HB_CUDA(cudaGetLastError());
