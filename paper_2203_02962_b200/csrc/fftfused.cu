@@ -259,6 +259,9 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
 #ifndef HB_INV_SPLIT
 #define HB_INV_SPLIT 2
 #endif
+#ifndef HB_INV_GROUPUPD
+#define HB_INV_GROUPUPD 1
+#endif
 template <int NP>
 __global__ void __launch_bounds__(NP, HB_INV_MINB) k_plane_inv(const PlaneArgs a) {
   constexpr int P = NP / 2 + 1;
@@ -343,43 +346,97 @@ __global__ void __launch_bounds__(NP, HB_INV_MINB) k_plane_inv(const PlaneArgs a
     fft::group_sync();
     fft::fft4step_regs<NP, true>(u, buf, t, tws);
   }
-  __syncthreads();
   const int64_t plane = (int64_t)comp * a.np + (int64_t)i0 * NP * NP + (int64_t)rank * 32 * NP;
-  auto zval = [&](int idx) {
-    const int row = idx / H, c2 = idx % H;
-    const double2* zb = rows + (row & ~1) * P + 2 * c2;
-    const double2 z0 = zb[0], z1 = zb[1];
-    return (row & 1) ? make_double2(z0.y, z1.y) : make_double2(z0.x, z1.x);
-  };
+#if HB_INV_GROUPUPD
+  // each transform group updates its own row pair as soon as its inverse is
+  // done (no block barrier: early groups' loads overlap later groups' FFTs)
   if (a.dbg & 256) return;  // profiling: no p / x traffic
+  {
+    const double2* zb = rows + (2 * g) * P;
+    const int64_t r0 = plane + (int64_t)(2 * g) * NP;
+    if (a.mode == kModePcg) {
+      const double alpha = a.st->alpha, beta = a.st->beta;
+      const int conv = a.st->converged;
+      constexpr int NC = NP / TPF;  // columns per thread
+      constexpr int CH = NC / HB_INV_SPLIT;
+#pragma unroll
+      for (int hh = 0; hh < HB_INV_SPLIT; ++hh) {
+        double pv[2][CH], xv[2][CH];
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const int n = t + TPF * (hh * CH + i);
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            pv[r][i] = a.p[r0 + r * NP + n];
+            xv[r][i] = a.x[r0 + r * NP + n];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          const int n = t + TPF * (hh * CH + i);
+          const double2 z = zb[n];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) a.x[r0 + r * NP + n] = fma(alpha, pv[r][i], xv[r][i]);
+          if (!conv) {
+            a.p[r0 + n] = fma(beta, pv[0][i], z.x);
+            a.p[r0 + NP + n] = fma(beta, pv[1][i], z.y);
+          }
+        }
+      }
+    } else {
+      double* out = (a.mode == kModeInit ? a.p : a.z) + r0;
+#pragma unroll
+      for (int i = 0; i < NP / TPF; ++i) {
+        const int n = t + TPF * i;
+        const double2 z = zb[n];
+        out[n] = z.x;
+        out[NP + n] = z.y;
+      }
+    }
+  }
+  return;
+#endif
+  __syncthreads();
+  // row pair (2 rp, 2 rp + 1) at column n is z = rows[2 rp P + n] (two-for-one
+  // packing): thread n reads it conflict-free and updates both rows' column n
+  // (coalesced 8-byte global accesses)
+  if (a.dbg & 256) return;  // profiling: no p / x traffic
+  const int n = tid;
   if (a.mode == kModePcg) {
-    double2* p2 = reinterpret_cast<double2*>(a.p + plane);
-    double2* x2 = reinterpret_cast<double2*>(a.x + plane);
+    double* pp = a.p + plane + n;
+    double* xp = a.x + plane + n;
     const double alpha = a.st->alpha, beta = a.st->beta;
     const int conv = a.st->converged;
-    constexpr int HP = PT / HB_INV_SPLIT;  // chunks bound the live registers
+    constexpr int RP = 16 / HB_INV_SPLIT;  // row pairs per chunk (bounds live registers)
 #pragma unroll
     for (int hh = 0; hh < HB_INV_SPLIT; ++hh) {
-      double2 pv[HP], xv[HP];
+      double pv[2 * RP], xv[2 * RP];
 #pragma unroll
-      for (int i = 0; i < HP; ++i) {
-        pv[i] = p2[tid + (hh * HP + i) * NP];
-        xv[i] = x2[tid + (hh * HP + i) * NP];
+      for (int i = 0; i < 2 * RP; ++i) {
+        const int r = hh * 2 * RP + i;
+        pv[i] = pp[r * NP];
+        xv[i] = xp[r * NP];
       }
 #pragma unroll
-      for (int i = 0; i < HP; ++i) {
-        const int idx = tid + (hh * HP + i) * NP;
-        x2[idx] = make_double2(fma(alpha, pv[i].x, xv[i].x), fma(alpha, pv[i].y, xv[i].y));
+      for (int i = 0; i < RP; ++i) {
+        const int rp = hh * RP + i;
+        const double2 z = rows[2 * rp * P + n];
+        xp[(2 * rp) * NP] = fma(alpha, pv[2 * i], xv[2 * i]);
+        xp[(2 * rp + 1) * NP] = fma(alpha, pv[2 * i + 1], xv[2 * i + 1]);
         if (!conv) {
-          const double2 zv = zval(idx);
-          p2[idx] = make_double2(fma(beta, pv[i].x, zv.x), fma(beta, pv[i].y, zv.y));
+          pp[(2 * rp) * NP] = fma(beta, pv[2 * i], z.x);
+          pp[(2 * rp + 1) * NP] = fma(beta, pv[2 * i + 1], z.y);
         }
       }
     }
   } else {
-    double2* out = reinterpret_cast<double2*>((a.mode == kModeInit ? a.p : a.z) + plane);
+    double* out = (a.mode == kModeInit ? a.p : a.z) + plane + n;
 #pragma unroll
-    for (int i = 0; i < PT; ++i) out[tid + i * NP] = zval(tid + i * NP);
+    for (int rp = 0; rp < 16; ++rp) {
+      const double2 z = rows[2 * rp * P + n];
+      out[(2 * rp) * NP] = z.x;
+      out[(2 * rp + 1) * NP] = z.y;
+    }
   }
 }
 
