@@ -84,6 +84,84 @@ def gen_scalar(iso):
     return "\n".join(out)
 
 
+def gen_fold(elastic, iso):
+    """Mode code for the z-march kernel with the residual folded into the
+    z-adjoint: contribution t to modal slot (k, v) adds +-t to A[k][v % 4]
+    (lower face, minus for v >= 4) and t to B[k][v % 4] (upper face). A is
+    seeded by the caller; B is assigned on its first contribution. Scaled
+    rows (isotropic shear, scalar) go straight into FMAs."""
+    out = []
+    seen = set()
+
+    def acc(k, v, t=None, scale=None, e=None):
+        m = v % 4
+        sgn = "-" if v >= 4 else ""
+        first = (k, m) not in seen
+        seen.add((k, m))
+        if t is not None:
+            out.append(f"    A[{k}][{m}] {'-' if v >= 4 else '+'}= {t};")
+            out.append(f"    B[{k}][{m}] {'=' if first else '+='} {t};")
+        else:
+            out.append(f"    A[{k}][{m}] = fma({sgn}{scale}, {e}, A[{k}][{m}]);")
+            if first:
+                out.append(f"    B[{k}][{m}] = {scale} * {e};")
+            else:
+                out.append(f"    B[{k}][{m}] = fma({scale}, {e}, B[{k}][{m}]);")
+
+    if elastic:
+        for md, inc in enumerate(INC3):
+            cls = CLASS[md]
+            rows = sorted({e for e, _, _ in inc})
+            out.append(f"  {{  /* mode {MODES[md]} */")
+            for e in rows:
+                terms = [f"V[{k}][{v}]" for (ee, k, v) in inc if ee == e]
+                out.append(f"    const double e{e} = {' + '.join(terms)};")
+            if iso:
+                out.append(f"    const double fl = mat[{cls * 3}], f2m = mat[{cls * 3 + 1}], fm = mat[{cls * 3 + 2}];")
+                normals = [e for e in rows if e < 3]
+                if normals:
+                    out.append(f"    const double lt = fl * ({' + '.join(f'e{e}' for e in normals)});")
+                for e in rows:
+                    if e < 3:
+                        out.append(f"    const double t{e} = fma(f2m, e{e}, lt);")
+                for (e, k, v) in inc:
+                    if e < 3:
+                        acc(k, v, t=f"t{e}")
+                    else:
+                        acc(k, v, scale="fm", e=f"e{e}")
+            else:
+                for i in rows:
+                    a = None
+                    for j in rows:
+                        term = f"mat[{cls * 36 + i * 6 + j}]"
+                        a = f"{term} * e{j}" if a is None else f"fma({term}, e{j}, {a})"
+                    out.append(f"    const double t{i} = {a};")
+                for (e, k, v) in inc:
+                    acc(k, v, t=f"t{e}")
+            out.append("  }")
+    else:
+        for md, inc in enumerate(INCS):
+            cls = CLASS[md]
+            dirs = [j for j, _ in inc]
+            out.append(f"  {{  /* mode {MODES[md]} */")
+            for j, v in inc:
+                out.append(f"    const double g{j} = V[0][{v}];")
+            if iso:
+                out.append(f"    const double kk = mat[{cls}];")
+                for j, v in inc:
+                    acc(0, v, scale="kk", e=f"g{j}")
+            else:
+                for j, v in inc:
+                    a = None
+                    for jj in dirs:
+                        term = f"mat[{cls * 9 + j * 3 + jj}]"
+                        a = f"{term} * g{jj}" if a is None else f"fma({term}, g{jj}, {a})"
+                    out.append(f"    const double q{j} = {a};")
+                    acc(0, v, t=f"q{j}")
+            out.append("  }")
+    return "\n".join(out)
+
+
 def gen_norm(elastic):
     """sum_q |eps_q + E|^2 / (8 w) over the quad modes (orthogonal patterns):
     mode m contributes sum_rows (sc * e_row (+ E_row for sss))^2, with
@@ -123,6 +201,8 @@ def main():
              "#define HB_HEX_MODES_ELASTIC_ISO \\"]
     for name, body in (("ELASTIC_ISO", gen_elastic(True)), ("ELASTIC_GEN", gen_elastic(False)),
                        ("SCALAR_ISO", gen_scalar(True)), ("SCALAR_GEN", gen_scalar(False)),
+                       ("FOLD_ELASTIC_ISO", gen_fold(True, True)), ("FOLD_ELASTIC_GEN", gen_fold(True, False)),
+                       ("FOLD_SCALAR_ISO", gen_fold(False, True)), ("FOLD_SCALAR_GEN", gen_fold(False, False)),
                        ("NRM_ELASTIC", gen_norm(True)), ("NRM_SCALAR", gen_norm(False)),
                        ("SSS_ELASTIC", gen_sss(True)), ("SSS_SCALAR", gen_sss(False))):
         if name != "ELASTIC_ISO":

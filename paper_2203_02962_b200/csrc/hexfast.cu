@@ -511,30 +511,25 @@ __global__ void __launch_bounds__(256, C == 3 ? HB_HEXZ_MINB3 : 2) k_hex_z(const
           }
         // modal residual folded straight into the z-adjoint: A = lower face
         // (seeded with the previous element's upper face), B = upper face
-        double A[C][4], B[C][4];
+        double A[C][4], B[C][4];  // B: assigned by its first contribution
 #pragma unroll
         for (int k = 0; k < C; ++k)
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            A[k][m] = zc[k][m];
-            B[k][m] = 0.0;
-          }
+          for (int m = 0; m < 4; ++m) A[k][m] = zc[k][m];
         const double* mat = matp + ph * MS;
-#define HB_ACC(k, v, t) acc_fold<v>(A[k], B[k], (t))
         if constexpr (C == 3) {
           if constexpr (ISO) {
-            HB_HEX_MODES_ELASTIC_ISO
+            HB_HEX_MODES_FOLD_ELASTIC_ISO
           } else {
-            HB_HEX_MODES_ELASTIC_GEN
+            HB_HEX_MODES_FOLD_ELASTIC_GEN
           }
         } else {
           if constexpr (ISO) {
-            HB_HEX_MODES_SCALAR_ISO
+            HB_HEX_MODES_FOLD_SCALAR_ISO
           } else {
-            HB_HEX_MODES_SCALAR_GEN
+            HB_HEX_MODES_FOLD_SCALAR_GEN
           }
         }
-#undef HB_ACC
         if constexpr (FE) {  // element load, moved to the modal basis (fwd / 8)
 #pragma unroll
           for (int k = 0; k < C; ++k) {
