@@ -236,9 +236,18 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
   constexpr int NG = t_groups(NP);
   const int64_t zs = (int64_t)a.L.nzl * kTG;
   double2* tdst = a.T + (int64_t)(rank * (16 / kTG)) * zs + i0 * kTG;  // this CTA's 16 columns
-  for (int idx = tid; idx < ncol * NP; idx += NP) {
-    const int k1 = idx / ncol, j = idx % ncol + first;
-    tdst[(int64_t)a.L.row1(comp, k1) * NG * zs + (j / kTG) * zs + (j % kTG)] = rows[j * (NP + 1) + k1];
+  if (first == 0) {
+    // 16 columns: shifts instead of divisions
+#pragma unroll 4
+    for (int idx = tid; idx < 16 * NP; idx += NP) {
+      const int k1 = idx >> 4, j = idx & 15;
+      tdst[(int64_t)a.L.row1(comp, k1) * NG * zs + (j / kTG) * zs + (j % kTG)] = rows[j * (NP + 1) + k1];
+    }
+  } else {
+    for (int idx = tid; idx < ncol * NP; idx += NP) {
+      const int k1 = idx / ncol, j = idx % ncol + first;
+      tdst[(int64_t)a.L.row1(comp, k1) * NG * zs + (j / kTG) * zs + (j % kTG)] = rows[j * (NP + 1) + k1];
+    }
   }
   if (rank == 0 && g == 0) {
     // split the paired real columns k2 = 0 and k2 = NP/2
