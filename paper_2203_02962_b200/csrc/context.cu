@@ -99,6 +99,8 @@ struct homfe_ctx {
   double* d_fe = nullptr;
   double* d_cmat = nullptr;
   double* d_hexmat = nullptr;       // modal-basis material table (hexfast.cu)
+  bool no_fast2d = false;           // HOMFE_FAST2D=0: generic 2-D element kernel
+  double* d_tri = nullptr;          // TwoTriangles flux tables (quad2d.cu)
   bool hex_fast = false, hex_iso = false;
   // vectors
   double *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_ap = nullptr, *d_z = nullptr, *d_u = nullptr;
@@ -248,6 +250,7 @@ void apply_K(homfe_ctx* c, const double* u, double* out, const double* fe, doubl
   if (c->dist) exchange_halo(c, u, s);
   ElemArgs a{u, c->d_hlo, c->d_hhi, c->d_ph_lo, out, c->d_phase, c->d_ke, c->n_phases, fe, scale, partials, st};
   if (c->hex_fast) launch_hex_fast(c->g, a, c->d_hexmat, c->hex_iso, s);
+  else if (elem2d_eligible(c->g) && !c->no_fast2d) launch_elem2d(c->g, a, c->d_tri, s);
   else launch_apply_elem(c->g, a, s);
   c->launches += 1;
 }
@@ -607,6 +610,12 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
   HB_CUDA(cudaMemcpyAsync(c->d_ke, ke.data(), ke.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   HB_CUDA(cudaMemcpyAsync(c->d_cmat, tangents, (size_t)n_phases * m * m * sizeof(double), cudaMemcpyHostToDevice,
                           c->stream));
+  if (c->g.d == 2 && c->g.kind == 1) {
+    std::vector<double> tt;
+    elem2d_tri_tables(c->g, n_phases, tangents, tt);
+    if (!c->d_tri) c->d_tri = dalloc<double>((size_t)kMaxPhases * 12);
+    HB_CUDA(cudaMemcpyAsync(c->d_tri, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  }
   // modal-basis tables of the element-centric hex kernel
   bool hex_fast = false, hex_iso = false;
   const char* env = std::getenv("HOMFE_HEX_FAST");
@@ -932,6 +941,7 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
       p.tab[a] = ctx->d_tab[a];
     }
     if (const char* env = std::getenv("HOMFE_NO_WHILE_GRAPH")) ctx->use_while = ctx->use_while && env[0] == '0';
+    if (const char* env = std::getenv("HOMFE_FAST2D")) ctx->no_fast2d = env[0] == '0';
     const char* fenv = std::getenv("HOMFE_FUSED_FFT");
     const bool fused_ok = fused_fft_eligible(g) && g.n1 % G == 0;
     if (dist && !fused_ok) throw ValidationError("slab mode: plane size must be 128 or 256 and n0 in {64,128,256}");
@@ -1027,7 +1037,7 @@ int homfe_gpu_destroy(homfe_ctx* c) {
   destroy_graphs(c);
   if (c->fwd) cufftDestroy(c->fwd);
   if (c->inv) cufftDestroy(c->inv);
-  double* bufs[] = {c->d_x, c->d_r, c->d_p, c->d_ap, c->d_z, c->d_u, c->d_ke, c->d_fe, c->d_cmat, c->d_hexmat,
+  double* bufs[] = {c->d_x, c->d_r, c->d_p, c->d_ap, c->d_z, c->d_u, c->d_ke, c->d_fe, c->d_cmat, c->d_hexmat, c->d_tri,
                     c->d_quad, c->d_partials, c->d_scal, c->d_hist, c->d_e};
   for (double* b : bufs)
     if (b) cudaFree(b);

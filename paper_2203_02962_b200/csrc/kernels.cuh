@@ -35,6 +35,10 @@ bool hex_fast_eligible(const Grid& g);
 bool hex_fast_tables(const Grid& g, int n_phases, const double* cmats, std::vector<double>& iso,
                      std::vector<double>& gen);
 void launch_hex_fast(const Grid& g, const ElemArgs& a, const double* d_mat, bool iso, cudaStream_t s);
+// 2-D one-node pixel stencils: warp-strip element-matrix K u (quad2d.cu)
+bool elem2d_eligible(const Grid& g);
+void elem2d_tri_tables(const Grid& g, int n_phases, const double* cmats, std::vector<double>& tab);
+void launch_elem2d(const Grid& g, const ElemArgs& a, const double* d_tri, cudaStream_t s);
 void launch_phase_counts(const uint8_t* ph, int64_t n, unsigned long long* counts, cudaStream_t s);
 // mode 0: sum_q w |D u + e|^2 / h^3 (1 partial per block); 1: sum_q w C (D u + e) / h^3 (m per block)
 bool launch_hex_quad(const Grid& g, int mode, const double* u, const double* halo_hi, const double* e,
