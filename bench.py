@@ -265,8 +265,8 @@ def run_gpu(args, rank, world, local_rank):
                      "stencil K apply (k_apply_elem)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
                      "peak_source": peak_kind, "bytes_per_launch": bytes_k},
-        "kernel_ms": ({"apply_K": ms[0], "update_xr": ms[1], "fft_fwd": ms[2], "spectral": ms[3],
-                       "fft_inv": ms[4], "update_p": ms[5], "scalars": ms[6], "sum": ms[7]} if ms[2] >= 0 else
+        "kernel_ms": ({"apply_K": ms[0], "update_r": ms[1], "fft_fwd": ms[2], "spectral": ms[3],
+                       "fft_inv": ms[4], "update_xp": ms[5], "scalars": ms[6], "sum": ms[7]} if ms[2] >= 0 else
                       {"apply_K": ms[0], "pass1_r_update_plane_fft": ms[1], "pass2_pencil_fft_solve": ms[3],
                        "pass3_plane_ifft_update": ms[5], "scalars": ms[6], "sum": ms[7]}),
         "e2e": {"value": e2e_value, "unit": "DOF*it/s",

@@ -371,13 +371,13 @@ void body_sequence(homfe_ctx* c, cudaStream_t s, bool cond, cudaGraphConditional
   }
   apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s);
   launch_pcg_alpha(c->d_st, c->d_partials, s);
-  launch_update_xr(c->d_x, c->d_r, c->d_p, c->d_ap, n, c->d_st, s);
+  launch_update_r(c->d_r, c->d_ap, n, c->d_st, s);
   fft_forward(c, c->d_r, s);
   launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s);
   launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
   fft_inverse(c, c->d_z, s);
-  if (cond) launch_update_p_cond(c->d_p, c->d_z, n, c->d_st, h, s);
-  else launch_update_p(c->d_p, c->d_z, n, c->d_st, s);
+  if (cond) launch_update_xp_cond(c->d_x, c->d_p, c->d_z, n, c->d_st, h, s);
+  else launch_update_xp(c->d_x, c->d_p, c->d_z, n, c->d_st, s);
 }
 
 void write_state(homfe_ctx* c, double eta, int it_max, int active = 0) {
@@ -1293,11 +1293,11 @@ int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
       cudaEventDestroy(b);
       return;
     }
-    ms[1] = timeit([&] { launch_update_xr(c->d_x, c->d_r, c->d_p, c->d_ap, n, c->d_st, s); });
+    ms[1] = timeit([&] { launch_update_r(c->d_r, c->d_ap, n, c->d_st, s); });
     ms[2] = timeit([&] { fft_forward(c, c->d_r, s); });
     ms[3] = timeit([&] { launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s); });
     ms[4] = timeit([&] { fft_inverse(c, c->d_z, s); });
-    ms[5] = timeit([&] { launch_update_p(c->d_p, c->d_z, n, c->d_st, s); });
+    ms[5] = timeit([&] { launch_update_xp(c->d_x, c->d_p, c->d_z, n, c->d_st, s); });
     ms[6] = timeit([&] {
       launch_pcg_alpha(c->d_st, c->d_partials, s);
       launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);

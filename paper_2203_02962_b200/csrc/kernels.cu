@@ -427,14 +427,13 @@ __global__ void k_pcg_alpha(PcgState* st, const double* partials, int nblocks) {
   }
 }
 
-__global__ void k_update_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
-                            const double* __restrict__ ap, int64_t n, const PcgState* st) {
+// r -= alpha Ap (solver.cpp:81-82; x is updated with p in k_update_xp, which
+// reads p anyway: one vector pass fewer per iteration)
+__global__ void k_update_r(double* __restrict__ r, const double* __restrict__ ap, int64_t n, const PcgState* st) {
   if (!st->active) return;
   const double alpha = st->alpha;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    x[i] = fma(alpha, p[i], x[i]);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     r[i] = fma(-alpha, ap[i], r[i]);
-  }
 }
 
 // rz_next, history, stopping test, beta (solver.cpp:84-93).
@@ -482,25 +481,35 @@ __global__ void k_pcg_beta_cond(PcgState* st, const double* partials, int nblock
   }
 }
 
-__global__ void k_update_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, const PcgState* st) {
-  if (st->done) return;
-  const double beta = st->beta;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], z[i]);
+// x += alpha p (this iteration), p = z + beta p unless the loop just ended
+// (solver.cpp:81, 93)
+__global__ void k_update_xp(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                            const PcgState* st) {
+  if (!st->active) return;
+  const double alpha = st->alpha, beta = st->beta;
+  const bool upd = !st->done;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double pv = p[i];
+    x[i] = fma(alpha, pv, x[i]);
+    if (upd) p[i] = fma(beta, pv, z[i]);
+  }
 }
 
 __global__ void k_set_while(cudaGraphConditionalHandle h, const PcgState* st) {
   if (threadIdx.x == 0 && blockIdx.x == 0) cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
 
-__global__ void k_update_p_cond(double* __restrict__ p, const double* __restrict__ z, int64_t n,
-                                const PcgState* st, cudaGraphConditionalHandle h) {
+__global__ void k_update_xp_cond(double* __restrict__ x, double* __restrict__ p, const double* __restrict__ z,
+                                 int64_t n, const PcgState* st, cudaGraphConditionalHandle h) {
   const int done = st->done;
   if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(h, done ? 0u : 1u);
-  if (done) return;
-  const double beta = st->beta;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = fma(beta, p[i], z[i]);
+  if (!st->active) return;
+  const double alpha = st->alpha, beta = st->beta;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double pv = p[i];
+    x[i] = fma(alpha, pv, x[i]);
+    if (!done) p[i] = fma(beta, pv, z[i]);
+  }
 }
 
 int grid_for(int64_t n) {
@@ -648,9 +657,8 @@ void launch_pcg_alpha(PcgState* st, const double* partials, cudaStream_t s, int 
   k_pcg_alpha<<<1, 1024, 0, s>>>(st, partials, nblocks);
   HB_CUDA(cudaGetLastError());
 }
-void launch_update_xr(double* x, double* r, const double* p, const double* ap, int64_t n, const PcgState* st,
-                      cudaStream_t s) {
-  k_update_xr<<<grid_for(n), kBlock, 0, s>>>(x, r, p, ap, n, st);
+void launch_update_r(double* r, const double* ap, int64_t n, const PcgState* st, cudaStream_t s) {
+  k_update_r<<<grid_for(n), kBlock, 0, s>>>(r, ap, n, st);
   HB_CUDA(cudaGetLastError());
 }
 void launch_pcg_beta(PcgState* st, const double* partials, double* hist, cudaStream_t s, int nblocks) {
@@ -662,17 +670,17 @@ void launch_pcg_beta_cond(PcgState* st, const double* partials, double* hist, cu
   k_pcg_beta_cond<<<1, 1024, 0, s>>>(st, partials, kRedBlocks, hist, h);
   HB_CUDA(cudaGetLastError());
 }
-void launch_update_p(double* p, const double* z, int64_t n, const PcgState* st, cudaStream_t s) {
-  k_update_p<<<grid_for(n), kBlock, 0, s>>>(p, z, n, st);
+void launch_update_xp(double* x, double* p, const double* z, int64_t n, const PcgState* st, cudaStream_t s) {
+  k_update_xp<<<grid_for(n), kBlock, 0, s>>>(x, p, z, n, st);
   HB_CUDA(cudaGetLastError());
 }
 void launch_set_while(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s) {
   k_set_while<<<1, 32, 0, s>>>(h, st);
   HB_CUDA(cudaGetLastError());
 }
-void launch_update_p_cond(double* p, const double* z, int64_t n, const PcgState* st, cudaGraphConditionalHandle h,
-                          cudaStream_t s) {
-  k_update_p_cond<<<grid_for(n), kBlock, 0, s>>>(p, z, n, st, h);
+void launch_update_xp_cond(double* x, double* p, const double* z, int64_t n, const PcgState* st,
+                           cudaGraphConditionalHandle h, cudaStream_t s) {
+  k_update_xp_cond<<<grid_for(n), kBlock, 0, s>>>(x, p, z, n, st, h);
   HB_CUDA(cudaGetLastError());
 }
 

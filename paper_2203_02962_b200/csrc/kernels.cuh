@@ -72,13 +72,12 @@ void launch_axpy(double* y, double a, const double* x, int64_t n, cudaStream_t s
 // PCG steps (solver.cpp:62-94) with device-resident scalars.
 void launch_pcg_init(PcgState* st, const double* partials, double* hist, cudaStream_t s, int nblocks = kRedBlocks);
 void launch_pcg_alpha(PcgState* st, const double* partials, cudaStream_t s, int nblocks = kRedBlocks);
-void launch_update_xr(double* x, double* r, const double* p, const double* ap, int64_t n,
-                      const PcgState* st, cudaStream_t s);
+void launch_update_r(double* r, const double* ap, int64_t n, const PcgState* st, cudaStream_t s);
 void launch_pcg_beta(PcgState* st, const double* partials, double* hist, cudaStream_t s, int nblocks = kRedBlocks);
-void launch_update_p(double* p, const double* z, int64_t n, const PcgState* st, cudaStream_t s);
+void launch_update_xp(double* x, double* p, const double* z, int64_t n, const PcgState* st, cudaStream_t s);
 void launch_set_while(cudaGraphConditionalHandle h, const PcgState* st, cudaStream_t s);
-void launch_update_p_cond(double* p, const double* z, int64_t n, const PcgState* st,
-                          cudaGraphConditionalHandle h, cudaStream_t s);
+void launch_update_xp_cond(double* x, double* p, const double* z, int64_t n, const PcgState* st,
+                           cudaGraphConditionalHandle h, cudaStream_t s);
 
 // Spectral solve z_hat = K_ref_hat(xi)^+ r_hat / N_p (precond.cpp:126-162),
 // with the analytic symbol of the Nn = 1 stencils.
