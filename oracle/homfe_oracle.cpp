@@ -1225,4 +1225,308 @@ int or_newton_solve(const or_grid* g, int32_t thermal, int32_t n_phases, const d
   });
 }
 
+
+// ---------------------------------------------------------------- J2 (f1)
+namespace {
+
+const double kS32 = 1.2247448713915890491;  // sqrt(3/2)
+
+// material.cpp:122-171 restated: total strain e6 (3-D Mandel), state
+// g = [plastic strain (6), accumulated (1)].
+void j2_return6(double k, double gm, double tau0, double hard, const double* e6, const double* g, double* s6,
+                double* t6 /* 6x6 col-major or null */, double* gn /* 7 or null */) {
+  double ee[6];
+  for (int i = 0; i < 6; ++i) ee[i] = e6[i] - g[i];
+  const double tr = ee[0] + ee[1] + ee[2];
+  double dev[6];
+  for (int i = 0; i < 6; ++i) dev[i] = ee[i] - (i < 3 ? tr / 3.0 : 0.0);
+  double st[6];
+  for (int i = 0; i < 6; ++i) st[i] = 2.0 * gm * dev[i];
+  for (int i = 0; i < 6; ++i) s6[i] = st[i] + (i < 3 ? k * tr : 0.0);
+  double sn2 = 0.0;
+  for (int i = 0; i < 6; ++i) sn2 += st[i] * st[i];
+  const double s_norm = std::sqrt(sn2);
+  const double q_tr = kS32 * s_norm;
+  const double f = q_tr - (tau0 + hard * g[6]);
+  auto proj = [](int i, int j, double& vol, double& dv) {
+    vol = (i < 3 && j < 3) ? 1.0 / 3.0 : 0.0;
+    dv = (i == j ? 1.0 : 0.0) - vol;
+  };
+  if (f <= 0.0) {
+    if (t6)
+      for (int j = 0; j < 6; ++j)
+        for (int i = 0; i < 6; ++i) {
+          double vol, dv;
+          proj(i, j, vol, dv);
+          t6[j * 6 + i] = 3.0 * k * vol + 2.0 * gm * dv;
+        }
+    if (gn)
+      for (int i = 0; i < 7; ++i) gn[i] = g[i];
+    return;
+  }
+  const double dg = f / (3.0 * gm + hard);
+  double nh[6];
+  for (int i = 0; i < 6; ++i) nh[i] = st[i] / s_norm;
+  for (int i = 0; i < 6; ++i) s6[i] -= 2.0 * gm * dg * kS32 * nh[i];
+  if (gn) {
+    for (int i = 0; i < 6; ++i) gn[i] = g[i] + dg * kS32 * nh[i];
+    gn[6] = g[6] + dg;
+  }
+  if (t6) {
+    const double a = 1.0 - 3.0 * gm * dg / q_tr;
+    const double b = 6.0 * gm * gm * (1.0 / (3.0 * gm + hard) - dg / q_tr);
+    for (int j = 0; j < 6; ++j)
+      for (int i = 0; i < 6; ++i) {
+        double vol, dv;
+        proj(i, j, vol, dv);
+        t6[j * 6 + i] = 3.0 * k * vol + 2.0 * gm * a * dv - b * nh[i] * nh[j];
+      }
+  }
+}
+
+// MaterialModel::evaluate (material.cpp:173-226) for a J2 model in d dims.
+void j2_eval(int d, double k, double gm, double tau0, double hard, const double* eps, const double* g, double* sigma,
+             double* tangent, double* gn) {
+  const int m = d == 3 ? 6 : 3;
+  for (int i = 0; i < m; ++i)
+    if (!std::isfinite(eps[i])) throw NumericalError("evaluate: non-finite strain input");
+  double e6[6] = {0, 0, 0, 0, 0, 0}, s6[6], t6[36];
+  if (d == 3) {
+    for (int i = 0; i < 6; ++i) e6[i] = eps[i];
+  } else {
+    e6[0] = eps[0];
+    e6[1] = eps[1];
+    e6[5] = eps[2];
+  }
+  j2_return6(k, gm, tau0, hard, e6, g, s6, tangent ? t6 : nullptr, gn);
+  if (d == 3) {
+    for (int i = 0; i < 6; ++i) sigma[i] = s6[i];
+    if (tangent)
+      for (int i = 0; i < 36; ++i) tangent[i] = t6[i];
+  } else {
+    const int idx[3] = {0, 1, 5};
+    for (int a = 0; a < 3; ++a) sigma[a] = s6[idx[a]];
+    if (tangent)
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) tangent[b * 3 + a] = t6[idx[b] * 6 + idx[a]];
+  }
+}
+
+}  // namespace
+
+int or_j2_evaluate(int32_t d, double bulk, double shear, double yield_stress, double hardening, const double* eps,
+                   const double* g_in, double* sigma, double* tangent, double* g_new) {
+  return guarded([&] {
+    if (!(bulk > 0.0) || !(shear > 0.0) || !(yield_stress > 0.0))
+      throw ValidationError("j2_plastic: K, G and tau_y0 must be > 0");
+    if (hardening < 0.0) throw ValidationError("j2_plastic: H must be >= 0");
+    if (d != 2 && d != 3) throw ValidationError("j2_plastic: dimension must be 2 or 3");
+    j2_eval(d, bulk, shear, yield_stress, hardening, eps, g_in, sigma, tangent, g_new);
+  });
+}
+
+int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
+                           const uint8_t* phase, const double* g0_in, const double* e, const or_solve_cfg* cfg,
+                           const double* warm_u, double* u_out, double* g_out, double* avg_out, or_report* rep) {
+  return guarded([&] {
+    const auto t_total = Clock::now();
+    const Layout l = make_layout(g);
+    const int d = l.d, c = thermal ? 1 : d, m = grad_components(d, c), nq = l.nq();
+    if (!(cfg->eta_newton > 0.0 && cfg->eta_newton < 1.0) ||
+        !(cfg->eta_cg > 0.0 && cfg->eta_cg < 1.0))
+      throw ValidationError("solver: tolerances must lie in (0,1)");
+    if (cfg->max_newton < 1 || cfg->max_cg < 1) throw ValidationError("solver: iteration caps must be >= 1");
+    if (!(cfg->reassembly_threshold >= 0.0)) throw ValidationError("solver: reassembly threshold must be >= 0");
+    if (n_phases < 1) throw ValidationError("materials: catalog is empty");
+    int width = 0;
+    for (int ph = 0; ph < n_phases; ++ph) {
+      if (models[ph].kind == 0) {
+        check_spd(models[ph].tangent, m, "material tangent");
+      } else {
+        if (thermal) throw ValidationError("materials: mixed thermal and mechanical models");
+        const or_material& md = models[ph];
+        if (!(md.bulk > 0.0) || !(md.shear > 0.0) || !(md.yield_stress > 0.0))
+          throw ValidationError("j2_plastic: K, G and tau_y0 must be > 0");
+        if (md.hardening < 0.0) throw ValidationError("j2_plastic: H must be >= 0");
+        width = 7;
+      }
+    }
+    for (Index p = 0; p < l.np; ++p)
+      if (phase[p] >= n_phases) throw ValidationError("materials: phase id missing from catalog");
+    for (int k = 0; k < m; ++k)
+      if (!std::isfinite(e[k])) throw ValidationError("load vector has non-finite entries");
+
+    const Index nodes = l.num_nodes(), n = c * nodes, nQ = l.num_quads();
+    std::vector<double> gstate((size_t)width * nQ, 0.0);
+    if (width && g0_in) std::copy(g0_in, g0_in + (size_t)width * nQ, gstate.begin());
+    std::vector<double> u(n, 0.0);
+    if (warm_u) std::copy(warm_u, warm_u + n, u.begin());
+
+    std::vector<double> eps(nQ * m), sig(nQ * m), tan((size_t)nQ * m * m), trial((size_t)width * nQ), b(n), z(n),
+        x(n), gz(nQ * m), tmpq(nQ * m);
+    // constitutive_sweep (solver.cpp:144-169)
+    auto sweep = [&](const double* uu) {
+      gradient(l, c, uu, eps.data());
+      for (Index q = 0; q < nQ; ++q) {
+        double et[6];
+        for (int k = 0; k < m; ++k) et[k] = e[k] + eps[q * m + k];
+        const or_material& md = models[phase[q / nq]];
+        if (md.kind == 0) {
+          for (int k = 0; k < m; ++k)
+            if (!std::isfinite(et[k])) throw NumericalError("evaluate: non-finite strain input");
+          const double* cm = md.tangent;
+          for (int i = 0; i < m; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < m; ++j) acc += cm[j * m + i] * et[j];
+            sig[q * m + i] = acc;
+          }
+          std::copy(cm, cm + m * m, tan.data() + (size_t)q * m * m);
+          // linear evaluate leaves the trial slot untouched: zero (solver.cpp:152-155)
+          if (width)
+            for (int i = 0; i < width; ++i) trial[(size_t)q * width + i] = 0.0;
+        } else {
+          j2_eval(d, md.bulk, md.shear, md.yield_stress, md.hardening, et, gstate.data() + (size_t)q * width,
+                  sig.data() + q * m, tan.data() + (size_t)q * m * m, trial.data() + (size_t)q * width);
+        }
+      }
+    };
+    auto tan_at = [&](Index q) { return tan.data() + (size_t)q * m * m; };
+    // volume_average_tangent (fields.cpp:52-61)
+    auto mean_tangent = [&](std::vector<double>& avg) {
+      avg.assign(m * m, 0.0);
+      for (Index q = 0; q < nQ; ++q) {
+        const double w = l.quads[q % nq].w;
+        const double* blk = tan_at(q);
+        for (int i = 0; i < m * m; ++i) avg[i] += w * blk[i];
+      }
+      const double vol = l.cell_volume();
+      for (int i = 0; i < m * m; ++i) avg[i] /= vol;
+    };
+    auto fro = [&](const std::vector<double>& a) {
+      double s2 = 0.0;
+      for (double v : a) s2 += v * v;
+      return std::sqrt(s2);
+    };
+    // PrecondManager state (solver.cpp:120-142)
+    std::unique_ptr<or_precond> minv;
+    std::vector<double> c_ref_used, mean_at_assembly, mean;
+
+    double bnorm0 = 0.0, inc_rel = std::numeric_limits<double>::infinity();
+    bool have_inc = false;
+    rep->n_steps = 0;
+    rep->assemblies = 0;
+    rep->seconds_cg = rep->seconds_assembly = 0.0;
+    Op A = [&](const double* v, double* out) { fused(l, c, v, true, tan_at, out); };
+    Op M = [&](const double* v, double* out) { precond_apply(l, minv.get(), v, out); };
+    bool converged_state = false;
+    for (int step = 0;; ++step) {
+      sweep(u.data());
+      divergence(l, c, sig.data(), true, b.data());
+      for (Index i = 0; i < n; ++i) b[i] = -b[i];
+      auto t0 = Clock::now();
+      bool reassembled = false;
+      mean_tangent(mean);
+      bool need = !minv;
+      if (!need) {
+        std::vector<double> diff(m * m);
+        for (int i = 0; i < m * m; ++i) diff[i] = mean[i] - mean_at_assembly[i];
+        need = fro(diff) > cfg->reassembly_threshold * fro(mean_at_assembly);
+      }
+      if (need) {
+        std::vector<double> c_ref(m * m, 0.0);
+        if (cfg->policy == 0) {
+          if (!(cfg->policy_scale > 0.0)) throw ValidationError("reference: identity scale must be > 0");
+          for (int i = 0; i < m; ++i) c_ref[i * m + i] = cfg->policy_scale;
+        } else if (cfg->policy == 1) {
+          c_ref = mean;
+        } else if (cfg->policy == 2) {
+          std::copy(cfg->policy_matrix, cfg->policy_matrix + m * m, c_ref.begin());
+        } else {
+          throw ValidationError("reference: invalid policy");
+        }
+        if (!minv || c_ref != c_ref_used) {
+          minv.reset(assemble(l, c_ref.data(), c, true));
+          invert(minv.get());
+          c_ref_used = c_ref;
+          mean_at_assembly = mean;
+          reassembled = true;
+          rep->assemblies += 1;
+        }
+      }
+      rep->seconds_assembly += since(t0);
+      precond_apply(l, minv.get(), b.data(), z.data());
+      const double bnorm = std::sqrt(std::max(0.0, dot(b.data(), z.data(), n)));
+      if (step == 0) bnorm0 = bnorm;
+      for (Index q = 0; q < nQ; ++q)
+        for (int k = 0; k < m; ++k) tmpq[q * m + k] = eps[q * m + k] + e[k];
+      const double strain_scale = std::sqrt(weighted_dot(l, m, tmpq.data(), tmpq.data()));
+      bool b_zero = bnorm == 0.0;
+      if (!b_zero) {
+        gradient(l, c, z.data(), gz.data());
+        b_zero = std::sqrt(weighted_dot(l, m, gz.data(), gz.data())) <= 1e-12 * strain_scale;
+      }
+      const bool residual_ok = bnorm <= cfg->eta_newton * bnorm0;
+      const bool increment_ok = have_inc && inc_rel <= cfg->eta_newton;
+      if (step > 0 && (increment_ok || residual_ok)) {
+        rep->cause = 0;
+        rep->converged = 1;
+        converged_state = true;
+        break;
+      }
+      if (step == cfg->max_newton) {
+        rep->cause = 2;
+        rep->converged = 0;
+        break;
+      }
+      t0 = Clock::now();
+      PcgOut po;
+      if (b_zero) {
+        std::fill(x.begin(), x.end(), 0.0);
+        po.history = {bnorm};
+        po.converged = true;
+      } else {
+        po = pcg(A, M, b.data(), n, c, nodes, cfg->eta_cg, cfg->max_cg, x.data());
+      }
+      rep->seconds_cg += since(t0);
+      for (Index i = 0; i < n; ++i) u[i] += x[i];
+      remove_means(u.data(), c, nodes);
+      if (cfg->criterion == 0) {
+        gradient(l, c, x.data(), gz.data());
+        gradient(l, c, u.data(), tmpq.data());
+        const double num = std::sqrt(weighted_dot(l, m, gz.data(), gz.data()));
+        const double den = std::sqrt(weighted_dot(l, m, tmpq.data(), tmpq.data()));
+        inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+      } else {
+        const double num = std::sqrt(dot(x.data(), x.data(), n));
+        const double den = std::sqrt(dot(u.data(), u.data(), n));
+        inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+      }
+      have_inc = true;
+      if (rep->n_steps < 32) {
+        or_newton_step& s = rep->steps[rep->n_steps];
+        s.cg_iterations = po.iterations;
+        s.residual_initial = bnorm;
+        s.residual_final = po.history.back();
+        s.increment_rel = inc_rel;
+        s.precond_reassembled = reassembled ? 1 : 0;
+      }
+      rep->n_steps += 1;
+      if (!po.converged) {
+        rep->cause = 1;
+        rep->converged = 0;
+        sweep(u.data());  // stress at the returned iterate (solver.cpp:281-290)
+        break;
+      }
+    }
+    volume_average(l, m, sig.data(), avg_out);
+    if (u_out) std::copy(u.begin(), u.end(), u_out);
+    if (g_out && width) {
+      const std::vector<double>& src = converged_state ? trial : gstate;
+      std::copy(src.begin(), src.end(), g_out);
+    }
+    rep->seconds_total = since(t_total);
+    if (!rep->converged) throw NonConvergence(rep->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
 }  // extern "C"

@@ -120,6 +120,30 @@ int or_newton_solve(const or_grid* g, int32_t thermal, int32_t n_phases,
                     const or_solve_cfg* cfg, const double* warm_u, double* u_out,
                     double* avg_stress_out, or_report* report);
 
+/* Material catalog entry (material.cpp:37-101): kind 0 linear (tangent m*m
+   col-major), kind 1 J2 plasticity (bulk, shear, yield stress, hardening). */
+typedef struct {
+  int32_t kind;
+  double tangent[36];
+  double bulk, shear, yield_stress, hardening;
+} or_material;
+
+/* J2 radial return (material.cpp:122-226, j2_return + plane-strain embedding):
+   eps m Mandel, g_in 7 (plastic strain Mandel 6 + accumulated); outputs sigma
+   (m), tangent (m*m col-major, nullable), g_new (7, nullable). */
+int or_j2_evaluate(int32_t d, double bulk, double shear, double yield_stress, double hardening,
+                   const double* eps, const double* g_in, double* sigma, double* tangent, double* g_new);
+
+/* Newton solve (solver.cpp:171-296) for a general catalog (linear and J2),
+   with PrecondManager::ensure (solver.cpp:120-142: volume-mean tangent drift,
+   reassembly when the resolved C_ref changes). g0 / g_out: internal state
+   (width 7 per quad, quad-major) or NULL (zeros / not returned). g_out is the
+   trial state on convergence, g0 otherwise (solver.cpp:228-290). */
+int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
+                           const uint8_t* phase, const double* g0, const double* e, const or_solve_cfg* cfg,
+                           const double* warm_u, double* u_out, double* g_out, double* avg_stress_out,
+                           or_report* report);
+
 /* Field reductions (fields.cpp). */
 int or_volume_average(const or_grid* g, int32_t m, const double* s, double* out);
 int or_weighted_dot(const or_grid* g, int32_t m, const double* a, const double* b,

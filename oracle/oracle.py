@@ -319,6 +319,80 @@ def newton_solve(g, thermal, cmats, phase, e, eta_newton=1e-5, eta_cg=1e-5, max_
                 assemblies=rep.assemblies, seconds_cg=rep.seconds_cg, seconds_total=rep.seconds_total)
 
 
+class _Material(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("tangent", C.c_double * 36), ("bulk", C.c_double), ("shear", C.c_double),
+                ("yield_stress", C.c_double), ("hardening", C.c_double)]
+
+
+def material(kind, tangent=None, bulk=0.0, shear=0.0, yield_stress=0.0, hardening=0.0):
+    """Catalog entry: kind "linear" (m x m tangent) or "j2" (material.cpp:37-101)."""
+    mt = _Material()
+    mt.kind = 0 if kind == "linear" else 1
+    if tangent is not None:
+        t = np.asarray(tangent, dtype=np.float64)
+        flat = t.T.ravel()  # column-major
+        for i, v in enumerate(flat):
+            mt.tangent[i] = v
+    mt.bulk, mt.shear, mt.yield_stress, mt.hardening = bulk, shear, yield_stress, hardening
+    return mt
+
+
+def j2_evaluate(d, bulk, shear, yield_stress, hardening, eps, g):
+    """MaterialModel::evaluate for J2 (material.cpp:122-226): (sigma, tangent, g_new)."""
+    m = 6 if d == 3 else 3
+    eps = _f64(eps).ravel()
+    g = _f64(g).ravel()
+    sig = np.zeros(m)
+    tan = np.zeros(m * m)
+    gn = np.zeros(7)
+    _check(lib().or_j2_evaluate(C.c_int32(d), C.c_double(bulk), C.c_double(shear), C.c_double(yield_stress),
+                                C.c_double(hardening), _ptr(eps), _ptr(g), _ptr(sig), _ptr(tan), _ptr(gn)))
+    return sig, tan.reshape(m, m).T.copy(), gn
+
+
+def newton_solve_models(g, thermal, models, phase, e, g0=None, eta_newton=1e-5, eta_cg=1e-5, max_newton=25,
+                        max_cg=20000, reassembly_threshold=0.1, criterion="strain", reference="volume-mean",
+                        reference_scale=1.0, reference_matrix=None, warm_u=None):
+    """Newton solve for a general (linear + J2) catalog with internal state."""
+    d = g.dim
+    c = 1 if thermal else d
+    m = g.m(c)
+    arr = (_Material * len(models))(*models)
+    ph = np.ascontiguousarray(phase, dtype=np.uint8).ravel()
+    e = _f64(e).ravel()
+    cfg = _Cfg()
+    cfg.eta_newton, cfg.eta_cg = eta_newton, eta_cg
+    cfg.max_newton, cfg.max_cg = max_newton, max_cg
+    cfg.reassembly_threshold = reassembly_threshold
+    cfg.criterion = 0 if criterion == "strain" else 1
+    cfg.policy = POLICIES[reference]
+    cfg.policy_scale = reference_scale
+    pm = None
+    if reference_matrix is not None:
+        pm = _cmat(reference_matrix, m)
+        cfg.policy_matrix = _ptr(pm)
+    nq = g.quads_per_pixel * g.num_pixels
+    width = 7 if any(mm.kind == 1 for mm in models) else 0
+    g0a = _f64(g0).ravel() if g0 is not None else None
+    gout = np.zeros(width * nq)
+    u = np.zeros(c * g.num_nodes)
+    avg = np.zeros(m)
+    rep = _Report()
+    wu = _f64(warm_u).ravel() if warm_u is not None else None
+    code = lib().or_newton_solve_models(g.ref, C.c_int32(int(thermal)), C.c_int32(len(models)), arr,
+                                        _ptr(ph, C.c_uint8), _ptr(g0a), _ptr(e), C.byref(cfg), _ptr(wu), _ptr(u),
+                                        _ptr(gout) if width else None, _ptr(avg), C.byref(rep))
+    if code not in (0, 3):
+        _check(code)
+    steps = [dict(cg_iterations=rep.steps[i].cg_iterations, residual_initial=rep.steps[i].residual_initial,
+                  residual_final=rep.steps[i].residual_final, increment_rel=rep.steps[i].increment_rel,
+                  precond_reassembled=bool(rep.steps[i].precond_reassembled))
+             for i in range(min(rep.n_steps, 32))]
+    return dict(u=u, average_stress=avg, internal=gout, converged=bool(rep.converged),
+                cause=["converged", "cg-stall", "newton-cap"][rep.cause], steps=steps,
+                assemblies=rep.assemblies)
+
+
 def volume_average(g, s):
     s = _f64(s)
     m = s.shape[-1]

@@ -131,3 +131,98 @@ def test_linear_newton_one_step_and_errors(oracle_mod):
     with pytest.raises(oracle_mod.OracleError) as ei:
         oracle_mod.Preconditioner(g, -np.eye(3), 2)
     assert ei.value.code == 2
+
+
+# ------------------------------------------------------------ J2
+def _von_mises_mandel6(s):
+    tr = s[:3].sum()
+    dev = s.copy()
+    dev[:3] -= tr / 3.0
+    return np.sqrt(1.5) * np.linalg.norm(dev)
+
+
+def test_j2_elastic_below_yield(oracle_mod):
+    """test_material.cpp:68-81: J2 below the yield surface equals the
+    isotropic elastic model, state untouched."""
+    eps = np.zeros(6)
+    eps[5] = 0.2
+    sig, tan, gn = oracle_mod.j2_evaluate(3, 1.0, 0.7, 1.0, 0.5, eps, np.zeros(7))
+    c = oracle_mod.isotropic_stiffness(1.0, 0.7, 3)
+    assert np.abs(sig - c @ eps).max() < 1e-14
+    assert np.abs(tan - c).max() < 1e-14
+    assert np.abs(gn).max() == 0.0
+
+
+def test_j2_consistency_condition(oracle_mod):
+    """test_material.cpp:83-101: accumulated plastic strain never decreases and
+    a plastic state sits on the yield surface."""
+    k, g_mod, tau0, hard = 1.2, 0.8, 0.01, 0.25
+    g = np.zeros(7)
+    draws = oracle_mod.uniform(17, 24)
+    for step in range(4):
+        eps = 0.05 * draws[6 * step:6 * step + 6]
+        sig, _, gn = oracle_mod.j2_evaluate(3, k, g_mod, tau0, hard, eps, g)
+        assert gn[6] >= g[6]
+        if gn[6] > g[6]:
+            assert abs(_von_mises_mandel6(sig) - (tau0 + hard * gn[6])) < 1e-10 * tau0
+        g = gn
+
+
+@pytest.mark.parametrize("d", [3, 2])
+def test_j2_tangent_matches_finite_differences(oracle_mod, d):
+    """test_material.cpp:103-139."""
+    k, g_mod, tau0, hard = 1.2, 0.8, 0.01, 0.25
+    n = 6 if d == 3 else 3
+    eps0 = np.zeros(n)
+    eps0[0] = 0.04
+    eps0[n - 1] = 0.02
+    _, _, g1 = oracle_mod.j2_evaluate(d, k, g_mod, tau0, hard, eps0, np.zeros(7))
+    assert g1[6] > 0.0
+    eps = eps0.copy()
+    eps[1] += 0.015
+    _, tan, g2 = oracle_mod.j2_evaluate(d, k, g_mod, tau0, hard, eps, g1)
+    assert g2[6] > g1[6]
+    h = 1e-6
+    fd = np.zeros((n, n))
+    for j in range(n):
+        ep, em = eps.copy(), eps.copy()
+        ep[j] += h
+        em[j] -= h
+        fd[:, j] = (oracle_mod.j2_evaluate(d, k, g_mod, tau0, hard, ep, g1)[0] -
+                    oracle_mod.j2_evaluate(d, k, g_mod, tau0, hard, em, g1)[0]) / (2 * h)
+    assert np.abs(fd - tan).max() / np.abs(tan).max() < 1e-5
+    assert np.abs(tan - tan.T).max() < 1e-12 * np.abs(tan).max()
+
+
+def test_models_newton_linear_catalog_equals_linear_newton(oracle_mod):
+    """The general-catalog Newton reduces to the linear one for linear models."""
+    og = oracle_mod.Grid((12, 10), (1.0, 1.0), "two-triangles")
+    c0 = oracle_mod.isotropic_stiffness(1.0, 0.5, 2)
+    c1 = oracle_mod.isotropic_stiffness(12.0, 7.0, 2)
+    ph = (oracle_mod.uniform(5, 120, 0.0, 1.0) < 0.4).astype(np.uint8)
+    e = np.array([0.01, -0.002, 0.003])
+    ref = oracle_mod.newton_solve(og, False, [c0, c1], ph, e, eta_cg=1e-10, eta_newton=1e-8)
+    got = oracle_mod.newton_solve_models(og, False, [oracle_mod.material("linear", c0),
+                                                     oracle_mod.material("linear", c1)], ph, e,
+                                         eta_cg=1e-10, eta_newton=1e-8)
+    assert got["converged"] and ref["converged"]
+    assert [s["cg_iterations"] for s in got["steps"]] == [s["cg_iterations"] for s in ref["steps"]]
+    np.testing.assert_allclose(got["u"], ref["u"], rtol=0, atol=1e-14 * np.abs(ref["u"]).max())
+    np.testing.assert_allclose(got["average_stress"], ref["average_stress"], rtol=1e-13)
+
+
+def test_models_newton_j2_plastic_flow(oracle_mod):
+    """acceptance.cpp:333-345 plastic instances: two J2 phases on an 8x8
+    plane-strain grid converge, plastify and keep the reference's state
+    contract (trial state returned on convergence)."""
+    og = oracle_mod.Grid((8, 8), (1.0, 1.0), "two-triangles")
+    mats = [oracle_mod.material("j2", bulk=0.833, shear=0.385, yield_stress=3e-3, hardening=0.08),
+            oracle_mod.material("j2", bulk=0.833, shear=0.385, yield_stress=6e-3, hardening=0.16)]
+    ph = (oracle_mod.uniform(7007, 64, 0.0, 1.0) < 0.5).astype(np.uint8)
+    e = np.array([5e-3, -5e-3, 1e-3])
+    out = oracle_mod.newton_solve_models(og, False, mats, ph, e, eta_newton=1e-5, eta_cg=1e-5,
+                                         reference="explicit", reference_matrix=np.eye(3))
+    assert out["converged"]
+    g = out["internal"].reshape(-1, 7)
+    assert g[:, 6].max() > 0.0 and g[:, 6].min() >= 0.0
+    assert len(out["steps"]) >= 2  # nonlinear: more than one Newton step
