@@ -134,6 +134,33 @@ int homfe_gpu_solve_device(homfe_ctx* ctx, const double* e, const homfe_solve_cf
                            const double* d_warm_u, double* d_u_out, double* avg_stress_out,
                            homfe_report* report);
 
+/* ---- nonlinear materials (J2 plasticity) --------------------- */
+#define HOMFE_MATERIAL_LINEAR 0
+#define HOMFE_MATERIAL_J2 1
+/* Catalog entry, MaterialModel factories (material.cpp:37-101):
+   LINEAR: tangent = m x m column-major Mandel (linear_elastic / conductivity);
+   J2: j2_plastic(bulk, shear, yield_stress, hardening), mechanical only. */
+typedef struct {
+  int32_t kind;
+  double tangent[36];
+  double bulk, shear, yield_stress, hardening;
+} homfe_material;
+/* MaterialMap (material.hpp:100-118) with a general catalog. Linear-only
+   catalogs behave exactly as homfe_gpu_set_material. */
+int homfe_gpu_set_material_models(homfe_ctx* ctx, int32_t n_phases, const homfe_material* models,
+                                  const uint8_t* phase);
+/* InternalState shape (material.hpp:83-97): width 7 (J2) or 0, num_quads. */
+int homfe_gpu_internal_width(homfe_ctx* ctx, int32_t* width, int64_t* num_quads);
+/* newton_solve (solver.hpp:163-166) with the committed internal state g0
+   (width x num_quads, quad-major; NULL = zeros) and the outgoing state g_out
+   (trial state on convergence, g0 otherwise; NULL = not returned). */
+int homfe_gpu_solve_state(homfe_ctx* ctx, const double* e, const homfe_solve_cfg* cfg,
+                          const double* warm_u, const double* g0, double* u_out, double* g_out,
+                          double* avg_stress_out, homfe_report* report);
+/* NewtonOutcome::stress of the last solve (num_quads x m, quad-interleaved
+   QuadField layout, fields.hpp:40-62). Mechanical contexts. */
+int homfe_gpu_stress_field(homfe_ctx* ctx, double* out);
+
 /* ---- parity hooks (host buffers) ---------------------------------------- */
 /* apply_tangent_operator (operators.hpp:31-33) with the material set above. */
 int homfe_gpu_apply_K(homfe_ctx* ctx, const double* u, double* ku);

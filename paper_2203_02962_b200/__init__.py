@@ -113,12 +113,14 @@ def isotropic_stiffness(bulk, shear, dim):
 
 
 class Material:
-    """Linear constitutive models of proj/include/homfe/material.hpp:36-69."""
+    """Constitutive models of proj/include/homfe/material.hpp:36-69: linear
+    (elastic / conductivity) and J2 plasticity (material.cpp:78-101,122-226)."""
 
-    def __init__(self, tangent, thermal, dim):
+    def __init__(self, tangent, thermal, dim, j2=None):
         self.tangent = np.array(tangent, dtype=float)
         self.thermal = thermal
         self.dim = dim
+        self.j2 = j2  # (bulk, shear, yield_stress, hardening) or None
 
     @staticmethod
     def linear_elastic(stiffness):
@@ -148,7 +150,18 @@ class Material:
 
     @staticmethod
     def j2_plastic(bulk, shear, yield_stress, hardening, dim):
-        raise ValidationError("j2_plastic: nonlinear materials are not on the GPU hot path (SURVEY.md 8(f) f1)")
+        if not (bulk > 0.0 and shear > 0.0 and yield_stress > 0.0):
+            raise ValidationError("j2_plastic: K, G and tau_y0 must be > 0")
+        if hardening < 0.0:
+            raise ValidationError("j2_plastic: H must be >= 0")
+        if dim not in (2, 3):
+            raise ValidationError("j2_plastic: dimension must be 2 or 3")
+        return Material(isotropic_stiffness(bulk, shear, dim), False, dim,
+                        j2=(float(bulk), float(shear), float(yield_stress), float(hardening)))
+
+    @property
+    def nonlinear(self):
+        return self.j2 is not None
 
     @property
     def flux_components(self):
@@ -156,7 +169,19 @@ class Material:
 
     @property
     def internal_width(self):
-        return 0
+        return 7 if self.j2 is not None else 0
+
+    def model(self):
+        """homfe_material catalog entry for the C ABI."""
+        mm = _native.MaterialModel()
+        if self.j2 is None:
+            mm.kind = 0
+            for i, v in enumerate(self.tangent.T.ravel()):
+                mm.tangent[i] = v
+        else:
+            mm.kind = 1
+            mm.bulk, mm.shear, mm.yield_stress, mm.hardening = self.j2
+        return mm
 
     def evaluate(self, strain, internal=None):
         eps = np.asarray(strain, dtype=float)
@@ -164,6 +189,8 @@ class Material:
             raise ValidationError("evaluate: strain has wrong length")
         if not np.all(np.isfinite(eps)):
             raise NumericalSolverError("evaluate: non-finite strain input")
+        if self.j2 is not None:
+            raise ValidationError("evaluate: J2 is evaluated on the device inside the Newton solve")
         return self.tangent @ eps, self.tangent.copy(), np.zeros(0)
 
 
@@ -214,6 +241,14 @@ class _Context:
         _check(lib.homfe_gpu_set_material(self.h, cm.shape[0], _dp(cm),
                                           ph.ctypes.data_as(C.POINTER(C.c_uint8))))
         self._material_key = key
+
+    def set_models(self, materials, phases):
+        """General catalog (linear + J2): homfe_gpu_set_material_models."""
+        ph = np.ascontiguousarray(phases, dtype=np.uint8).ravel()
+        arr = (_native.MaterialModel * len(materials))(*[m.model() for m in materials])
+        self._material_key = None
+        _check(lib.homfe_gpu_set_material_models(self.h, len(materials), arr,
+                                                 ph.ctypes.data_as(C.POINTER(C.c_uint8))))
 
     def set_reference(self, c_ref):
         cr = _f64(np.asarray(c_ref).T)
@@ -451,7 +486,12 @@ class Solver:
         self.grid = grid
         self.c = 1 if thermal.pop() else grid.dim
         self.ctx = grid.context(self.c)
-        self.ctx.set_material(np.stack([m.tangent for m in materials]), ph)
+        self.nonlinear = any(m.nonlinear for m in materials)
+        if self.nonlinear:
+            self.ctx.set_models(materials, ph)
+        else:
+            self.ctx.set_material(np.stack([m.tangent for m in materials]), ph)
+        self.width = 7 if self.nonlinear else 0
         self.cfg = _native.SolveCfg()
         self.cfg.eta_newton, self.cfg.eta_cg = eta_newton, eta_cg
         self.cfg.max_newton, self.cfg.max_cg = max_newton, max_cg
@@ -466,7 +506,10 @@ class Solver:
             self._refmat = _f64(np.asarray(reference_matrix).T)
             self.cfg.reference_matrix = _dp(self._refmat)
 
-    def solve(self, e, warm_start=None, raise_on_nonconvergence=False):
+    def solve(self, e, warm_start=None, raise_on_nonconvergence=False, internal=None, stress=False):
+        """newton_solve (solver.cpp:171-296). ``internal``: committed state
+        (num_quads x 7) for J2 catalogs; the result holds the outgoing state
+        (trial state on convergence, the input otherwise)."""
         m = self.ctx.m
         e = _f64(e).ravel()
         if e.size != m:
@@ -475,10 +518,29 @@ class Solver:
         avg = np.zeros(m)
         rep = _native.Report()
         warm = _nodal(self.grid, warm_start) if warm_start is not None else None
-        code = lib.homfe_gpu_solve(self.ctx.h, _dp(e), C.byref(self.cfg), _dp(warm), _dp(u), _dp(avg), C.byref(rep))
+        out = {}
+        if self.nonlinear:
+            nq = self.grid.num_quads
+            g0 = None
+            if internal is not None:
+                g0 = _f64(internal).reshape(-1)
+                if g0.size != nq * 7:
+                    raise ValidationError("internal state does not match layout and catalog")
+            g_out = np.zeros((nq, 7))
+            code = lib.homfe_gpu_solve_state(self.ctx.h, _dp(e), C.byref(self.cfg), _dp(warm), _dp(g0), _dp(u),
+                                             _dp(g_out), _dp(avg), C.byref(rep))
+            out["internal"] = g_out
+        else:
+            code = lib.homfe_gpu_solve(self.ctx.h, _dp(e), C.byref(self.cfg), _dp(warm), _dp(u), _dp(avg),
+                                       C.byref(rep))
         if code != _native.NONCONVERGED or raise_on_nonconvergence:
             _check(code)
-        return dict(converged=bool(rep.converged), u=u, average_stress=avg, report=_report_dict(rep))
+        out.update(converged=bool(rep.converged), u=u, average_stress=avg, report=_report_dict(rep))
+        if stress:
+            sig = np.zeros((self.grid.num_quads, m))
+            _check(lib.homfe_gpu_stress_field(self.ctx.h, _dp(sig)))
+            out["stress"] = sig
+        return out
 
 
 def newton_solve(grid, materials, phases, e, eta_newton=1e-5, eta_cg=1e-5, max_newton=25, max_cg=20000,
@@ -488,4 +550,28 @@ def newton_solve(grid, materials, phases, e, eta_newton=1e-5, eta_cg=1e-5, max_n
     Python signature of proj/src/bindings/module.cpp:299-328)."""
     s = Solver(grid, materials, phases, eta_newton, eta_cg, max_newton, max_cg, reassembly_threshold, reference,
                reference_scale, reference_matrix, criterion)
-    return s.solve(e)
+    return s.solve(e, stress=not s.ctx.c == 1)
+
+
+def run_load_program(grid, materials, phases, loads, eta_newton=1e-5, eta_cg=1e-5, max_newton=25, max_cg=20000,
+                     reassembly_threshold=0.1, reference="volume-mean", reference_scale=1.0, reference_matrix=None,
+                     criterion="strain"):
+    """run_load_program (proj/src/solver.cpp:298-319): load steps with warm
+    starts; the internal state is committed after each converged step and the
+    program stops at the first non-converged step."""
+    if not len(loads):
+        raise ValidationError("loading: at least one load step is required")
+    s = Solver(grid, materials, phases, eta_newton, eta_cg, max_newton, max_cg, reassembly_threshold, reference,
+               reference_scale, reference_matrix, criterion)
+    results = []
+    g = np.zeros((grid.num_quads, 7)) if s.nonlinear else None
+    warm = None
+    for e in loads:
+        out = s.solve(e, warm_start=warm, internal=g)
+        if out["converged"] and s.nonlinear:
+            g = out["internal"]
+        results.append(dict(load=np.asarray(e, dtype=float), **out))
+        if not out["converged"]:
+            break
+        warm = out["u"]
+    return results

@@ -41,6 +41,12 @@ class Report(C.Structure):
                 ("cg_device_ms", C.c_double), ("kernel_launches", C.c_int64)]
 
 
+class MaterialModel(C.Structure):
+    """homfe_material (include/homfe_gpu.h)."""
+    _fields_ = [("kind", C.c_int32), ("tangent", C.c_double * 36), ("bulk", C.c_double), ("shear", C.c_double),
+                ("yield_stress", C.c_double), ("hardening", C.c_double)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -73,6 +79,10 @@ def _load():
         "homfe_nccl_unique_id": (C.c_int, [vp]),
         "homfe_gpu_create_dist": (C.c_int, [P(GridDesc), i32, i32, vp, P(vp)]),
         "homfe_random_normal": (C.c_int, [C.c_uint64, i64, P(d)]),
+        "homfe_gpu_set_material_models": (C.c_int, [vp, i32, P(MaterialModel), P(C.c_uint8)]),
+        "homfe_gpu_internal_width": (C.c_int, [vp, P(i32), P(i64)]),
+        "homfe_gpu_solve_state": (C.c_int, [vp, P(d), P(SolveCfg), P(d), P(d), P(d), P(d), P(d), P(Report)]),
+        "homfe_gpu_stress_field": (C.c_int, [vp, P(d)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -89,4 +99,5 @@ EXPORTED = ("homfe_gpu_last_error", "homfe_isotropic_stiffness", "homfe_gpu_crea
             "homfe_gpu_reference_blocks", "homfe_gpu_gradient", "homfe_gpu_divergence",
             "homfe_gpu_volume_average", "homfe_gpu_pcg", "homfe_gpu_index_maps", "homfe_gpu_sizes",
             "homfe_random_uniform", "homfe_random_normal", "homfe_gpu_kernel_times",
-            "homfe_nccl_unique_id", "homfe_gpu_create_dist")
+            "homfe_nccl_unique_id", "homfe_gpu_create_dist", "homfe_gpu_set_material_models",
+            "homfe_gpu_internal_width", "homfe_gpu_solve_state", "homfe_gpu_stress_field")

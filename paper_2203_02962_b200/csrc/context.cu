@@ -101,6 +101,16 @@ struct homfe_ctx {
   double* d_hexmat = nullptr;       // modal-basis material table (hexfast.cu)
   bool no_fast2d = false;           // HOMFE_FAST2D=0: generic 2-D element kernel
   double* d_tri = nullptr;          // TwoTriangles flux tables (quad2d.cu)
+  // nonlinear (J2) path, j2.cu
+  bool nonlinear = false;           // the catalog holds a J2 phase
+  bool nl_op = false;               // apply_K is the tangent operator (inside newton_nl)
+  bool graphs_nl = false;           // captured graphs hold the tangent operator
+  std::vector<NLModel> models;
+  NLModel* d_models = nullptr;
+  double *d_g0 = nullptr, *d_gtr = nullptr, *d_tanc = nullptr, *d_sig = nullptr, *d_qs = nullptr,
+         *d_tpart = nullptr;
+  int* d_status = nullptr;
+  bool sig_valid = false;           // d_sig holds the last solve's stress
   bool hex_fast = false, hex_iso = false;
   // vectors
   double *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_ap = nullptr, *d_z = nullptr, *d_u = nullptr;
@@ -245,8 +255,38 @@ void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st,
   c->launches += 3;
 }
 
+NLArgs nl_args(homfe_ctx* c, const double* u) {
+  NLArgs a{};
+  a.u = u;
+  a.e = c->d_e;
+  a.phase = c->d_phase;
+  a.models = c->d_models;
+  a.cmat = c->d_cmat;
+  a.g0 = c->d_g0;
+  a.g_trial = c->d_gtr;
+  a.tanc = c->d_tanc;
+  a.sig = c->d_sig;
+  a.partials = c->d_tpart;
+  a.status = c->d_status;
+  a.width = c->nonlinear ? 7 : 0;
+  return a;
+}
+
 void apply_K(homfe_ctx* c, const double* u, double* out, const double* fe, double scale, double* partials,
              const PcgState* st, cudaStream_t s) {
+  if (c->nl_op) {
+    // tangent operator of the current Newton state: sigma_q = C_q (D u)_q,
+    // then the weighted divergence (operators.cpp:197-257 in two passes)
+    NLArgs a = nl_args(c, u);
+    a.sig = c->d_qs;
+    launch_tan_stress(c->g, c->sp, a, st, s);
+    launch_divergence(c->g, c->sp, c->d_qs, true, out, s);
+    const int64_t n = c->nvec();
+    if (scale != 1.0) launch_scale(out, scale, n, s);
+    if (partials) launch_dot_partials(u, out, n, partials, s);
+    c->launches += 3;
+    return;
+  }
   if (c->dist) exchange_halo(c, u, s);
   ElemArgs a{u, c->d_hlo, c->d_hhi, c->d_ph_lo, out, c->d_phase, c->d_ke, c->n_phases, fe, scale, partials, st};
   if (c->hex_fast) launch_hex_fast(c->g, a, c->d_hexmat, c->hex_iso, s);
@@ -562,6 +602,7 @@ void remove_means(homfe_ctx* c, double* v) {
 
 void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint8_t* phase, bool device_phase) {
   const int m = c->g.m;
+  c->sig_valid = false;
   if (n_phases < 1) throw ValidationError("materials: catalog is empty");
   if (n_phases > kMaxPhases) throw ValidationError("materials: at most 256 phases");
   for (int ph = 0; ph < n_phases; ++ph) check_spd(tangents + ph * m * m, m, "material");
@@ -675,6 +716,11 @@ void newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* a
     if (!std::isfinite(e[k])) throw ValidationError("load vector has non-finite entries");
   std::memset(rep, 0, sizeof(*rep));
   c->launches = 0;
+  c->sig_valid = false;
+  if (c->graphs_nl) {
+    destroy_graphs(c);  // captured graphs hold the tangent operator
+    c->graphs_nl = false;
+  }
   HB_CUDA(cudaMemcpyAsync(c->d_e, e, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
   // element load vectors f_e = sum_q w B^T C e per phase
   std::vector<double> fe((size_t)c->n_phases * ne);
@@ -779,6 +825,189 @@ void newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* a
   for (int k = 0; k < m; ++k) avg_out[k] = avg[k] * sscale / c->g.cell_volume;
   rep->seconds_total = since(t_total);
   rep->kernel_launches = c->launches;
+}
+
+
+void ensure_nl_buffers(homfe_ctx* c) {
+  if (c->d_sig) return;
+  const size_t nq = (size_t)c->g.np * c->sp.nq;
+  const int m = c->g.m;
+  c->d_models = reinterpret_cast<NLModel*>(dalloc<double>(kMaxPhases * sizeof(NLModel) / sizeof(double) + 1));
+  c->d_g0 = dalloc<double>(nq * 7);
+  c->d_gtr = dalloc<double>(nq * 7);
+  c->d_tanc = dalloc<double>(nq * 8);
+  c->d_sig = dalloc<double>(nq * m);
+  c->d_qs = dalloc<double>(nq * m);
+  c->d_tpart = dalloc<double>((size_t)kRedBlocks * 36);
+  c->d_status = reinterpret_cast<int*>(dalloc<double>(1));
+}
+
+// constitutive_sweep (solver.cpp:144-169) at d_u: stress, trial state,
+// compact tangents; returns the volume-mean tangent (fields.cpp:52-61).
+std::vector<double> nl_sweep(homfe_ctx* c) {
+  const int m = c->g.m;
+  HB_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(int), c->stream));
+  launch_sweep(c->g, c->sp, nl_args(c, c->d_u), c->stream);
+  c->launches += 1;
+  std::vector<double> part((size_t)kRedBlocks * m * m);
+  int bad = 0;
+  HB_CUDA(cudaMemcpyAsync(part.data(), c->d_tpart, part.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaMemcpyAsync(&bad, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  if (bad) throw NumericalError("evaluate: non-finite strain input");
+  std::vector<double> mean(m * m, 0.0);
+  for (int b = 0; b < kRedBlocks; ++b)
+    for (int i = 0; i < m * m; ++i) mean[i] += part[(size_t)b * m * m + i];
+  for (int i = 0; i < m * m; ++i) mean[i] /= c->g.cell_volume;
+  c->sig_valid = true;
+  return mean;
+}
+
+double frob(const std::vector<double>& a) {
+  double s2 = 0.0;
+  for (double v : a) s2 += v * v;
+  return std::sqrt(s2);
+}
+
+// newton_solve (solver.cpp:171-296) for a catalog with J2 phases: a
+// constitutive sweep per Newton step, PrecondManager::ensure with the
+// volume-mean tangent drift (solver.cpp:120-142), PCG on the tangent
+// operator. d_g0 holds the committed state; on return d_gtr (converged) or
+// d_g0 (otherwise) is the outgoing state.
+bool newton_nl(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* avg_out, homfe_report* rep) {
+  const auto t_total = Clock::now();
+  validate_cfg(cfg);
+  require_material(c);
+  const int m = c->g.m;
+  for (int k = 0; k < m; ++k)
+    if (!std::isfinite(e[k])) throw ValidationError("load vector has non-finite entries");
+  std::memset(rep, 0, sizeof(*rep));
+  c->launches = 0;
+  HB_CUDA(cudaMemcpyAsync(c->d_e, e, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (!c->graphs_nl) {
+    destroy_graphs(c);  // captured operator changes
+    c->graphs_nl = true;
+  }
+  std::vector<double> mean_at_assembly;
+  double bnorm0 = 0.0, inc_rel = INFINITY;
+  bool have_inc = false, converged_state = false;
+  const int64_t n = c->nvec();
+  for (int step = 0;; ++step) {
+    auto t0 = Clock::now();
+    const std::vector<double> mean = nl_sweep(c);
+    // b = -D^T W sigma
+    launch_divergence(c->g, c->sp, c->d_sig, true, c->d_r, c->stream);
+    launch_scale(c->d_r, -1.0, n, c->stream);
+    rep->seconds_constitutive += since(t0);
+    // PrecondManager::ensure
+    t0 = Clock::now();
+    bool reassembled = false;
+    bool need = !c->have_ref || mean_at_assembly.empty();
+    if (!need) {
+      std::vector<double> diff(m * m);
+      for (int i = 0; i < m * m; ++i) diff[i] = mean[i] - mean_at_assembly[i];
+      need = frob(diff) > cfg->reassembly_threshold * frob(mean_at_assembly);
+    }
+    if (need) {
+      std::vector<double> cref(m * m, 0.0);
+      if (cfg->reference_policy == HOMFE_REF_IDENTITY_SCALED) {
+        if (!(cfg->reference_scale > 0.0)) throw ValidationError("reference: identity scale must be > 0");
+        for (int i = 0; i < m; ++i) cref[i * m + i] = cfg->reference_scale;
+      } else if (cfg->reference_policy == HOMFE_REF_VOLUME_MEAN) {
+        cref = mean;
+      } else if (cfg->reference_policy == HOMFE_REF_EXPLICIT) {
+        if (!cfg->reference_matrix) throw ValidationError("reference: explicit matrix has wrong size");
+        std::copy(cfg->reference_matrix, cfg->reference_matrix + m * m, cref.begin());
+      } else {
+        throw ValidationError("reference: invalid policy");
+      }
+      if (!c->have_ref || mean_at_assembly.empty() || cref != c->c_ref) {
+        set_reference(c, cref.data());
+        mean_at_assembly = mean;
+        reassembled = true;
+        rep->assemblies += 1;
+      }
+    }
+    rep->seconds_assembly += since(t0);
+    // z = M^-1 b and b.z
+    c->nl_op = false;
+    precond_apply(c, c->d_r, c->d_z, nullptr, c->d_partials, c->stream);
+    double bz = 0.0;
+    reduce_to_host(c, 1, &bz);
+    const double bnorm = std::sqrt(std::max(0.0, bz));
+    if (step == 0) bnorm0 = bnorm;
+    const double strain_scale = quad_norm(c, c->d_u, c->d_e);
+    const bool b_is_zero = bnorm == 0.0 || quad_norm(c, c->d_z, nullptr) <= 1e-12 * strain_scale;
+    const bool residual_ok = bnorm <= cfg->eta_newton * bnorm0;
+    const bool increment_ok = have_inc && inc_rel <= cfg->eta_newton;
+    if (step > 0 && (increment_ok || residual_ok)) {
+      rep->cause = 0;
+      rep->converged = 1;
+      converged_state = true;
+      break;
+    }
+    if (step == cfg->max_newton) {
+      rep->cause = 2;
+      rep->converged = 0;
+      break;
+    }
+    t0 = Clock::now();
+    PcgResult pr;
+    if (b_is_zero) {
+      HB_CUDA(cudaMemsetAsync(c->d_x, 0, n * sizeof(double), c->stream));
+      pr.converged = true;
+      pr.last_history = bnorm;
+    } else {
+      c->nl_op = true;
+      try {
+        pr = run_pcg(c, cfg->eta_cg, cfg->max_cg, nullptr);
+      } catch (...) {
+        c->nl_op = false;
+        throw;
+      }
+      c->nl_op = false;
+    }
+    rep->seconds_cg += since(t0);
+    rep->cg_device_ms += pr.device_ms;
+    launch_axpy(c->d_u, 1.0, c->d_x, n, c->stream);
+    c->launches += 1;
+    remove_means(c, c->d_u);
+    if (cfg->criterion == 0) {
+      const double num = quad_norm(c, c->d_x, nullptr);
+      const double den = quad_norm(c, c->d_u, nullptr);
+      inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+    } else {
+      const double num = std::sqrt(vec_dot(c, c->d_x, c->d_x));
+      const double den = std::sqrt(vec_dot(c, c->d_u, c->d_u));
+      inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+    }
+    have_inc = true;
+    if (rep->n_steps < 32) {
+      homfe_newton_step& sr = rep->steps[rep->n_steps];
+      sr.cg_iterations = pr.iterations;
+      sr.residual_initial = bnorm;
+      sr.residual_final = pr.last_history;
+      sr.increment_rel = inc_rel;
+      sr.precond_reassembled = reassembled ? 1 : 0;
+    }
+    rep->n_steps += 1;
+    rep->total_cg += pr.iterations;
+    if (!pr.converged) {
+      rep->cause = 1;
+      rep->converged = 0;
+      nl_sweep(c);  // stress at the returned iterate (solver.cpp:281-290)
+      break;
+    }
+  }
+  // <sigma> = volume average of the state's stress (solver.cpp:321-324)
+  launch_quad_wsum(c->g, c->sp, c->d_sig, c->d_partials, c->stream);
+  c->launches += 2;
+  double avg[6];
+  reduce_to_host(c, m, avg);
+  for (int k = 0; k < m; ++k) avg_out[k] = avg[k] / c->g.cell_volume;
+  rep->seconds_total = since(t_total);
+  rep->kernel_launches = c->launches;
+  return converged_state;
 }
 
 }  // namespace
@@ -1097,10 +1326,108 @@ int homfe_gpu_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, c
     else HB_CUDA(cudaMemsetAsync(c->d_u, 0, n * sizeof(double), c->stream));
     homfe_report local;
     homfe_report* r = rep ? rep : &local;
-    newton(c, e, cfg, avg_out, r);
+    if (c->nonlinear) {
+      HB_CUDA(cudaMemsetAsync(c->d_g0, 0, (size_t)c->g.np * c->sp.nq * 7 * sizeof(double), c->stream));
+      newton_nl(c, e, cfg, avg_out, r);
+    } else {
+      newton(c, e, cfg, avg_out, r);
+    }
     if (u_out) HB_CUDA(cudaMemcpyAsync(u_out, c->d_u, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     if (!r->converged) throw NonConverged(r->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
+int homfe_gpu_set_material_models(homfe_ctx* c, int32_t n_phases, const homfe_material* models,
+                                  const uint8_t* phase) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    if (!models) throw ValidationError("materials: null catalog");
+    if (n_phases < 1) throw ValidationError("materials: catalog is empty");
+    if (n_phases > kMaxPhases) throw ValidationError("materials: at most 256 phases");
+    const int m = c->g.m, d = c->g.d;
+    bool nonlinear = false;
+    std::vector<double> eff((size_t)n_phases * m * m);
+    std::vector<NLModel> nm(n_phases);
+    for (int ph = 0; ph < n_phases; ++ph) {
+      const homfe_material& md = models[ph];
+      if (md.kind == HOMFE_MATERIAL_LINEAR) {
+        std::copy(md.tangent, md.tangent + m * m, eff.begin() + (size_t)ph * m * m);
+        nm[ph] = NLModel{0, 0.0, 0.0, 0.0, 0.0};
+      } else if (md.kind == HOMFE_MATERIAL_J2) {
+        if (!(md.bulk > 0.0) || !(md.shear > 0.0) || !(md.yield_stress > 0.0))
+          throw ValidationError("j2_plastic: K, G and tau_y0 must be > 0");
+        if (md.hardening < 0.0) throw ValidationError("j2_plastic: H must be >= 0");
+        if (c->g.c == 1) throw ValidationError("materials: mixed thermal and mechanical models");
+        if (c->dist) throw ValidationError("j2_plastic: the nonlinear path runs on one GPU");
+        isotropic_stiffness(md.bulk, md.shear, d, &eff[(size_t)ph * m * m]);  // elastic tables
+        nm[ph] = NLModel{1, md.bulk, md.shear, md.yield_stress, md.hardening};
+        nonlinear = true;
+      } else {
+        throw ValidationError("materials: unknown model kind");
+      }
+    }
+    c->nonlinear = false;
+    set_material(c, n_phases, eff.data(), phase, false);
+    ensure_nl_buffers(c);
+    c->models = nm;
+    HB_CUDA(cudaMemcpy(c->d_models, nm.data(), nm.size() * sizeof(NLModel), cudaMemcpyHostToDevice));
+    c->nonlinear = nonlinear;
+  });
+}
+
+int homfe_gpu_internal_width(homfe_ctx* c, int32_t* width, int64_t* num_quads) {
+  return guarded([&] {
+    if (width) *width = c->nonlinear ? 7 : 0;
+    if (num_quads) *num_quads = c->g.np * c->sp.nq;
+  });
+}
+
+int homfe_gpu_solve_state(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* warm_u,
+                          const double* g0, double* u_out, double* g_out, double* avg_out, homfe_report* rep) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    const int64_t n = c->nvec();
+    const size_t gq = (size_t)c->g.np * c->sp.nq * 7;
+    if (warm_u) HB_CUDA(cudaMemcpyAsync(c->d_u, warm_u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    else HB_CUDA(cudaMemsetAsync(c->d_u, 0, n * sizeof(double), c->stream));
+    homfe_report local;
+    homfe_report* r = rep ? rep : &local;
+    if (c->nonlinear) {
+      if (g0) HB_CUDA(cudaMemcpyAsync(c->d_g0, g0, gq * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      else HB_CUDA(cudaMemsetAsync(c->d_g0, 0, gq * sizeof(double), c->stream));
+      const bool ok = newton_nl(c, e, cfg, avg_out, r);
+      if (g_out)
+        HB_CUDA(cudaMemcpyAsync(g_out, ok ? c->d_gtr : c->d_g0, gq * sizeof(double), cudaMemcpyDeviceToHost,
+                                c->stream));
+    } else {
+      newton(c, e, cfg, avg_out, r);
+    }
+    if (u_out) HB_CUDA(cudaMemcpyAsync(u_out, c->d_u, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (!r->converged) throw NonConverged(r->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
+int homfe_gpu_stress_field(homfe_ctx* c, double* out) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    require_material(c);
+    if (c->dist) throw ValidationError("stress_field: single-GPU contexts only");
+    if (c->g.c == 1 && !c->sig_valid) throw ValidationError("stress_field: mechanical contexts only");
+    if (!c->sig_valid) {
+      // linear solve: sigma = C (e + D u) at the last solution (solver.cpp:321-324)
+      ensure_nl_buffers(c);
+      if ((int)c->models.size() != c->n_phases) {
+        c->models.assign(c->n_phases, NLModel{0, 0.0, 0.0, 0.0, 0.0});
+        HB_CUDA(cudaMemcpy(c->d_models, c->models.data(), c->models.size() * sizeof(NLModel),
+                           cudaMemcpyHostToDevice));
+      }
+      nl_sweep(c);
+    }
+    const size_t nq = (size_t)c->g.np * c->sp.nq * c->g.m;
+    HB_CUDA(cudaMemcpyAsync(out, c->d_sig, nq * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
   });
 }
 

@@ -39,6 +39,28 @@ void launch_hex_fast(const Grid& g, const ElemArgs& a, const double* d_mat, bool
 bool elem2d_eligible(const Grid& g);
 void elem2d_tri_tables(const Grid& g, int n_phases, const double* cmats, std::vector<double>& tab);
 void launch_elem2d(const Grid& g, const ElemArgs& a, const double* d_tri, cudaStream_t s);
+// Nonlinear (J2) path, j2.cu. Per phase: kind 0 linear (catalog matrix in
+// cmat), 1 J2 (bulk k, shear g, yield stress tau0, hardening).
+struct NLModel {
+  int kind;
+  double k, g, tau0, hard;
+};
+struct NLArgs {
+  const double* u;        // nodal field (c x N)
+  const double* e;        // macro strain (m), sweep only
+  const uint8_t* phase;
+  const NLModel* models;
+  const double* cmat;     // n_phases x m x m column-major
+  const double* g0;       // committed internal state (7 per quad)
+  double* g_trial;        // trial internal state (7 per quad)
+  double* tanc;           // compact tangent (a, b, n[6]) per quad
+  double* sig;            // stress quad field (m per quad)
+  double* partials;       // sweep: per block m x m of sum_q w C_q
+  int* status;            // sweep: set to 1 on a non-finite strain
+  int width;              // internal width (7 when any J2 phase)
+};
+void launch_sweep(const Grid& g, const StencilParams& sp, const NLArgs& a, cudaStream_t s);
+void launch_tan_stress(const Grid& g, const StencilParams& sp, const NLArgs& a, const PcgState* st, cudaStream_t s);
 void launch_phase_counts(const uint8_t* ph, int64_t n, unsigned long long* counts, cudaStream_t s);
 // mode 0: sum_q w |D u + e|^2 / h^3 (1 partial per block); 1: sum_q w C (D u + e) / h^3 (m per block)
 bool launch_hex_quad(const Grid& g, int mode, const double* u, const double* halo_hi, const double* e,

@@ -60,8 +60,11 @@ def test_grid_validation_mirrors_reference():
         hb.Grid([4, 4], [1.0, 0.0], "two-triangles")
     with pytest.raises(hb.ValidationError):
         hb.Material.linear_elastic(-np.eye(3))
+    assert hb.Material.j2_plastic(1.0, 0.5, 1.0, 0.1, 3).internal_width == 7
     with pytest.raises(hb.ValidationError):
-        hb.Material.j2_plastic(1.0, 0.5, 1.0, 0.1, 3)
+        hb.Material.j2_plastic(1.0, 0.5, 1.0, -0.1, 3)  # material.cpp:86-88
+    with pytest.raises(hb.ValidationError):
+        hb.Material.j2_plastic(1.0, 0.0, 1.0, 0.1, 3)
 
 
 def test_mandel_roundtrip():
