@@ -10,9 +10,9 @@
 //   * non-convergence is reported, not thrown (NewtonOutcome::converged,
 //     SolveReport::cause), as in proj/src/solver.cpp:229-290.
 // Forced deviations (documented in DESIGN.md): Eigen vectors become
-// std::vector<double>; materials are linear (pixel-constant tangents; J2 is
-// not on the GPU path); InternalState is omitted (width 0 for linear models,
-// proj/src/material.cpp:107-111).
+// std::vector<double>. Both newton_solve forms exist: the reference's
+// (layout, map, g0, e, cfg, precond, warm) and the linear shorthand without
+// InternalState (width 0 for linear models, proj/src/material.cpp:107-111).
 #ifndef HOMFE_GPU_HPP
 #define HOMFE_GPU_HPP
 
@@ -93,6 +93,16 @@ class GridLayout {
   int dim() const { return cell_.dim(); }
   Index num_pixels() const { return cell_.pixel_count(); }
   Index num_nodes() const { return num_pixels(); }
+  // grid.cpp:114-229: 1 (BilinearQuad here: 4), 2, 4, 8 Gauss points per pixel
+  int quads_per_pixel() const {
+    switch (kind_) {
+      case StencilKind::BilinearQuad: return 4;
+      case StencilKind::TwoTriangles: return 2;
+      case StencilKind::FourTrianglesTwoNode: return 4;
+      case StencilKind::TrilinearHex: return 8;
+    }
+    return 0;
+  }
 
   homfe_ctx* context(int components, int device = 0) const {
     auto it = ctx_.find(components);
@@ -130,9 +140,41 @@ struct NodalField {
   double operator()(int c, Index node) const { return data[static_cast<std::size_t>(c * nodes + node)]; }
 };
 
-// material.hpp:36-69, linear models only
+// material.hpp:36-69 (linear models and J2 plasticity)
 class MaterialModel {
  public:
+  enum class Kind { LinearElastic, Conductivity, J2Plastic };
+  // material.cpp:78-101
+  static MaterialModel j2_plastic(double bulk, double shear, double yield_stress, double hardening, int d) {
+    if (!(bulk > 0.0) || !(shear > 0.0) || !(yield_stress > 0.0))
+      throw ValidationError("j2_plastic: K, G and tau_y0 must be > 0");
+    if (hardening < 0.0) throw ValidationError("j2_plastic: H must be >= 0");
+    if (d != 2 && d != 3) throw ValidationError("j2_plastic: dimension must be 2 or 3");
+    MaterialModel m = isotropic_elastic(bulk, shear, d);
+    m.kind_ = Kind::J2Plastic;
+    m.j2_[0] = bulk;
+    m.j2_[1] = shear;
+    m.j2_[2] = yield_stress;
+    m.j2_[3] = hardening;
+    return m;
+  }
+  Kind kind() const { return kind_; }
+  bool nonlinear() const { return kind_ == Kind::J2Plastic; }
+  int internal_width() const { return nonlinear() ? 7 : 0; }
+  homfe_material c_model() const {
+    homfe_material mm{};
+    if (nonlinear()) {
+      mm.kind = HOMFE_MATERIAL_J2;
+      mm.bulk = j2_[0];
+      mm.shear = j2_[1];
+      mm.yield_stress = j2_[2];
+      mm.hardening = j2_[3];
+    } else {
+      mm.kind = HOMFE_MATERIAL_LINEAR;
+      for (std::size_t i = 0; i < tangent_.size() && i < 36; ++i) mm.tangent[i] = tangent_[i];
+    }
+    return mm;
+  }
   static MaterialModel linear_elastic(std::vector<double> c_colmajor, int d) {
     const int m = d == 2 ? 3 : 6;
     if (static_cast<int>(c_colmajor.size()) != m * m) throw ValidationError("linear_elastic: stiffness must be 3x3 or 6x6");
@@ -156,13 +198,29 @@ class MaterialModel {
   bool thermal() const { return thermal_; }
   int dim() const { return dim_; }
   int flux_components() const { return thermal_ ? dim_ : (dim_ == 2 ? 3 : 6); }
-  const std::vector<double>& linear_tangent() const { return tangent_; }
+  const std::vector<double>& linear_tangent() const {
+    if (nonlinear()) throw ValidationError("linear_tangent: J2 has no constant tangent");
+    return tangent_;
+  }
 
  private:
-  MaterialModel(std::vector<double> t, int d, bool thermal) : tangent_(std::move(t)), dim_(d), thermal_(thermal) {}
+  MaterialModel(std::vector<double> t, int d, bool thermal)
+      : kind_(thermal ? Kind::Conductivity : Kind::LinearElastic), tangent_(std::move(t)), dim_(d), thermal_(thermal) {}
+  Kind kind_;
   std::vector<double> tangent_;
   int dim_;
   bool thermal_;
+  double j2_[4] = {0, 0, 0, 0};
+};
+
+// material.hpp:83-97: data[q * width + i]
+struct InternalState {
+  int width = 0;
+  Index quads = 0;
+  std::vector<double> data;
+  InternalState() = default;
+  InternalState(int width_, Index quads_)
+      : width(width_), quads(quads_), data(static_cast<std::size_t>(width_ * quads_), 0.0) {}
 };
 
 // material.hpp:100-118
@@ -171,6 +229,14 @@ struct MaterialMap {
   std::vector<std::uint8_t> phase;
   int node_components(int d) const { return catalog.front().thermal() ? 1 : d; }
   int flux_components() const { return catalog.front().flux_components(); }
+  int internal_width() const {
+    int w = 0;
+    for (const auto& mdl : catalog) w = mdl.internal_width() > w ? mdl.internal_width() : w;
+    return w;
+  }
+  InternalState make_state(const GridLayout& layout) const {
+    return InternalState(internal_width(), layout.num_pixels() * layout.quads_per_pixel());
+  }
 };
 
 // solver.hpp:16-31
@@ -238,6 +304,8 @@ class PrecondManager {
 // solver.hpp:145-161
 struct NewtonOutcome {
   NodalField u;
+  InternalState internal;      // trial state on convergence, g0 otherwise
+  std::vector<double> stress;  // QuadField (num_quads x m), mechanical maps
   std::vector<double> average_stress;
   SolveReport report;
   bool converged = false;
@@ -246,15 +314,16 @@ struct NewtonOutcome {
 namespace detail {
 inline void set_material(homfe_ctx* ctx, const MaterialMap& map) {
   if (map.catalog.empty()) throw ValidationError("materials: catalog is empty");
-  std::vector<double> t;
-  for (const auto& mdl : map.catalog) t.insert(t.end(), mdl.linear_tangent().begin(), mdl.linear_tangent().end());
-  check(homfe_gpu_set_material(ctx, static_cast<int32_t>(map.catalog.size()), t.data(), map.phase.data()));
+  std::vector<homfe_material> models;
+  for (const auto& mdl : map.catalog) models.push_back(mdl.c_model());
+  check(homfe_gpu_set_material_models(ctx, static_cast<int32_t>(models.size()), models.data(), map.phase.data()));
 }
 }  // namespace detail
 
-// newton_solve (solver.hpp:163-166) on the GPU.
-inline NewtonOutcome newton_solve(const GridLayout& layout, const MaterialMap& map, const std::vector<double>& e,
-                                  const SolveConfig& cfg, PrecondManager& precond,
+// newton_solve (solver.hpp:163-166) on the GPU, with the committed internal
+// state g0 (map.make_state(layout) for a fresh start).
+inline NewtonOutcome newton_solve(const GridLayout& layout, const MaterialMap& map, const InternalState& g0,
+                                  const std::vector<double>& e, const SolveConfig& cfg, PrecondManager& precond,
                                   const NodalField* warm_start = nullptr) {
   const int c = map.node_components(layout.dim());
   if (static_cast<Index>(map.phase.size()) != layout.num_pixels())
@@ -279,10 +348,20 @@ inline NewtonOutcome newton_solve(const GridLayout& layout, const MaterialMap& m
   out.average_stress.assign(static_cast<std::size_t>(map.flux_components()), 0.0);
   if (warm_start && (warm_start->components != c || warm_start->nodes != layout.num_nodes()))
     throw ValidationError("warm start has wrong shape");
+  const int width = map.internal_width();
+  const Index nq = layout.num_pixels() * layout.quads_per_pixel();
+  if (g0.width != width || g0.quads != nq) throw ValidationError("internal state does not match layout and catalog");
+  out.internal = InternalState(width, nq);
   homfe_report rep{};
-  const int code = homfe_gpu_solve(ctx, e.data(), &sc, warm_start ? warm_start->data.data() : nullptr,
-                                   out.u.data.data(), out.average_stress.data(), &rep);
+  const int code = homfe_gpu_solve_state(ctx, e.data(), &sc, warm_start ? warm_start->data.data() : nullptr,
+                                         width ? g0.data.data() : nullptr, out.u.data.data(),
+                                         width ? out.internal.data.data() : nullptr, out.average_stress.data(),
+                                         &rep);
   detail::check(code);
+  if (c > 1) {
+    out.stress.assign(static_cast<std::size_t>(nq * map.flux_components()), 0.0);
+    detail::check(homfe_gpu_stress_field(ctx, out.stress.data()));
+  }
   for (int i = 0; i < rep.n_steps && i < 32; ++i) {
     const auto& s = rep.steps[i];
     out.report.steps.push_back({s.cg_iterations, s.residual_initial, s.residual_final, s.increment_rel,
@@ -300,6 +379,13 @@ inline NewtonOutcome newton_solve(const GridLayout& layout, const MaterialMap& m
   return out;
 }
 
+// Linear shorthand (no internal state; linear catalogs).
+inline NewtonOutcome newton_solve(const GridLayout& layout, const MaterialMap& map, const std::vector<double>& e,
+                                  const SolveConfig& cfg, PrecondManager& precond,
+                                  const NodalField* warm_start = nullptr) {
+  return newton_solve(layout, map, map.make_state(layout), e, cfg, precond, warm_start);
+}
+
 struct LoadStepResult {
   std::vector<double> load;
   NewtonOutcome outcome;
@@ -313,9 +399,11 @@ inline std::vector<LoadStepResult> run_load_program(const GridLayout& layout, co
   if (loads.empty()) throw ValidationError("loading: at least one load step is required");
   PrecondManager precond(policy, cfg.reassembly_threshold, map.node_components(layout.dim()));
   std::vector<LoadStepResult> results;
+  InternalState g = map.make_state(layout);
   const NodalField* warm = nullptr;
   for (const auto& e : loads) {
-    results.push_back({e, newton_solve(layout, map, e, cfg, precond, warm)});
+    results.push_back({e, newton_solve(layout, map, g, e, cfg, precond, warm)});
+    if (results.back().outcome.converged) g = results.back().outcome.internal;
     if (!results.back().outcome.converged) break;
     warm = &results.back().outcome.u;
   }

@@ -431,3 +431,22 @@ def test_cpp_drop_in_example_runs(hb):
         r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("converged 1") == 2 and "ValidationError" in r.stdout
+
+
+def test_cpp_drop_in_j2_example_runs(hb):
+    """examples/solve_j2.cpp: J2 catalog through the reference's C++ API
+    (run_load_program with committed InternalState, 7-argument newton_solve)."""
+    import os
+    import subprocess
+    import tempfile
+    from paper_2203_02962_b200 import _native
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.dirname(_native.LIB_PATH)
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "solve_j2")
+        subprocess.run(["g++", "-std=c++17", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "examples", "solve_j2.cpp"), "-o", exe, "-L", lib_dir, "-lhomfe_gpu",
+                        f"-Wl,-rpath,{lib_dir}"], check=True)
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("converged 1") == 3, r.stdout

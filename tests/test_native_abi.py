@@ -102,3 +102,8 @@ def test_cpp_shim_compiles_and_links(tmp_path):
                     os.path.join(ROOT, "examples", "solve_c1.cpp"), "-o", str(out), "-L", lib_dir, "-lhomfe_gpu",
                     f"-Wl,-rpath,{lib_dir}"], check=True)
     assert out.exists()
+    out2 = tmp_path / "solve_j2"
+    subprocess.run(["g++", "-std=c++17", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "solve_j2.cpp"), "-o", str(out2), "-L", lib_dir, "-lhomfe_gpu",
+                    f"-Wl,-rpath,{lib_dir}"], check=True)
+    assert out2.exists()
