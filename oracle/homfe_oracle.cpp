@@ -1529,4 +1529,296 @@ int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, 
   });
 }
 
+
+// ------------------------------------------------- strain-based scheme (f4)
+int or_gamma_apply(const or_grid* g, const double* c_ref, int32_t c, const double* s_in, double* out) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    const int m = grad_components(l.d, c);
+    check_spd(c_ref, m, "reference tangent");
+    std::unique_ptr<or_precond> b(assemble(l, c_ref, c, false));
+    invert(b.get());
+    const Index n = c * l.num_nodes();
+    std::vector<double> div(n), z(n);
+    divergence(l, c, s_in, false, div.data());
+    precond_apply(l, b.get(), div.data(), z.data());
+    gradient(l, c, z.data(), out);
+  });
+}
+
+int or_sb_newton_solve(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
+                       const uint8_t* phase, const double* g0_in, const double* e, const or_solve_cfg* cfg,
+                       const double* c_ref, const double* warm_strain, double* strain_out, double* g_out,
+                       double* avg_out, or_report* rep) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    const int d = l.d, c = thermal ? 1 : d, m = grad_components(d, c), nq = l.nq();
+    if (!(cfg->eta_newton > 0.0 && cfg->eta_newton < 1.0) ||
+        !(cfg->eta_cg > 0.0 && cfg->eta_cg < 1.0))
+      throw ValidationError("solver: tolerances must lie in (0,1)");
+    if (cfg->max_newton < 1 || cfg->max_cg < 1) throw ValidationError("solver: iteration caps must be >= 1");
+    int width = 0;
+    for (int ph = 0; ph < n_phases; ++ph) {
+      if (models[ph].kind == 0) check_spd(models[ph].tangent, m, "material tangent");
+      else width = 7;
+    }
+    for (int k = 0; k < m; ++k)
+      if (!std::isfinite(e[k])) throw ValidationError("load vector has non-finite entries");
+    check_spd(c_ref, m, "reference tangent");
+    const Index nQ = l.num_quads(), nN = c * l.num_nodes(), nS = nQ * m;
+    std::unique_ptr<or_precond> blocks(assemble(l, c_ref, c, false));  // assemble_projection_blocks
+    invert(blocks.get());
+    std::vector<double> gstate((size_t)width * nQ, 0.0);
+    if (width && g0_in) std::copy(g0_in, g0_in + (size_t)width * nQ, gstate.begin());
+    std::vector<double> strain(nS, 0.0);
+    if (warm_strain) std::copy(warm_strain, warm_strain + nS, strain.begin());
+    std::vector<double> sig(nS), tan((size_t)nQ * m * m), trial((size_t)width * nQ), div(nN), z(nN);
+    auto gamma = [&](const double* sv, double* outq) {
+      divergence(l, c, sv, false, div.data());
+      precond_apply(l, blocks.get(), div.data(), z.data());
+      gradient(l, c, z.data(), outq);
+    };
+    auto sweep = [&]() {
+      for (Index q = 0; q < nQ; ++q) {
+        double et[6];
+        for (int k = 0; k < m; ++k) et[k] = e[k] + strain[q * m + k];
+        const or_material& md = models[phase[q / nq]];
+        if (md.kind == 0) {
+          for (int k = 0; k < m; ++k)
+            if (!std::isfinite(et[k])) throw NumericalError("evaluate: non-finite strain input");
+          for (int i = 0; i < m; ++i) {
+            double acc = 0.0;
+            for (int j = 0; j < m; ++j) acc += md.tangent[j * m + i] * et[j];
+            sig[q * m + i] = acc;
+          }
+          std::copy(md.tangent, md.tangent + m * m, tan.data() + (size_t)q * m * m);
+          if (width)
+            for (int i = 0; i < width; ++i) trial[(size_t)q * width + i] = 0.0;
+        } else {
+          j2_eval(d, md.bulk, md.shear, md.yield_stress, md.hardening, et, gstate.data() + (size_t)q * width,
+                  sig.data() + q * m, tan.data() + (size_t)q * m * m, trial.data() + (size_t)q * width);
+        }
+      }
+    };
+    auto tmul = [&](const double* x, double* y) {  // tangent_multiply
+      for (Index q = 0; q < nQ; ++q) {
+        const double* t = tan.data() + (size_t)q * m * m;
+        for (int i = 0; i < m; ++i) {
+          double acc = 0.0;
+          for (int j = 0; j < m; ++j) acc += t[j * m + i] * x[q * m + j];
+          y[q * m + i] = acc;
+        }
+      }
+    };
+    double bnorm0 = 0.0, inc_rel = std::numeric_limits<double>::infinity();
+    bool have_inc = false, converged_state = false;
+    rep->n_steps = 0;
+    rep->assemblies = 1;
+    std::vector<double> b(nS), x(nS), r(nS), pv(nS), cp(nS), ap(nS), etot(nS);
+    for (int step = 0;; ++step) {
+      sweep();
+      gamma(sig.data(), b.data());
+      for (Index i = 0; i < nS; ++i) b[i] = -b[i];
+      const double bnorm = std::sqrt(dot(b.data(), b.data(), nS));
+      if (step == 0) bnorm0 = bnorm;
+      for (Index q = 0; q < nQ; ++q)
+        for (int k = 0; k < m; ++k) etot[q * m + k] = strain[q * m + k] + e[k];
+      const bool b_zero = bnorm == 0.0 || bnorm <= 1e-12 * std::sqrt(dot(etot.data(), etot.data(), nS));
+      const bool residual_ok = bnorm <= cfg->eta_newton * bnorm0;
+      const bool increment_ok = have_inc && inc_rel <= cfg->eta_newton;
+      if (step > 0 && (increment_ok || residual_ok)) {
+        rep->cause = 0;
+        rep->converged = 1;
+        converged_state = true;
+        break;
+      }
+      if (step == cfg->max_newton) {
+        rep->cause = 2;
+        rep->converged = 0;
+        break;
+      }
+      // strain_cg (projection.cpp:54-91): plain CG, Euclidean products
+      int iters = 0;
+      double last = bnorm;
+      bool cg_ok = false;
+      std::fill(x.begin(), x.end(), 0.0);
+      if (b_zero) {
+        cg_ok = true;
+      } else {
+        r = b;
+        double rr = std::max(dot(r.data(), r.data(), nS), 0.0);
+        const double norm0 = std::sqrt(rr);
+        last = norm0;
+        if (norm0 == 0.0) {
+          cg_ok = true;
+        } else {
+          pv = r;
+          for (int k = 1; k <= cfg->max_cg; ++k) {
+            tmul(pv.data(), cp.data());
+            gamma(cp.data(), ap.data());
+            const double pap = dot(pv.data(), ap.data(), nS);
+            if (pap <= 0.0)
+              throw NumericalError("strain cg: non-positive curvature, operator is not positive definite");
+            const double alpha = rr / pap;
+            for (Index i = 0; i < nS; ++i) x[i] += alpha * pv[i];
+            for (Index i = 0; i < nS; ++i) r[i] -= alpha * ap[i];
+            const double rrn = std::max(dot(r.data(), r.data(), nS), 0.0);
+            iters = k;
+            last = std::sqrt(rrn);
+            if (std::sqrt(rrn) <= cfg->eta_cg * norm0) {
+              cg_ok = true;
+              break;
+            }
+            for (Index i = 0; i < nS; ++i) pv[i] = r[i] + (rrn / rr) * pv[i];
+            rr = rrn;
+          }
+        }
+      }
+      for (Index i = 0; i < nS; ++i) strain[i] += x[i];
+      const double num = std::sqrt(weighted_dot(l, m, x.data(), x.data()));
+      const double den = std::sqrt(weighted_dot(l, m, strain.data(), strain.data()));
+      inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+      have_inc = true;
+      if (rep->n_steps < 32) {
+        or_newton_step& st = rep->steps[rep->n_steps];
+        st.cg_iterations = iters;
+        st.residual_initial = bnorm;
+        st.residual_final = last;
+        st.increment_rel = inc_rel;
+        st.precond_reassembled = step == 0 ? 1 : 0;
+      }
+      rep->n_steps += 1;
+      if (!cg_ok) {
+        rep->cause = 1;
+        rep->converged = 0;
+        sweep();
+        break;
+      }
+    }
+    volume_average(l, m, sig.data(), avg_out);
+    if (strain_out) std::copy(strain.begin(), strain.end(), strain_out);
+    if (g_out && width) {
+      const std::vector<double>& src = converged_state ? trial : gstate;
+      std::copy(src.begin(), src.end(), g_out);
+    }
+    if (!rep->converged) throw NonConvergence(rep->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
+// --------------------------------------------- eigenvalue bounds (f4)
+namespace {
+// eigenvalues of a symmetric m x m (cyclic Jacobi)
+void sym_eigs(int m, std::vector<double> a, double& lo, double& hi) {
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int i = 0; i < m; ++i)
+      for (int j = i + 1; j < m; ++j) off += a[i * m + j] * a[i * m + j];
+    if (off < 1e-300) break;
+    for (int p = 0; p < m; ++p)
+      for (int q = p + 1; q < m; ++q) {
+        const double apq = a[p * m + q];
+        if (std::fabs(apq) < 1e-300) continue;
+        const double th = 0.5 * (a[q * m + q] - a[p * m + p]) / apq;
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
+        for (int k = 0; k < m; ++k) {
+          const double akp = a[k * m + p], akq = a[k * m + q];
+          a[k * m + p] = cs * akp - sn * akq;
+          a[k * m + q] = sn * akp + cs * akq;
+        }
+        for (int k = 0; k < m; ++k) {
+          const double apk = a[p * m + k], aqk = a[q * m + k];
+          a[p * m + k] = cs * apk - sn * aqk;
+          a[q * m + k] = sn * apk + cs * aqk;
+        }
+      }
+  }
+  lo = a[0];
+  hi = a[0];
+  for (int i = 1; i < m; ++i) {
+    lo = std::min(lo, a[i * m + i]);
+    hi = std::max(hi, a[i * m + i]);
+  }
+}
+}  // namespace
+
+int or_eigenvalue_bounds(const or_grid* g, const double* tangent, int32_t pixel_constant, const double* c_ref,
+                         int32_t c, double* lower, double* upper, double* cond) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    const int m = grad_components(l.d, c), nq = l.nq();
+    // C_ref = L L^T; L^{-1} by forward substitution
+    std::vector<double> L(m * m, 0.0);
+    for (int j = 0; j < m; ++j) {
+      double s = c_ref[j * m + j];
+      for (int k = 0; k < j; ++k) s -= L[j * m + k] * L[j * m + k];
+      if (!(s > 0.0)) throw ValidationError("eigenvalue_bounds: reference must be positive definite");
+      L[j * m + j] = std::sqrt(s);
+      for (int i = j + 1; i < m; ++i) {
+        double t = c_ref[j * m + i];
+        for (int k = 0; k < j; ++k) t -= L[i * m + k] * L[j * m + k];
+        L[i * m + j] = t / L[j * m + j];
+      }
+    }
+    std::vector<double> Li(m * m, 0.0);  // row-major L^{-1}
+    for (int col = 0; col < m; ++col)
+      for (int i = 0; i < m; ++i) {
+        double t = i == col ? 1.0 : 0.0;
+        for (int k = 0; k < i; ++k) t -= L[i * m + k] * Li[k * m + col];
+        Li[i * m + col] = t / L[i * m + i];
+      }
+    const Index nQ = l.num_quads();
+    std::vector<double> qmin(nQ), qmax(nQ), red(m * m), tmp(m * m);
+    for (Index q = 0; q < nQ; ++q) {
+      if (pixel_constant && q % nq != 0) {
+        qmin[q] = qmin[q - q % nq];
+        qmax[q] = qmax[q - q % nq];
+        continue;
+      }
+      const double* t = tangent + (size_t)q * m * m;  // col-major
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+          double acc = 0.0;
+          for (int k = 0; k < m; ++k) acc += Li[i * m + k] * t[j * m + k];
+          tmp[i * m + j] = acc;  // (L^-1 C)_ij
+        }
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < m; ++j) {
+          double acc = 0.0;
+          for (int k = 0; k < m; ++k) acc += tmp[i * m + k] * Li[j * m + k];
+          red[i * m + j] = acc;
+        }
+      sym_eigs(m, red, qmin[q], qmax[q]);
+      if (!(qmin[q] > 0.0)) throw ValidationError("eigenvalue_bounds: tangent must be positive definite per point");
+    }
+    const Index nn = l.num_nodes();
+    std::vector<double> nmin(nn, std::numeric_limits<double>::infinity()), nmax(nn, 0.0);
+    Walker w(l);
+    for (Index p = 0; p < l.np; ++p) {
+      w.neighbors();
+      for (int lq = 0; lq < nq; ++lq) {
+        const Index q = p * nq + lq;
+        for (const Entry& en : l.quads[lq].entries) {
+          const Index node = static_cast<Index>(en.node) * l.np + w.nbr[en.off];
+          nmin[node] = std::min(nmin[node], qmin[q]);
+          nmax[node] = std::max(nmax[node], qmax[q]);
+        }
+      }
+      w.advance();
+    }
+    std::vector<double> lo((size_t)c * nn), hi((size_t)c * nn);
+    for (Index i = 0; i < nn; ++i)
+      for (int k = 0; k < c; ++k) {
+        lo[i * c + k] = nmin[i];
+        hi[i * c + k] = nmax[i];
+      }
+    std::sort(lo.begin(), lo.end());
+    std::sort(hi.begin(), hi.end());
+    std::copy(lo.begin(), lo.end(), lower);
+    std::copy(hi.begin(), hi.end(), upper);
+    if (!(lo.front() > 0.0)) throw ValidationError("condition_estimate: bounds must be positive");
+    *cond = hi.back() / lo.front();
+  });
+}
+
 }  // extern "C"

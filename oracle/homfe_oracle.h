@@ -144,6 +144,21 @@ int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, 
                            const double* warm_u, double* u_out, double* g_out, double* avg_stress_out,
                            or_report* report);
 
+/* Strain-based scheme (projection.cpp): gamma_apply with the
+   unweighted reference blocks (projection.cpp:22-41), and the SB Newton
+   solve with Gamma-projected strain CG (projection.cpp:43-185). strain in /
+   out: QuadField num_quads x m (warm may be NULL). */
+int or_gamma_apply(const or_grid* g, const double* c_ref, int32_t c, const double* s, double* out);
+int or_sb_newton_solve(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
+                       const uint8_t* phase, const double* g0, const double* e, const or_solve_cfg* cfg,
+                       const double* c_ref, const double* warm_strain, double* strain_out, double* g_out,
+                       double* avg_stress_out, or_report* report);
+/* eigenvalue_bounds (spectral.cpp:33-118): tangent = num_quads m x m blocks
+   (col-major), pixel_constant shortcut flag; lower / upper = c * num_nodes
+   sorted; cond = condition_estimate (spectral.cpp:121-127). */
+int or_eigenvalue_bounds(const or_grid* g, const double* tangent, int32_t pixel_constant, const double* c_ref,
+                         int32_t c, double* lower, double* upper, double* cond);
+
 /* Field reductions (fields.cpp). */
 int or_volume_average(const or_grid* g, int32_t m, const double* s, double* out);
 int or_weighted_dot(const or_grid* g, int32_t m, const double* a, const double* b,

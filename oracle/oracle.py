@@ -393,6 +393,63 @@ def newton_solve_models(g, thermal, models, phase, e, g0=None, eta_newton=1e-5, 
                 assemblies=rep.assemblies)
 
 
+def gamma_apply(g, c_ref, c, s):
+    """projection.cpp:22-41: Gamma s with the unweighted reference blocks."""
+    m = g.m(c)
+    s = _f64(s).ravel()
+    out = np.zeros(g.num_quads * m)
+    cr = _cmat(c_ref, m)
+    _check(lib().or_gamma_apply(g.ref, _ptr(cr), C.c_int32(c), _ptr(s), _ptr(out)))
+    return out.reshape(g.num_quads, m)
+
+
+def sb_newton_solve_models(g, thermal, models, phase, e, c_ref, g0=None, warm_strain=None, eta_newton=1e-5,
+                           eta_cg=1e-5, max_newton=25, max_cg=20000):
+    """sb_newton_solve (projection.cpp:93-185)."""
+    d = g.dim
+    c = 1 if thermal else d
+    m = g.m(c)
+    arr = (_Material * len(models))(*models)
+    ph = np.ascontiguousarray(phase, dtype=np.uint8).ravel()
+    e = _f64(e).ravel()
+    cfg = _Cfg()
+    cfg.eta_newton, cfg.eta_cg = eta_newton, eta_cg
+    cfg.max_newton, cfg.max_cg = max_newton, max_cg
+    cfg.reassembly_threshold = 0.1
+    cr = _cmat(c_ref, m)
+    nq = g.num_quads
+    width = 7 if any(mm.kind == 1 for mm in models) else 0
+    g0a = _f64(g0).ravel() if g0 is not None else None
+    ws = _f64(warm_strain).ravel() if warm_strain is not None else None
+    gout = np.zeros(width * nq)
+    strain = np.zeros(nq * m)
+    avg = np.zeros(m)
+    rep = _Report()
+    code = lib().or_sb_newton_solve(g.ref, C.c_int32(int(thermal)), C.c_int32(len(models)), arr,
+                                    _ptr(ph, C.c_uint8), _ptr(g0a), _ptr(e), C.byref(cfg), _ptr(cr), _ptr(ws),
+                                    _ptr(strain), _ptr(gout) if width else None, _ptr(avg), C.byref(rep))
+    if code not in (0, 3):
+        _check(code)
+    steps = [dict(cg_iterations=rep.steps[i].cg_iterations, residual_initial=rep.steps[i].residual_initial,
+                  residual_final=rep.steps[i].residual_final, increment_rel=rep.steps[i].increment_rel)
+             for i in range(min(rep.n_steps, 32))]
+    return dict(strain=strain.reshape(nq, m), internal=gout, average_stress=avg, converged=bool(rep.converged),
+                cause=["converged", "cg-stall", "newton-cap"][rep.cause], steps=steps)
+
+
+def eigenvalue_bounds(g, tangent, c_ref, c, pixel_constant=False):
+    """eigenvalue_bounds + condition_estimate (spectral.cpp:33-127)."""
+    m = g.m(c)
+    t = np.ascontiguousarray(np.asarray(tangent, dtype=np.float64).transpose(0, 2, 1)).ravel()
+    cr = _cmat(c_ref, m)
+    lo = np.zeros(c * g.num_nodes)
+    hi = np.zeros(c * g.num_nodes)
+    cond = C.c_double()
+    _check(lib().or_eigenvalue_bounds(g.ref, _ptr(t), C.c_int32(int(pixel_constant)), _ptr(cr), C.c_int32(c),
+                                      _ptr(lo), _ptr(hi), C.byref(cond)))
+    return lo, hi, cond.value
+
+
 def volume_average(g, s):
     s = _f64(s)
     m = s.shape[-1]

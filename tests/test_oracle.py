@@ -226,3 +226,97 @@ def test_models_newton_j2_plastic_flow(oracle_mod):
     g = out["internal"].reshape(-1, 7)
     assert g[:, 6].max() > 0.0 and g[:, 6].min() >= 0.0
     assert len(out["steps"]) >= 2  # nonlinear: more than one Newton step
+
+
+# ---------------------------------------- strain-based scheme, bounds (8 f4)
+def test_gamma_fixes_compatible_fields_and_kills_constants(oracle_mod):
+    """test_projection.cpp:26-47."""
+    og = oracle_mod.Grid((4, 4), (1.0, 1.0), "two-triangles")
+    u = oracle_mod.uniform(401, 2 * 16)
+    du = oracle_mod.gradient(og, 2, u)
+    proj = oracle_mod.gamma_apply(og, np.eye(3), 2, du)
+    assert np.abs(proj - du).max() < 1e-10 * np.abs(du).max()
+    const = np.tile([1.0, -2.0, 0.5], (og.num_quads, 1))
+    assert np.abs(oracle_mod.gamma_apply(og, np.eye(3), 2, const)).max() < 1e-12
+
+
+def test_gamma_matches_dense_pinv_composition(oracle_mod, golden):
+    """test_projection.cpp:49-64: Gamma = D (D^T D)^+ D^T."""
+    dims = (3, 3)
+    og = oracle_mod.Grid(dims, (1.0, 1.0), "two-triangles")
+    D, _ = golden.dense_gradient(dims, (1.0, 1.0), "two-triangles", 2)
+    gd = D @ golden.dense_pinv(D.T @ D) @ D.T
+    s = oracle_mod.uniform(409, og.num_quads * 3).reshape(og.num_quads, 3)
+    flat = s.T.ravel()  # dense rows are component-major
+    want = (gd @ flat).reshape(3, og.num_quads).T
+    assert np.abs(oracle_mod.gamma_apply(og, np.eye(3), 2, s) - want).max() < 1e-10
+
+
+def test_sb_uniform_material_converges_immediately(oracle_mod):
+    """test_projection.cpp:108-123."""
+    og = oracle_mod.Grid((6, 6), (1.0, 1.0), "two-triangles")
+    mat = oracle_mod.material("linear", oracle_mod.isotropic_stiffness(1.0, 0.6, 2))
+    out = oracle_mod.sb_newton_solve_models(og, False, [mat], np.zeros(36, np.uint8), [0.5, -0.1, 0.2], np.eye(3))
+    assert out["converged"] and len(out["steps"]) == 1
+    assert np.abs(out["strain"]).max() < 1e-12
+
+
+@pytest.mark.parametrize("plastic", [False, True])
+def test_db_sb_equivalence(oracle_mod, plastic):
+    """test_projection.cpp:125-170: Newton counts equal, CG counts within 1,
+    strain discrepancy small (linear 1e-8, J2 two steps 1e-6)."""
+    og = oracle_mod.Grid((8, 8), (1.0, 1.0), "two-triangles")
+    ph = (oracle_mod.uniform(1001 if not plastic else 77, 64) > 0.0).astype(np.uint8)
+    if plastic:
+        mats = [oracle_mod.material("j2", bulk=0.833, shear=0.385, yield_stress=3e-3, hardening=0.08),
+                oracle_mod.material("j2", bulk=0.833, shear=0.385, yield_stress=6e-3, hardening=0.16)]
+        loads = [np.array([4e-3, -4e-3, 0.0]), np.array([6e-3, -6e-3, 0.0])]
+    else:
+        mats = [oracle_mod.material("linear", oracle_mod.isotropic_stiffness(1.0, 0.5, 2)),
+                oracle_mod.material("linear", oracle_mod.isotropic_stiffness(35.0, 17.0, 2))]
+        loads = [np.array([1.0, -0.2, 0.35])]
+    kw = dict(eta_newton=1e-5, eta_cg=1e-5)
+    g_db = g_sb = None
+    w_db = w_sb = None
+    for e in loads:
+        db = oracle_mod.newton_solve_models(og, False, mats, ph, e, g0=g_db, warm_u=w_db, reference="explicit",
+                                            reference_matrix=np.eye(3), **kw)
+        sb = oracle_mod.sb_newton_solve_models(og, False, mats, ph, e, np.eye(3), g0=g_sb, warm_strain=w_sb, **kw)
+        assert db["converged"] and sb["converged"]
+        assert len(db["steps"]) == len(sb["steps"])
+        assert all(abs(a["cg_iterations"] - b["cg_iterations"]) <= 1 for a, b in zip(db["steps"], sb["steps"]))
+        db_strain = oracle_mod.gradient(og, 2, db["u"])
+        disc = np.abs(sb["strain"] - db_strain).max() / np.abs(db_strain).max()
+        assert disc < (1e-6 if plastic else 1e-8)
+        g_db, g_sb, w_db, w_sb = db["internal"], sb["internal"], db["u"], sb["strain"]
+    if plastic:
+        assert len(db["steps"]) > 1
+
+
+def test_bounds_collapse_for_perfect_reference(oracle_mod):
+    """test_spectral.cpp:52-61."""
+    og = oracle_mod.Grid((4, 4), (1.0, 1.0), "two-triangles")
+    c = oracle_mod.isotropic_stiffness(1.1, 0.7, 2)
+    t = np.repeat(c[None], og.num_quads, axis=0)
+    lo, hi, cond = oracle_mod.eigenvalue_bounds(og, t, c, 2)
+    assert np.abs(lo - 1.0).max() < 1e-12 and np.abs(hi - 1.0).max() < 1e-12
+    assert abs(cond - 1.0) < 1e-12
+
+
+def test_thermal_bounds_match_support_sweep(oracle_mod, golden):
+    """test_spectral.cpp:63-108."""
+    dims = (4, 4)
+    og = oracle_mod.Grid(dims, (1.0, 1.0), "two-triangles")
+    ph = oracle_mod.uniform(307, 16) > 0.0
+    kap = np.where(np.repeat(ph, og.quads_per_pixel), 20.0, 0.05)
+    t = kap[:, None, None] * np.eye(2)[None]
+    lo, hi, _ = oracle_mod.eigenvalue_bounds(og, t, np.eye(2), 1, pixel_constant=True)
+    D, _ = golden.dense_gradient(dims, (1.0, 1.0), "two-triangles", 1)
+    nq = og.num_quads
+    blo, bhi = [], []
+    for n in range(og.num_nodes):
+        sup = [q for q in range(nq) if any(D[k * nq + q, n] != 0.0 for k in range(2))]
+        blo.append(min(kap[q] for q in sup))
+        bhi.append(max(kap[q] for q in sup))
+    assert np.abs(lo - np.sort(blo)).max() < 1e-12
+    assert np.abs(hi - np.sort(bhi)).max() < 1e-12
