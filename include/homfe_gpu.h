@@ -161,6 +161,22 @@ int homfe_gpu_solve_state(homfe_ctx* ctx, const double* e, const homfe_solve_cfg
    QuadField layout, fields.hpp:40-62). Mechanical contexts. */
 int homfe_gpu_stress_field(homfe_ctx* ctx, double* out);
 
+/* ---- strain-based scheme and spectral bounds --------------- */
+/* gamma_apply (projection.cpp:29-41) with the reference set by
+   homfe_gpu_set_reference: s_in / s_out num_quads x m QuadFields. */
+int homfe_gpu_gamma_apply(homfe_ctx* ctx, const double* s_in, double* s_out);
+/* sb_newton_solve (projection.cpp:93-185): Newton on the fluctuating strain
+   with Gamma-projected CG, fixed reference c_ref (m x m col-major). strain in
+   (warm, nullable) / out: num_quads x m; g0 / g_out as homfe_gpu_solve_state. */
+int homfe_gpu_sb_solve(homfe_ctx* ctx, const double* e, const homfe_solve_cfg* cfg, const double* c_ref,
+                       const double* warm_strain, const double* g0, double* strain_out, double* g_out,
+                       double* avg_stress_out, homfe_report* report);
+/* eigenvalue_bounds + condition_estimate (spectral.cpp:33-127): tangent =
+   num_quads blocks m x m col-major; lower / upper = components * num_nodes,
+   sorted ascending. */
+int homfe_gpu_eigenvalue_bounds(homfe_ctx* ctx, const double* tangent, int32_t pixel_constant,
+                                const double* c_ref, double* lower, double* upper, double* cond);
+
 /* ---- parity hooks (host buffers) ---------------------------------------- */
 /* apply_tangent_operator (operators.hpp:31-33) with the material set above. */
 int homfe_gpu_apply_K(homfe_ctx* ctx, const double* u, double* ku);

@@ -383,8 +383,9 @@ class Preconditioner:
     """Inverted Fourier blocks of the reference operator (precond.hpp:28-79)."""
 
     def __init__(self, grid, c_ref, components, weighted=True):
-        if not weighted:
-            raise ValidationError("unweighted reference operators are not on the GPU path")
+        # unweighted blocks (projection.cpp:22-27): with equal Gauss weights
+        # (all one-node stencils here) they are the weighted ones / w
+        self.weighted = bool(weighted)
         self.grid = grid
         self.components = components
         self.c_ref = np.array(c_ref, dtype=float)
@@ -404,7 +405,8 @@ class Preconditioner:
         ctx.set_reference(self.c_ref)
         out = np.zeros(self.num_frequencies * self.components * self.components * 2)
         _check(lib.homfe_gpu_reference_blocks(ctx.h, _dp(out)))
-        return out.view(np.complex128).reshape(self.num_frequencies, self.components, self.components)
+        blocks = out.view(np.complex128).reshape(self.num_frequencies, self.components, self.components)
+        return blocks if self.weighted else blocks / self.grid.quad_weights()[0]
 
 
 def assemble_preconditioner(grid, c_ref, components, weighted=True):
@@ -421,7 +423,43 @@ def apply_preconditioner(grid, preconditioner, r):
     ctx.set_reference(preconditioner.c_ref)
     out = np.zeros_like(r)
     _check(lib.homfe_gpu_apply_minv(ctx.h, _dp(r), _dp(out)))
+    return out if preconditioner.weighted else out * grid.quad_weights()[0]
+
+
+def gamma_apply(grid, preconditioner, s):
+    """Compatibility projection D (D^T C_ref D)^+ D^T (projection.cpp:29-41,
+    module.cpp:270-277); the blocks must be assembled unweighted."""
+    if preconditioner.weighted:
+        raise ValidationError("gamma_apply: blocks must be assembled without the weight fusion")
+    s = _quad(grid, s)
+    ctx = grid.context(preconditioner.components)
+    if s.shape[1] != ctx.m:
+        raise ValidationError("gamma_apply: field shape mismatch")
+    ctx.set_reference(preconditioner.c_ref)
+    out = np.zeros_like(s)
+    _check(lib.homfe_gpu_gamma_apply(ctx.h, _dp(s), _dp(out)))
     return out
+
+
+def eigenvalue_bounds(grid, tangent, c_ref, components, pixel_constant=False):
+    """Sorted two-sided eigenvalue bounds and the condition estimate
+    (spectral.cpp:33-127, module.cpp:286-297)."""
+    ctx = grid.context(components)
+    m = ctx.m
+    t = np.asarray(tangent, dtype=float)
+    if t.shape != (grid.num_quads, m, m):
+        raise ValidationError("eigenvalue_bounds: tangent does not match layout")
+    cr = np.asarray(c_ref, dtype=float)
+    if cr.shape != (m, m):
+        raise ValidationError("eigenvalue_bounds: reference has wrong size")
+    tc = _f64(t.transpose(0, 2, 1))
+    crc = _f64(cr.T)
+    lo = np.zeros(components * grid.num_nodes)
+    hi = np.zeros(components * grid.num_nodes)
+    cond = C.c_double()
+    _check(lib.homfe_gpu_eigenvalue_bounds(ctx.h, _dp(tc), int(pixel_constant), _dp(crc), _dp(lo), _dp(hi),
+                                           C.byref(cond)))
+    return lo, hi, cond.value
 
 
 def volume_average(grid, s):
@@ -543,6 +581,36 @@ class Solver:
         return out
 
 
+def _solver_sb_solve(self, e, c_ref, internal=None, warm_strain=None, raise_on_nonconvergence=False):
+    m = self.ctx.m
+    e = _f64(e).ravel()
+    if e.size != m:
+        raise ValidationError(f"load vector has {e.size} components, expected {m}")
+    nq = self.grid.num_quads
+    cr = _f64(np.asarray(c_ref, dtype=float).T)
+    if cr.size != m * m:
+        raise ValidationError("reference: explicit matrix has wrong size")
+    ws = _f64(warm_strain).reshape(-1) if warm_strain is not None else None
+    if ws is not None and ws.size != nq * m:
+        raise ValidationError("sb warm start has wrong shape")
+    g0 = _f64(internal).reshape(-1) if (internal is not None and self.nonlinear) else None
+    strain = np.zeros((nq, m))
+    g_out = np.zeros((nq, 7)) if self.nonlinear else None
+    avg = np.zeros(m)
+    rep = _native.Report()
+    code = lib.homfe_gpu_sb_solve(self.ctx.h, _dp(e), C.byref(self.cfg), _dp(cr), _dp(ws), _dp(g0), _dp(strain),
+                                  _dp(g_out), _dp(avg), C.byref(rep))
+    if code != _native.NONCONVERGED or raise_on_nonconvergence:
+        _check(code)
+    out = dict(converged=bool(rep.converged), strain=strain, average_stress=avg, report=_report_dict(rep))
+    if self.nonlinear:
+        out["internal"] = g_out
+    return out
+
+
+Solver.sb_solve = _solver_sb_solve
+
+
 def newton_solve(grid, materials, phases, e, eta_newton=1e-5, eta_cg=1e-5, max_newton=25, max_cg=20000,
                  reassembly_threshold=0.1, reference="volume-mean", reference_scale=1.0, reference_matrix=None,
                  criterion="strain"):
@@ -551,6 +619,49 @@ def newton_solve(grid, materials, phases, e, eta_newton=1e-5, eta_cg=1e-5, max_n
     s = Solver(grid, materials, phases, eta_newton, eta_cg, max_newton, max_cg, reassembly_threshold, reference,
                reference_scale, reference_matrix, criterion)
     return s.solve(e, stress=not s.ctx.c == 1)
+
+
+def sb_newton_solve(grid, materials, phases, e, c_ref, internal=None, warm_strain=None, eta_newton=1e-5,
+                    eta_cg=1e-5, max_newton=25, max_cg=20000):
+    """Strain-based scheme (projection.cpp:93-185): Newton on the
+    fluctuating strain with Gamma-projected CG at a fixed reference."""
+    s = Solver(grid, materials, phases, eta_newton, eta_cg, max_newton, max_cg)
+    return s.sb_solve(e, c_ref, internal=internal, warm_strain=warm_strain)
+
+
+def compare_db_sb(grid, materials, phases, loads, c_ref, eta_newton=1e-5, eta_cg=1e-5, max_newton=25,
+                  max_cg=20000, reassembly_threshold=0.1):
+    """DbSbComparison (projection.cpp:216-262): both schemes on one load
+    program at matched tolerances and the same reference tangent."""
+    s = Solver(grid, materials, phases, eta_newton, eta_cg, max_newton, max_cg, reassembly_threshold,
+               reference="explicit", reference_matrix=c_ref)
+    out = dict(db_reports=[], sb_reports=[], db_average_stress=[], sb_average_stress=[], strain_discrepancy=[],
+               converged=True)
+    g_db = g_sb = None
+    w_db = w_sb = None
+    db_u = []
+    for e in loads:
+        r = s.solve(e, warm_start=w_db, internal=g_db)
+        out["converged"] &= r["converged"]
+        if r["converged"] and s.nonlinear:
+            g_db = r["internal"]
+        out["db_reports"].append(r["report"])
+        out["db_average_stress"].append(r["average_stress"])
+        db_u.append(r["u"])
+        w_db = r["u"]
+    for i, e in enumerate(loads):
+        r = s.sb_solve(e, c_ref, internal=g_sb, warm_strain=w_sb)
+        out["converged"] &= r["converged"]
+        if r["converged"] and s.nonlinear:
+            g_sb = r["internal"]
+        out["sb_reports"].append(r["report"])
+        out["sb_average_stress"].append(r["average_stress"])
+        w_sb = r["strain"]
+        db_strain = gradient_apply(grid, db_u[i])
+        scale = np.abs(db_strain).max()
+        diff = np.abs(r["strain"] - db_strain).max()
+        out["strain_discrepancy"].append(diff / scale if scale > 0 else diff)
+    return out
 
 
 def run_load_program(grid, materials, phases, loads, eta_newton=1e-5, eta_cg=1e-5, max_newton=25, max_cg=20000,

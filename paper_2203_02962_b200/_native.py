@@ -83,6 +83,9 @@ def _load():
         "homfe_gpu_internal_width": (C.c_int, [vp, P(i32), P(i64)]),
         "homfe_gpu_solve_state": (C.c_int, [vp, P(d), P(SolveCfg), P(d), P(d), P(d), P(d), P(d), P(Report)]),
         "homfe_gpu_stress_field": (C.c_int, [vp, P(d)]),
+        "homfe_gpu_gamma_apply": (C.c_int, [vp, P(d), P(d)]),
+        "homfe_gpu_sb_solve": (C.c_int, [vp, P(d), P(SolveCfg), P(d), P(d), P(d), P(d), P(d), P(d), P(Report)]),
+        "homfe_gpu_eigenvalue_bounds": (C.c_int, [vp, P(d), i32, P(d), P(d), P(d), P(d)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -100,4 +103,5 @@ EXPORTED = ("homfe_gpu_last_error", "homfe_isotropic_stiffness", "homfe_gpu_crea
             "homfe_gpu_volume_average", "homfe_gpu_pcg", "homfe_gpu_index_maps", "homfe_gpu_sizes",
             "homfe_random_uniform", "homfe_random_normal", "homfe_gpu_kernel_times",
             "homfe_nccl_unique_id", "homfe_gpu_create_dist", "homfe_gpu_set_material_models",
-            "homfe_gpu_internal_width", "homfe_gpu_solve_state", "homfe_gpu_stress_field")
+            "homfe_gpu_internal_width", "homfe_gpu_solve_state", "homfe_gpu_stress_field",
+            "homfe_gpu_gamma_apply", "homfe_gpu_sb_solve", "homfe_gpu_eigenvalue_bounds")

@@ -9,6 +9,7 @@
 // host never synchronises inside a solve.
 #include <cufft.h>
 #include <nccl.h>
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <random>
@@ -111,6 +112,9 @@ struct homfe_ctx {
          *d_tpart = nullptr;
   int* d_status = nullptr;
   bool sig_valid = false;           // d_sig holds the last solve's stress
+  // strain-based scheme (projection.cpp): quad-space unknown and CG vectors
+  double *d_strain = nullptr, *d_sx = nullptr, *d_sr = nullptr, *d_sp = nullptr, *d_sap = nullptr,
+         *d_scp = nullptr;
   bool hex_fast = false, hex_iso = false;
   // vectors
   double *d_x = nullptr, *d_r = nullptr, *d_p = nullptr, *d_ap = nullptr, *d_z = nullptr, *d_u = nullptr;
@@ -1010,6 +1014,175 @@ bool newton_nl(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double
   return converged_state;
 }
 
+
+void ensure_sb_buffers(homfe_ctx* c) {
+  if (c->d_strain) return;
+  const size_t n = (size_t)c->g.np * c->sp.nq * c->g.m;
+  c->d_strain = dalloc<double>(n);
+  c->d_sx = dalloc<double>(n);
+  c->d_sr = dalloc<double>(n);
+  c->d_sp = dalloc<double>(n);
+  c->d_sap = dalloc<double>(n);
+  c->d_scp = dalloc<double>(n);
+}
+
+// Gamma s = D (D^T C_ref D)^+ D^T s (projection.cpp:29-41). With equal
+// Gauss weights (required by the reference, projection.cpp:12-17) the
+// unweighted blocks and divergence equal the weighted ones up to the weight
+// factor, which cancels: Gamma = D M_w^-1 D^T W.
+void gamma_apply(homfe_ctx* c, const double* s_in, double* out, cudaStream_t st) {
+  launch_divergence(c->g, c->sp, s_in, true, c->d_r, st);
+  precond_apply(c, c->d_r, c->d_z, nullptr, nullptr, st);
+  QuadArgs a{c->d_z, c->d_hhi, nullptr, c->d_phase, c->d_cmat, out, nullptr};
+  launch_quad(c->g, c->sp, kQuadGrad, a, st);
+  c->launches += 5;
+}
+
+double qdot(homfe_ctx* c, const double* a, const double* b, int64_t n) {
+  launch_dot_partials(a, b, n, c->d_partials, c->stream);
+  double v = 0.0;
+  reduce_to_host(c, 1, &v);
+  return v;
+}
+
+// sb_newton_solve (projection.cpp:93-185) with strain_cg (:54-91). The
+// unknown (fluctuating strain, compatible by construction) lives in d_strain.
+bool sb_newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* cref, double* avg_out,
+               homfe_report* rep) {
+  const auto t_total = Clock::now();
+  validate_cfg(cfg);
+  require_material(c);
+  if (c->dist) throw ValidationError("sb_newton_solve: single-GPU contexts only");
+  const int m = c->g.m;
+  for (int k = 0; k < m; ++k)
+    if (!std::isfinite(e[k])) throw ValidationError("load vector has non-finite entries");
+  std::memset(rep, 0, sizeof(*rep));
+  c->launches = 0;
+  ensure_nl_buffers(c);
+  ensure_sb_buffers(c);
+  if ((int)c->models.size() != c->n_phases) {
+    c->models.assign(c->n_phases, NLModel{0, 0.0, 0.0, 0.0, 0.0});
+    HB_CUDA(cudaMemcpy(c->d_models, c->models.data(), c->models.size() * sizeof(NLModel), cudaMemcpyHostToDevice));
+  }
+  HB_CUDA(cudaMemcpyAsync(c->d_e, e, m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  // assemble_projection_blocks
+  auto t0 = Clock::now();
+  if (!c->have_ref || std::vector<double>(cref, cref + m * m) != c->c_ref) set_reference(c, cref);
+  rep->assemblies = 1;
+  rep->seconds_assembly += since(t0);
+  const int64_t nq = c->g.np * c->sp.nq, ns = nq * m;
+  const double wq = c->g.cell_volume / (double)nq;  // equal Gauss weights
+  NLArgs na = nl_args(c, nullptr);
+  na.qeps = c->d_strain;
+  double bnorm0 = 0.0, inc_rel = INFINITY;
+  bool have_inc = false, converged_state = false;
+  auto sweep = [&]() {
+    HB_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(int), c->stream));
+    launch_sweep(c->g, c->sp, na, c->stream);
+    int bad = 0;
+    HB_CUDA(cudaMemcpyAsync(&bad, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (bad) throw NumericalError("evaluate: non-finite strain input");
+    c->sig_valid = true;
+  };
+  for (int step = 0;; ++step) {
+    t0 = Clock::now();
+    sweep();
+    rep->seconds_constitutive += since(t0);
+    // b = -Gamma sigma
+    gamma_apply(c, c->d_sig, c->d_sr, c->stream);
+    launch_scale(c->d_sr, -1.0, ns, c->stream);
+    const double bnorm = std::sqrt(std::max(0.0, qdot(c, c->d_sr, c->d_sr, ns)));
+    if (step == 0) bnorm0 = bnorm;
+    launch_qshift_norm2(c->d_strain, c->d_e, nq, m, c->d_partials, c->stream);
+    double et2 = 0.0;
+    reduce_to_host(c, 1, &et2);
+    const bool b_is_zero = bnorm == 0.0 || bnorm <= 1e-12 * std::sqrt(et2);
+    const bool residual_ok = bnorm <= cfg->eta_newton * bnorm0;
+    const bool increment_ok = have_inc && inc_rel <= cfg->eta_newton;
+    if (step > 0 && (increment_ok || residual_ok)) {
+      rep->cause = 0;
+      rep->converged = 1;
+      converged_state = true;
+      break;
+    }
+    if (step == cfg->max_newton) {
+      rep->cause = 2;
+      rep->converged = 0;
+      break;
+    }
+    // strain_cg: r = b (d_sr), x = 0, p = r
+    t0 = Clock::now();
+    HB_CUDA(cudaMemsetAsync(c->d_sx, 0, ns * sizeof(double), c->stream));
+    int iters = 0;
+    double last = bnorm;
+    bool cg_ok = false;
+    if (b_is_zero) {
+      cg_ok = true;
+    } else {
+      double rr = std::max(qdot(c, c->d_sr, c->d_sr, ns), 0.0);
+      const double norm0 = std::sqrt(rr);
+      last = norm0;
+      if (norm0 == 0.0) {
+        cg_ok = true;
+      } else {
+        HB_CUDA(cudaMemcpyAsync(c->d_sp, c->d_sr, ns * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        for (int k = 1; k <= cfg->max_cg; ++k) {
+          launch_tan_mult(c->g, c->sp, na, c->d_sp, c->d_scp, c->stream);
+          gamma_apply(c, c->d_scp, c->d_sap, c->stream);
+          const double pap = qdot(c, c->d_sp, c->d_sap, ns);
+          if (pap <= 0.0)
+            throw NumericalError("strain cg: non-positive curvature, operator is not positive definite");
+          const double alpha = rr / pap;
+          launch_axpy(c->d_sx, alpha, c->d_sp, ns, c->stream);
+          launch_axpy(c->d_sr, -alpha, c->d_sap, ns, c->stream);
+          const double rrn = std::max(qdot(c, c->d_sr, c->d_sr, ns), 0.0);
+          iters = k;
+          last = std::sqrt(rrn);
+          c->launches += 4;
+          if (std::sqrt(rrn) <= cfg->eta_cg * norm0) {
+            cg_ok = true;
+            break;
+          }
+          // p = r + (rrn / rr) p
+          launch_scale(c->d_sp, rrn / rr, ns, c->stream);
+          launch_axpy(c->d_sp, 1.0, c->d_sr, ns, c->stream);
+          rr = rrn;
+        }
+      }
+    }
+    rep->seconds_cg += since(t0);
+    launch_axpy(c->d_strain, 1.0, c->d_sx, ns, c->stream);
+    const double num = std::sqrt(wq * qdot(c, c->d_sx, c->d_sx, ns));
+    const double den = std::sqrt(wq * qdot(c, c->d_strain, c->d_strain, ns));
+    inc_rel = den > 0.0 ? num / den : (num > 0.0 ? 1.0 : 0.0);
+    have_inc = true;
+    if (rep->n_steps < 32) {
+      homfe_newton_step& sr = rep->steps[rep->n_steps];
+      sr.cg_iterations = iters;
+      sr.residual_initial = bnorm;
+      sr.residual_final = last;
+      sr.increment_rel = inc_rel;
+      sr.precond_reassembled = step == 0 ? 1 : 0;
+    }
+    rep->n_steps += 1;
+    rep->total_cg += iters;
+    if (!cg_ok) {
+      rep->cause = 1;
+      rep->converged = 0;
+      sweep();
+      break;
+    }
+  }
+  launch_quad_wsum(c->g, c->sp, c->d_sig, c->d_partials, c->stream);
+  double avg[6];
+  reduce_to_host(c, m, avg);
+  for (int k = 0; k < m; ++k) avg_out[k] = avg[k] / c->g.cell_volume;
+  rep->seconds_total = since(t_total);
+  rep->kernel_launches = c->launches;
+  return converged_state;
+}
+
 }  // namespace
 
 // ===================================================================== C ABI
@@ -1267,9 +1440,13 @@ int homfe_gpu_destroy(homfe_ctx* c) {
   if (c->fwd) cufftDestroy(c->fwd);
   if (c->inv) cufftDestroy(c->inv);
   double* bufs[] = {c->d_x, c->d_r, c->d_p, c->d_ap, c->d_z, c->d_u, c->d_ke, c->d_fe, c->d_cmat, c->d_hexmat, c->d_tri,
+                    c->d_strain, c->d_sx, c->d_sr, c->d_sp, c->d_sap, c->d_scp, c->d_g0, c->d_gtr, c->d_tanc,
+                    c->d_sig, c->d_qs, c->d_tpart,
                     c->d_quad, c->d_partials, c->d_scal, c->d_hist, c->d_e};
   for (double* b : bufs)
     if (b) cudaFree(b);
+  if (c->d_models) cudaFree(c->d_models);
+  if (c->d_status) cudaFree(c->d_status);
   for (auto* t : c->d_tab)
     if (t) cudaFree(t);
   if (c->d_spec) cudaFree(c->d_spec);
@@ -1406,6 +1583,104 @@ int homfe_gpu_solve_state(homfe_ctx* c, const double* e, const homfe_solve_cfg* 
     if (u_out) HB_CUDA(cudaMemcpyAsync(u_out, c->d_u, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     if (!r->converged) throw NonConverged(r->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
+int homfe_gpu_gamma_apply(homfe_ctx* c, const double* s_in, double* s_out) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    require_reference(c);
+    if (c->dist) throw ValidationError("gamma_apply: single-GPU contexts only");
+    ensure_sb_buffers(c);
+    const size_t n = (size_t)c->g.np * c->sp.nq * c->g.m;
+    HB_CUDA(cudaMemcpyAsync(c->d_sp, s_in, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    gamma_apply(c, c->d_sp, c->d_sap, c->stream);
+    HB_CUDA(cudaMemcpyAsync(s_out, c->d_sap, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  });
+}
+
+int homfe_gpu_sb_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* c_ref,
+                       const double* warm_strain, const double* g0, double* strain_out, double* g_out,
+                       double* avg_out, homfe_report* rep) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    if (!c_ref) throw ValidationError("sb_newton_solve: reference tangent required");
+    require_material(c);
+    ensure_nl_buffers(c);
+    ensure_sb_buffers(c);
+    const int64_t nq = c->g.np * c->sp.nq;
+    const size_t ns = (size_t)nq * c->g.m, gq = (size_t)nq * 7;
+    if (warm_strain) HB_CUDA(cudaMemcpyAsync(c->d_strain, warm_strain, ns * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    else HB_CUDA(cudaMemsetAsync(c->d_strain, 0, ns * sizeof(double), c->stream));
+    if (c->nonlinear) {
+      if (g0) HB_CUDA(cudaMemcpyAsync(c->d_g0, g0, gq * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+      else HB_CUDA(cudaMemsetAsync(c->d_g0, 0, gq * sizeof(double), c->stream));
+    }
+    homfe_report local;
+    homfe_report* r = rep ? rep : &local;
+    const bool ok = sb_newton(c, e, cfg, c_ref, avg_out, r);
+    if (strain_out)
+      HB_CUDA(cudaMemcpyAsync(strain_out, c->d_strain, ns * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (g_out && c->nonlinear)
+      HB_CUDA(cudaMemcpyAsync(g_out, ok ? c->d_gtr : c->d_g0, gq * sizeof(double), cudaMemcpyDeviceToHost,
+                              c->stream));
+    sync(c);
+    if (!r->converged) throw NonConverged(r->cause == 1 ? "cg-stall" : "newton-cap");
+  });
+}
+
+int homfe_gpu_eigenvalue_bounds(homfe_ctx* c, const double* tangent, int32_t pixel_constant, const double* c_ref,
+                                double* lower, double* upper, double* cond) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    if (c->dist) throw ValidationError("eigenvalue_bounds: single-GPU contexts only");
+    const int m = c->g.m;
+    // C_ref = L L^T (spectral.cpp:41-53)
+    std::vector<double> L(m * m, 0.0), Li(m * m, 0.0);
+    for (int j = 0; j < m; ++j) {
+      double sum = c_ref[j * m + j];
+      for (int k = 0; k < j; ++k) sum -= L[j * m + k] * L[j * m + k];
+      if (!(sum > 0.0)) throw ValidationError("eigenvalue_bounds: reference must be positive definite");
+      L[j * m + j] = std::sqrt(sum);
+      for (int i = j + 1; i < m; ++i) {
+        double t = c_ref[j * m + i];
+        for (int k = 0; k < j; ++k) t -= L[i * m + k] * L[j * m + k];
+        L[i * m + j] = t / L[j * m + j];
+      }
+    }
+    for (int col = 0; col < m; ++col)
+      for (int i = 0; i < m; ++i) {
+        double t = i == col ? 1.0 : 0.0;
+        for (int k = 0; k < i; ++k) t -= L[i * m + k] * Li[k * m + col];
+        Li[i * m + col] = t / L[i * m + i];
+      }
+    const int64_t nq = c->g.np * c->sp.nq, nn = c->g.np;
+    const int cc = c->g.c;
+    double* d_t = nullptr;
+    double *d_lo = nullptr, *d_hi = nullptr, *d_lo2 = nullptr, *d_hi2 = nullptr;
+    HB_CUDA(cudaMallocAsync(&d_t, (size_t)nq * m * m * sizeof(double), c->stream));
+    HB_CUDA(cudaMallocAsync(&d_lo, (size_t)nn * cc * sizeof(double), c->stream));
+    HB_CUDA(cudaMallocAsync(&d_hi, (size_t)nn * cc * sizeof(double), c->stream));
+    HB_CUDA(cudaMallocAsync(&d_lo2, (size_t)nn * cc * sizeof(double), c->stream));
+    HB_CUDA(cudaMallocAsync(&d_hi2, (size_t)nn * cc * sizeof(double), c->stream));
+    HB_CUDA(cudaMemcpyAsync(d_t, tangent, (size_t)nq * m * m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    const int st = bounds_device(c->g, c->sp, d_t, pixel_constant, Li.data(), cc, d_lo, d_hi, c->stream);
+    if (st == 2) throw ValidationError("eigenvalue_bounds: tangent must be positive definite per point");
+    // sorted sequences (spectral.cpp:115-116): device radix sort
+    size_t tmp_bytes = 0;
+    const int nk = (int)(nn * cc);
+    HB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, d_lo, d_lo2, nk, 0, 64, c->stream));
+    void* d_tmp = nullptr;
+    HB_CUDA(cudaMallocAsync(&d_tmp, tmp_bytes, c->stream));
+    HB_CUDA(cub::DeviceRadixSort::SortKeys(d_tmp, tmp_bytes, d_lo, d_lo2, nk, 0, 64, c->stream));
+    HB_CUDA(cub::DeviceRadixSort::SortKeys(d_tmp, tmp_bytes, d_hi, d_hi2, nk, 0, 64, c->stream));
+    HB_CUDA(cudaMemcpyAsync(lower, d_lo2, (size_t)nk * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HB_CUDA(cudaMemcpyAsync(upper, d_hi2, (size_t)nk * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    for (void* ptr : {(void*)d_t, (void*)d_lo, (void*)d_hi, (void*)d_lo2, (void*)d_hi2, d_tmp}) cudaFree(ptr);
+    if (!(lower[0] > 0.0)) throw ValidationError("condition_estimate: bounds must be positive");
+    if (cond) *cond = upper[nk - 1] / lower[0];
   });
 }
 

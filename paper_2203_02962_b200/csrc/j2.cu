@@ -30,6 +30,11 @@ namespace {
 
 constexpr double kS32 = 1.2247448713915890491;  // sqrt(3/2)
 
+template <int M>
+struct LinvM {
+  double v[M * M];  // row-major L^-1 (C_ref = L L^T)
+};
+
 __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
 // Mandel gradient rows at Gauss point q from the element corner values
@@ -144,19 +149,26 @@ __global__ void __launch_bounds__(kBlock) k_sweep(const Grid g, const __grid_con
       c0 = (int)(p / g.n1);
     }
     double uv[8][3];
-    for (int o = 0; o < sp.noff; ++o) {
-      const int i0 = wrapi(c0 + sp.offs[o][0], g.n0), i1 = wrapi(c1 + sp.offs[o][1], g.n1);
-      const int i2 = D == 3 ? wrapi(c2 + sp.offs[o][2], g.n2) : 0;
-      const int64_t nd = D == 3 ? ((int64_t)i0 * g.n1 + i1) * g.n2 + i2 : (int64_t)i0 * g.n1 + i1;
+    if (!a.qeps) {
+      for (int o = 0; o < sp.noff; ++o) {
+        const int i0 = wrapi(c0 + sp.offs[o][0], g.n0), i1 = wrapi(c1 + sp.offs[o][1], g.n1);
+        const int i2 = D == 3 ? wrapi(c2 + sp.offs[o][2], g.n2) : 0;
+        const int64_t nd = D == 3 ? ((int64_t)i0 * g.n1 + i1) * g.n2 + i2 : (int64_t)i0 * g.n1 + i1;
 #pragma unroll
-      for (int k = 0; k < C; ++k) uv[o][k] = a.u ? a.u[k * np + nd] : 0.0;
+        for (int k = 0; k < C; ++k) uv[o][k] = a.u ? a.u[k * np + nd] : 0.0;
+      }
     }
     const int ph = a.phase[p];
     const NLModel md = a.models[ph];
     for (int q = 0; q < sp.nq; ++q) {
       const int64_t qi = p * sp.nq + q;
       double eps[M];
-      grad_rows<D, C>(sp, q, uv, eps);
+      if (a.qeps) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) eps[k] = a.qeps[qi * M + k];
+      } else {
+        grad_rows<D, C>(sp, q, uv, eps);
+      }
 #pragma unroll
       for (int k = 0; k < M; ++k) {
         eps[k] += E[k];
@@ -308,7 +320,211 @@ __global__ void __launch_bounds__(kBlock) k_tan_stress(const Grid g, const __gri
   }
 }
 
+template <int D, int C>
+__global__ void __launch_bounds__(kBlock) k_tan_mult(const Grid g, const __grid_constant__ StencilParams sp,
+                                                      const NLArgs a, const double* __restrict__ x,
+                                                      double* __restrict__ y) {
+  constexpr int M = C == 1 ? D : (D == 2 ? 3 : 6);
+  constexpr int NV = M * M;
+  const int64_t nq = g.np * sp.nq;
+  for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < nq; qi += (int64_t)gridDim.x * blockDim.x) {
+    const int ph = a.phase[qi / sp.nq];
+    const NLModel md = a.models[ph];
+    double ev[M], sv[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) ev[k] = x[qi * M + k];
+    if (md.kind == 0) {
+      const double* cm = a.cmat + (size_t)ph * NV;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        double t = 0.0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) t = fma(cm[j * M + i], ev[j], t);
+        sv[i] = t;
+      }
+    } else {
+      const double* tc = a.tanc + qi * 8;
+      double e6[6], s6[6];
+      embed6<D>(ev, e6);
+      compact_apply(md.k, md.g, tc[0], tc[1], tc + 2, e6, s6);
+      extract<D>(s6, sv);
+    }
+#pragma unroll
+    for (int k = 0; k < M; ++k) y[qi * M + k] = sv[k];
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_qshift_norm2(const double* __restrict__ x, const double* __restrict__ e,
+                                                          int64_t nq, int m, double* partials) {
+  double acc = 0.0;
+  for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < nq; qi += (int64_t)gridDim.x * blockDim.x)
+    for (int k = 0; k < m; ++k) {
+      const double v = x[qi * m + k] + (e ? e[k] : 0.0);
+      acc = fma(v, v, acc);
+    }
+  double arr[1] = {acc};
+  block_sum_store_nv<1>(arr, partials + blockIdx.x);
+}
+
+// per point: extreme generalized eigenvalues of (C_q, C_ref) via the
+// reduced pencil L^-1 C L^-T (cyclic Jacobi, m <= 6)
+template <int M>
+__global__ void __launch_bounds__(kBlock) k_bounds_quad(const double* __restrict__ tan, int64_t nq, int nqp,
+                                                         int pixel_constant, const __grid_constant__ LinvM<M> li,
+                                                         double* qmin, double* qmax, int* status) {
+  for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < nq; qi += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t src = pixel_constant ? qi - qi % nqp : qi;
+    const double* t = tan + src * M * M;  // column-major
+    double tmp[M][M], a[M][M];
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) acc = fma(li.v[i * M + k], t[j * M + k], acc);
+        tmp[i][j] = acc;
+      }
+#pragma unroll
+    for (int i = 0; i < M; ++i)
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) acc = fma(tmp[i][k], li.v[j * M + k], acc);
+        a[i][j] = acc;
+      }
+    for (int sweep = 0; sweep < 60; ++sweep) {
+      double off = 0.0;
+#pragma unroll
+      for (int i = 0; i < M; ++i)
+#pragma unroll
+        for (int j = i + 1; j < M; ++j) off += a[i][j] * a[i][j];
+      if (off < 1e-300) break;
+#pragma unroll
+      for (int pp = 0; pp < M; ++pp)
+#pragma unroll
+        for (int qq = pp + 1; qq < M; ++qq) {
+          const double apq = a[pp][qq];
+          if (fabs(apq) < 1e-300) continue;
+          const double th = 0.5 * (a[qq][qq] - a[pp][pp]) / apq;
+          const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+          const double cs = 1.0 / sqrt(tt * tt + 1.0), sn = tt * cs;
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const double akp = a[k][pp], akq = a[k][qq];
+            a[k][pp] = cs * akp - sn * akq;
+            a[k][qq] = sn * akp + cs * akq;
+          }
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const double apk = a[pp][k], aqk = a[qq][k];
+            a[pp][k] = cs * apk - sn * aqk;
+            a[qq][k] = sn * apk + cs * aqk;
+          }
+        }
+    }
+    double lo = a[0][0], hi = a[0][0];
+#pragma unroll
+    for (int i = 1; i < M; ++i) {
+      lo = fmin(lo, a[i][i]);
+      hi = fmax(hi, a[i][i]);
+    }
+    if (!(lo > 0.0)) status[0] = 2;
+    qmin[qi] = lo;
+    qmax[qi] = hi;
+  }
+}
+
+// node min / max over the Gauss points whose basis supports the node
+// (spectral.cpp:84-105), written c times per node (interleaved, i * c + k)
+template <int D>
+__global__ void __launch_bounds__(kBlock) k_bounds_nodes(const Grid g, const __grid_constant__ StencilParams sp,
+                                                          const double* qmin, const double* qmax, int c,
+                                                          double* lower, double* upper) {
+  const int64_t np = g.np;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < np; n += (int64_t)gridDim.x * blockDim.x) {
+    int c0, c1, c2 = 0;
+    if (D == 3) {
+      c2 = (int)(n % g.n2);
+      const int64_t t = n / g.n2;
+      c1 = (int)(t % g.n1);
+      c0 = (int)(t / g.n1);
+    } else {
+      c1 = (int)(n % g.n1);
+      c0 = (int)(n / g.n1);
+    }
+    double mn = INFINITY, mx = 0.0;
+    for (int o = 0; o < sp.noff; ++o) {
+      const int e0 = wrapi(c0 - sp.offs[o][0], g.n0), e1 = wrapi(c1 - sp.offs[o][1], g.n1);
+      const int e2 = D == 3 ? wrapi(c2 - sp.offs[o][2], g.n2) : 0;
+      const int64_t ep = D == 3 ? ((int64_t)e0 * g.n1 + e1) * g.n2 + e2 : (int64_t)e0 * g.n1 + e1;
+      for (int q = 0; q < sp.nq; ++q) {
+        bool sup = false;
+        for (int en = 0; en < sp.ne[q]; ++en)
+          if (sp.off[q][en] == o) sup = true;
+        if (!sup) continue;
+        mn = fmin(mn, qmin[ep * sp.nq + q]);
+        mx = fmax(mx, qmax[ep * sp.nq + q]);
+      }
+    }
+    for (int k = 0; k < c; ++k) {
+      lower[n * c + k] = mn;
+      upper[n * c + k] = mx;
+    }
+  }
+}
+
 }  // namespace
+
+void launch_tan_mult(const Grid& g, const StencilParams& sp, const NLArgs& a, const double* x, double* y,
+                     cudaStream_t s) {
+  if (g.d == 2 && g.c == 2) k_tan_mult<2, 2><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, x, y);
+  else if (g.d == 3 && g.c == 3) k_tan_mult<3, 3><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, x, y);
+  else if (g.d == 2 && g.c == 1) k_tan_mult<2, 1><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, x, y);
+  else k_tan_mult<3, 1><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, x, y);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_qshift_norm2(const double* x, const double* e, int64_t nq, int m, double* partials, cudaStream_t s) {
+  k_qshift_norm2<<<kRedBlocks, kBlock, 0, s>>>(x, e, nq, m, partials);
+  HB_CUDA(cudaGetLastError());
+}
+
+int bounds_device(const Grid& g, const StencilParams& sp, const double* d_tangent, int pixel_constant,
+                  const double* linv, int c, double* d_lower, double* d_upper, cudaStream_t s) {
+  const int64_t nq = g.np * sp.nq;
+  double* qmin = nullptr;
+  double* qmax = nullptr;
+  int* status = nullptr;
+  HB_CUDA(cudaMallocAsync(&qmin, nq * sizeof(double), s));
+  HB_CUDA(cudaMallocAsync(&qmax, nq * sizeof(double), s));
+  HB_CUDA(cudaMallocAsync(&status, sizeof(int), s));
+  HB_CUDA(cudaMemsetAsync(status, 0, sizeof(int), s));
+#define HB_BQ(M)                                                                          \
+  do {                                                                                    \
+    LinvM<M> li;                                                                          \
+    for (int i = 0; i < M * M; ++i) li.v[i] = linv[i];                                    \
+    k_bounds_quad<M><<<kRedBlocks, kBlock, 0, s>>>(d_tangent, nq, sp.nq, pixel_constant, li, qmin, qmax, status); \
+  } while (0)
+  switch (g.m) {
+    case 2: HB_BQ(2); break;
+    case 3: HB_BQ(3); break;
+    default: HB_BQ(6); break;
+  }
+#undef HB_BQ
+  HB_CUDA(cudaGetLastError());
+  if (g.d == 2) k_bounds_nodes<2><<<kRedBlocks, kBlock, 0, s>>>(g, sp, qmin, qmax, c, d_lower, d_upper);
+  else k_bounds_nodes<3><<<kRedBlocks, kBlock, 0, s>>>(g, sp, qmin, qmax, c, d_lower, d_upper);
+  HB_CUDA(cudaGetLastError());
+  int st = 0;
+  HB_CUDA(cudaMemcpyAsync(&st, status, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HB_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(qmin, s);
+  cudaFreeAsync(qmax, s);
+  cudaFreeAsync(status, s);
+  return st;
+}
 
 void launch_sweep(const Grid& g, const StencilParams& sp, const NLArgs& a, cudaStream_t s) {
   if (g.d == 2 && g.c == 2) k_sweep<2, 2><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a);

@@ -58,8 +58,19 @@ struct NLArgs {
   double* partials;       // sweep: per block m x m of sum_q w C_q
   int* status;            // sweep: set to 1 on a non-finite strain
   int width;              // internal width (7 when any J2 phase)
+  const double* qeps;     // sweep: quad strain field (strain-based scheme) instead of D u
 };
 void launch_sweep(const Grid& g, const StencilParams& sp, const NLArgs& a, cudaStream_t s);
+// y_q = C_q x_q over the quad field (tangent_multiply, strain-based scheme)
+void launch_tan_mult(const Grid& g, const StencilParams& sp, const NLArgs& a, const double* x, double* y,
+                     cudaStream_t s);
+// per-block partials of sum_q |x_q + E|^2 (E nullable)
+void launch_qshift_norm2(const double* x, const double* e, int64_t nq, int m, double* partials, cudaStream_t s);
+// eigenvalue_bounds (spectral.cpp:33-118) on the device: per-point pencil
+// extremes, node min/max over supports, sorted; returns 0 or a status
+// (1: reference not SPD handled by the host; 2: tangent not PD at a point)
+int bounds_device(const Grid& g, const StencilParams& sp, const double* d_tangent, int pixel_constant,
+                  const double* linv_rowmajor, int c, double* d_lower, double* d_upper, cudaStream_t s);
 void launch_tan_stress(const Grid& g, const StencilParams& sp, const NLArgs& a, const PcgState* st, cudaStream_t s);
 void launch_phase_counts(const uint8_t* ph, int64_t n, unsigned long long* counts, cudaStream_t s);
 // mode 0: sum_q w |D u + e|^2 / h^3 (1 partial per block); 1: sum_q w C (D u + e) / h^3 (m per block)
