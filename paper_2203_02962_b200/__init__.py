@@ -12,8 +12,10 @@ Deviations forced by the GPU design (documented in DESIGN.md):
   * operators act on pixel-constant linear tangents (a phase map plus a
     catalog of at most 256 m x m matrices) instead of arbitrary per-point
     TangentFields; ``apply_operator`` converts a pixel-constant tangent array;
-  * J2 plasticity, the FourTrianglesTwoNode stencil and the strain-based
-    projection scheme are not on this path.
+  * J2 plasticity runs on the device with compact per-point tangents; the
+    FourTrianglesTwoNode stencil uses the impulse-probed complex blocks; the
+    strain-based scheme and spectral bounds are on the device too
+    (SURVEY.md section 8(f) rows f1, f3, f4).
 """
 from __future__ import annotations
 
@@ -403,9 +405,11 @@ class Preconditioner:
         """K_ref_hat(xi), (num_frequencies, c, c), before inversion."""
         ctx = self.grid.context(self.components)
         ctx.set_reference(self.c_ref)
-        out = np.zeros(self.num_frequencies * self.components * self.components * 2)
+        bd = self.block_dim
+        out = np.zeros(self.num_frequencies * bd * bd * 2)
         _check(lib.homfe_gpu_reference_blocks(ctx.h, _dp(out)))
-        blocks = out.view(np.complex128).reshape(self.num_frequencies, self.components, self.components)
+        # column-major blocks (precond.hpp:38-45) -> (frequency, row, col)
+        blocks = out.view(np.complex128).reshape(self.num_frequencies, bd, bd).transpose(0, 2, 1)
         return blocks if self.weighted else blocks / self.grid.quad_weights()[0]
 
 

@@ -45,6 +45,8 @@ struct StencilParams {
   double w[kMaxQuads];                     // quadrature weights
   int noff;                                // distinct offsets (4 or 8)
   int offs[8][3];                          // offset vectors (axis 0 slowest)
+  int node[kMaxQuads][kMaxEntries];        // node type of each entry (0 corner, 1 centre)
+  int nn;                                  // node types per pixel (1, or 2 for FourTrianglesTwoNode)
 };
 
 // Periodic grid geometry. 2-D grids use (n0, n1) with n2 = 1.
@@ -54,7 +56,7 @@ struct Grid {
   int m;        // gradient components (d or Mandel d(d+1)/2)
   int kind;     // StencilKind
   int n0, n1, n2;
-  int64_t np;   // pixels == nodes (one node type per pixel)
+  int64_t np;   // pixels (nodes = nn * np)
   double h[3];
   double cell_volume;
   // slab decomposition along axis 0 (dist = 1): n0 / np are the LOCAL plane
@@ -62,6 +64,7 @@ struct Grid {
   int dist;
   int n0g, z0, rank, world;
   int64_t npg;
+  int nn;       // node types per pixel (grid.hpp nodes_per_pixel)
 };
 
 // PCG scalars resident on the device (solver.cpp:62-94).

@@ -112,6 +112,12 @@ struct homfe_ctx {
          *d_tpart = nullptr;
   int* d_status = nullptr;
   bool sig_valid = false;           // d_sig holds the last solve's stress
+  // impulse-probed block preconditioner (probe.cu), node types per pixel > 1
+  double2* d_blocks = nullptr;      // inverted blocks (nf x b x b)
+  double2* d_blocks_raw = nullptr;  // K_ref_hat before inversion (reference_blocks hook)
+  uint8_t* d_phase0 = nullptr;      // zero phase map for the reference operator
+  NLModel* d_model0 = nullptr;
+  double* d_cref = nullptr;
   // strain-based scheme (projection.cpp): quad-space unknown and CG vectors
   double *d_strain = nullptr, *d_sx = nullptr, *d_sr = nullptr, *d_sp = nullptr, *d_sap = nullptr,
          *d_scp = nullptr;
@@ -158,7 +164,8 @@ struct homfe_ctx {
   double2* d_spec_r = nullptr;      // all-to-all receive buffers of the fused passes
   double2* d_spec2_r = nullptr;
 
-  int64_t nvec() const { return (int64_t)g.c * g.np; }
+  int64_t nvec() const { return (int64_t)g.c * g.nn * g.np; }
+  int64_t nodes() const { return (int64_t)g.nn * g.np; }
 };
 
 namespace {
@@ -244,6 +251,16 @@ void fft_inverse(homfe_ctx* c, double* out, cudaStream_t s) {
 // z = M^-1 r; optional Parseval r.z partials.
 void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st, double* partials,
                    cudaStream_t s) {
+  if (c->g.nn > 1) {
+    // apply_preconditioner (precond.cpp:126-162): all slices D2Z, block
+    // matvec per frequency (1/N_p folded in), all slices Z2D
+    fft_forward(c, r, s);
+    launch_probe_apply(c->d_spec, c->d_blocks, c->nf, c->g.c * c->g.nn, 1.0 / (double)c->g.np, s);
+    fft_inverse(c, z, s);
+    if (partials) launch_dot_partials(r, z, c->nvec(), partials, s);
+    c->launches += 4;
+    return;
+  }
   if (c->fused) {
     fused_forward(c->ff, c->spp, const_cast<double*>(r), nullptr, nullptr, partials, s, 1);
     all_to_all(c, c->ff.T, c->ff.Trecv, c->ff.chunk_t(), s);
@@ -278,7 +295,7 @@ NLArgs nl_args(homfe_ctx* c, const double* u) {
 
 void apply_K(homfe_ctx* c, const double* u, double* out, const double* fe, double scale, double* partials,
              const PcgState* st, cudaStream_t s) {
-  if (c->nl_op) {
+  if (c->nl_op || c->g.nn > 1) {  // two node types: the quadrature-point path
     // tangent operator of the current Newton state: sigma_q = C_q (D u)_q,
     // then the weighted divergence (operators.cpp:197-257 in two passes)
     NLArgs a = nl_args(c, u);
@@ -308,9 +325,63 @@ void require_reference(homfe_ctx* c) {
 
 // assemble_reference + invert_blocks (precond.cpp:44-124) for the analytic
 // symbol: validate C_ref, load the tensor, run the singularity test.
+void ensure_nl_buffers(homfe_ctx* c);
+
+// assemble_reference + invert_blocks (precond.cpp:44-124) by impulse probing,
+// for stencils with two node types (complex Hermitian blocks, probe.cu).
+void probe_assemble(homfe_ctx* c, const double* cref) {
+  const int m = c->g.m, b = c->g.c * c->g.nn;
+  const int64_t np = c->g.np, nv = c->nvec();
+  ensure_nl_buffers(c);
+  if (!c->d_blocks) {
+    c->d_blocks = dalloc<double2>((size_t)c->nf * b * b);
+    c->d_blocks_raw = dalloc<double2>((size_t)c->nf * b * b);
+    c->d_phase0 = dalloc<uint8_t>(np);
+    HB_CUDA(cudaMemset(c->d_phase0, 0, np));
+    c->d_model0 = reinterpret_cast<NLModel*>(dalloc<double>(sizeof(NLModel) / sizeof(double) + 1));
+    const NLModel lin{0, 0.0, 0.0, 0.0, 0.0};
+    HB_CUDA(cudaMemcpy(c->d_model0, &lin, sizeof(NLModel), cudaMemcpyHostToDevice));
+    c->d_cref = dalloc<double>(36);
+  }
+  HB_CUDA(cudaMemcpyAsync(c->d_cref, cref, (size_t)m * m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  NLArgs a{};
+  a.u = c->d_p;
+  a.phase = c->d_phase0;
+  a.models = c->d_model0;
+  a.cmat = c->d_cref;
+  a.sig = c->d_qs;
+  const double one = 1.0;
+  for (int col = 0; col < b; ++col) {
+    // one impulse per (component, node type) slice -> one block column
+    HB_CUDA(cudaMemsetAsync(c->d_p, 0, nv * sizeof(double), c->stream));
+    HB_CUDA(cudaMemcpyAsync(c->d_p + (int64_t)col * np, &one, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    launch_tan_stress(c->g, c->sp, a, nullptr, c->stream);
+    launch_divergence(c->g, c->sp, c->d_qs, true, c->d_ap, c->stream);
+    fft_forward(c, c->d_ap, c->stream);
+    launch_probe_store(c->d_spec, b, c->nf, col, c->d_blocks_raw, c->stream);
+  }
+  HB_CUDA(cudaMemcpyAsync(c->d_blocks, c->d_blocks_raw, (size_t)c->nf * b * b * sizeof(double2),
+                          cudaMemcpyDeviceToDevice, c->stream));
+  HB_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(int), c->stream));
+  launch_probe_invert(c->d_blocks, c->nf, b, c->g.nn, c->d_status, c->stream);
+  int st = 0;
+  HB_CUDA(cudaMemcpyAsync(&st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  sync(c);
+  if (st == 1) throw NumericalError("invert_blocks: singular zero-frequency block");
+  if (st == 2) throw NumericalError("invert_blocks: singular non-zero-frequency block");
+}
+
 void set_reference(homfe_ctx* c, const double* cref) {
   const int m = c->g.m, d = c->g.d;
   check_spd(cref, m, "reference tangent");
+  if (c->g.nn > 1) {
+    c->have_ref = false;
+    destroy_graphs(c);
+    probe_assemble(c, cref);
+    c->c_ref.assign(cref, cref + m * m);
+    c->have_ref = true;
+    return;
+  }
   SpecParams& p = c->spp;
   if (c->g.c == 1) {
     for (int j = 0; j < d; ++j)
@@ -381,12 +452,13 @@ void capture_init(homfe_ctx* c, cudaStream_t s) {
 }
 
 void remove_means_on(homfe_ctx* c, double* v, cudaStream_t s) {
-  launch_comp_sums(v, c->g.c, c->g.np, c->d_partials, s);
+  const int64_t nodes = c->nodes();
+  launch_comp_sums(v, c->g.c, nodes, c->d_partials, s);
   if (c->dist) {
-    launch_sub_means(v, c->g.c, c->g.np, reduce_global(c, c->g.c, 4, s), s, (double)c->g.npg);
+    launch_sub_means(v, c->g.c, nodes, reduce_global(c, c->g.c, 4, s), s, (double)c->g.npg);
   } else {
     launch_final_sum(c->d_partials, kRedBlocks, c->g.c, c->d_scal, s);
-    launch_sub_means(v, c->g.c, c->g.np, c->d_scal, s);
+    launch_sub_means(v, c->g.c, nodes, c->d_scal, s);
   }
 }
 
@@ -416,10 +488,16 @@ void body_sequence(homfe_ctx* c, cudaStream_t s, bool cond, cudaGraphConditional
   apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s);
   launch_pcg_alpha(c->d_st, c->d_partials, s);
   launch_update_r(c->d_r, c->d_ap, n, c->d_st, s);
-  fft_forward(c, c->d_r, s);
-  launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s);
-  launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
-  fft_inverse(c, c->d_z, s);
+  if (c->g.nn > 1) {
+    // probed blocks: z = M^-1 r, then r.z in real space
+    precond_apply(c, c->d_r, c->d_z, c->d_st, c->d_partials, s);
+    launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
+  } else {
+    fft_forward(c, c->d_r, s);
+    launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s);
+    launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
+    fft_inverse(c, c->d_z, s);
+  }
   if (cond) launch_update_xp_cond(c->d_x, c->d_p, c->d_z, n, c->d_st, h, s);
   else launch_update_xp(c->d_x, c->d_p, c->d_z, n, c->d_st, s);
 }
@@ -670,6 +748,13 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
     const std::vector<double>& t = hex_iso ? iso : gen;
     HB_CUDA(cudaMemcpyAsync(c->d_hexmat, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     hex_fast = true;
+  }
+  if (c->g.nn > 1) {
+    // two node types run on the quadrature-point path with linear models
+    ensure_nl_buffers(c);
+    c->models.assign(n_phases, NLModel{0, 0.0, 0.0, 0.0, 0.0});
+    HB_CUDA(cudaMemcpyAsync(c->d_models, c->models.data(), c->models.size() * sizeof(NLModel),
+                            cudaMemcpyHostToDevice, c->stream));
   }
   sync(c);
   if (hex_fast != c->hex_fast || hex_iso != c->hex_iso || n_phases != c->n_phases)
@@ -1271,6 +1356,8 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     if ((int64_t)c * g.np >= (int64_t)1 << 31) throw ValidationError("cell: grid too large for one device");
     ctx->dist = dist;
     ctx->sp = make_stencil(g.kind, d, g.h);
+    g.nn = ctx->sp.nn;
+    if (g.nn > 1 && dist) throw ValidationError("slab mode: one-node stencils only");
     ctx->nl = ctx->sp.noff;
     ctx->ne = ctx->nl * c;
     const int nh = (d == 3 ? g.n2 : g.n1) / 2 + 1;
@@ -1300,7 +1387,7 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     // passes (16-column blocks, fftfused.cu) when that is larger
     const int64_t pitch = ((int64_t)(g.n2 / 2 + 1) + 15) / 16 * 16;
     const int64_t fused_sz = d == 3 ? (int64_t)c * g.n0 * g.n1 * pitch : 0;
-    ctx->d_spec = dalloc<double2>(std::max<int64_t>(dist ? 0 : (int64_t)c * ctx->nf, fused_sz));
+    ctx->d_spec = dalloc<double2>(std::max<int64_t>(dist ? 0 : (int64_t)c * g.nn * ctx->nf, fused_sz));
     ctx->d_phase = dalloc<uint8_t>(g.np);
     ctx->d_partials = dalloc<double>((size_t)kRedBlocks * 8);
     ctx->d_scal = dalloc<double>(64);
@@ -1313,8 +1400,10 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     if (!dist) {
       // cuFFT plans: batched over the c components (component-planar fields)
       int nn[3] = {g.n0, g.n1, g.n2};
-      HB_CUFFT(cufftPlanMany(&ctx->fwd, d, nn, nullptr, 1, (int)g.np, nullptr, 1, (int)ctx->nf, CUFFT_D2Z, c));
-      HB_CUFFT(cufftPlanMany(&ctx->inv, d, nn, nullptr, 1, (int)ctx->nf, nullptr, 1, (int)g.np, CUFFT_Z2D, c));
+      HB_CUFFT(cufftPlanMany(&ctx->fwd, d, nn, nullptr, 1, (int)g.np, nullptr, 1, (int)ctx->nf, CUFFT_D2Z,
+                             c * g.nn));
+      HB_CUFFT(cufftPlanMany(&ctx->inv, d, nn, nullptr, 1, (int)ctx->nf, nullptr, 1, (int)g.np, CUFFT_Z2D,
+                             c * g.nn));
     }
     // per-axis phase tables for the analytic symbol (global grid)
     SpecParams& p = ctx->spp;
@@ -1446,6 +1535,11 @@ int homfe_gpu_destroy(homfe_ctx* c) {
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (c->d_models) cudaFree(c->d_models);
+  if (c->d_blocks) cudaFree(c->d_blocks);
+  if (c->d_blocks_raw) cudaFree(c->d_blocks_raw);
+  if (c->d_phase0) cudaFree(c->d_phase0);
+  if (c->d_model0) cudaFree(c->d_model0);
+  if (c->d_cref) cudaFree(c->d_cref);
   if (c->d_status) cudaFree(c->d_status);
   for (auto* t : c->d_tab)
     if (t) cudaFree(t);
@@ -1503,7 +1597,7 @@ int homfe_gpu_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, c
     else HB_CUDA(cudaMemsetAsync(c->d_u, 0, n * sizeof(double), c->stream));
     homfe_report local;
     homfe_report* r = rep ? rep : &local;
-    if (c->nonlinear) {
+    if (c->nonlinear || c->g.nn > 1) {
       HB_CUDA(cudaMemsetAsync(c->d_g0, 0, (size_t)c->g.np * c->sp.nq * 7 * sizeof(double), c->stream));
       newton_nl(c, e, cfg, avg_out, r);
     } else {
@@ -1570,7 +1664,7 @@ int homfe_gpu_solve_state(homfe_ctx* c, const double* e, const homfe_solve_cfg* 
     else HB_CUDA(cudaMemsetAsync(c->d_u, 0, n * sizeof(double), c->stream));
     homfe_report local;
     homfe_report* r = rep ? rep : &local;
-    if (c->nonlinear) {
+    if (c->nonlinear || c->g.nn > 1) {
       if (g0) HB_CUDA(cudaMemcpyAsync(c->d_g0, g0, gq * sizeof(double), cudaMemcpyHostToDevice, c->stream));
       else HB_CUDA(cudaMemsetAsync(c->d_g0, 0, gq * sizeof(double), c->stream));
       const bool ok = newton_nl(c, e, cfg, avg_out, r);
@@ -1655,7 +1749,7 @@ int homfe_gpu_eigenvalue_bounds(homfe_ctx* c, const double* tangent, int32_t pix
         for (int k = 0; k < i; ++k) t -= L[i * m + k] * Li[k * m + col];
         Li[i * m + col] = t / L[i * m + i];
       }
-    const int64_t nq = c->g.np * c->sp.nq, nn = c->g.np;
+    const int64_t nq = c->g.np * c->sp.nq, nn = c->nodes();
     const int cc = c->g.c;
     double* d_t = nullptr;
     double *d_lo = nullptr, *d_hi = nullptr, *d_lo2 = nullptr, *d_hi2 = nullptr;
@@ -1761,6 +1855,12 @@ int homfe_gpu_reference_blocks(homfe_ctx* c, double* blocks) {
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_reference(c);
+    if (c->g.nn > 1) {
+      const size_t cntb = (size_t)c->nf * c->g.c * c->g.nn * c->g.c * c->g.nn;
+      HB_CUDA(cudaMemcpyAsync(blocks, c->d_blocks_raw, cntb * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+      sync(c);
+      return;
+    }
     const size_t cnt = (size_t)c->nf * c->g.c * c->g.c;
     double2* d = dalloc<double2>(cnt);
     launch_symbol_dump(c->spp, d, c->stream);

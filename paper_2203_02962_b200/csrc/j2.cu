@@ -40,14 +40,14 @@ __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >
 // Mandel gradient rows at Gauss point q from the element corner values
 // (operators.cpp:16-32 accumulate_rows).
 template <int D, int C>
-__device__ __forceinline__ void grad_rows(const StencilParams& sp, int q, const double (&uv)[8][3], double* gq) {
+__device__ __forceinline__ void grad_rows(const StencilParams& sp, int q, const double (&uv)[9][3], double* gq) {
   constexpr int M = C == 1 ? D : (D == 2 ? 3 : 6);
   const double s2 = 0.70710678118654752440;
 #pragma unroll
   for (int k = 0; k < M; ++k) gq[k] = 0.0;
   for (int en = 0; en < sp.ne[q]; ++en) {
     const double* dp = sp.dphi[q][en];
-    const double* v = uv[sp.off[q][en]];
+    const double* v = uv[sp.node[q][en] ? 8 : sp.off[q][en]];  // slot 8: centre node (type 1)
     if (C == 1) {
 #pragma unroll
       for (int k = 0; k < D; ++k) gq[k] += dp[k] * v[0];
@@ -148,14 +148,19 @@ __global__ void __launch_bounds__(kBlock) k_sweep(const Grid g, const __grid_con
       c1 = (int)(p % g.n1);
       c0 = (int)(p / g.n1);
     }
-    double uv[8][3];
+    double uv[9][3];
     if (!a.qeps) {
+      const int64_t nodes = np * sp.nn;
       for (int o = 0; o < sp.noff; ++o) {
         const int i0 = wrapi(c0 + sp.offs[o][0], g.n0), i1 = wrapi(c1 + sp.offs[o][1], g.n1);
         const int i2 = D == 3 ? wrapi(c2 + sp.offs[o][2], g.n2) : 0;
         const int64_t nd = D == 3 ? ((int64_t)i0 * g.n1 + i1) * g.n2 + i2 : (int64_t)i0 * g.n1 + i1;
 #pragma unroll
-        for (int k = 0; k < C; ++k) uv[o][k] = a.u ? a.u[k * np + nd] : 0.0;
+        for (int k = 0; k < C; ++k) uv[o][k] = a.u ? a.u[k * nodes + nd] : 0.0;
+      }
+      if (sp.nn == 2) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) uv[8][k] = a.u ? a.u[k * nodes + np + p] : 0.0;
       }
     }
     const int ph = a.phase[p];
@@ -284,13 +289,18 @@ __global__ void __launch_bounds__(kBlock) k_tan_stress(const Grid g, const __gri
       c1 = (int)(p % g.n1);
       c0 = (int)(p / g.n1);
     }
-    double uv[8][3];
+    double uv[9][3];
+    const int64_t nodes = np * sp.nn;
     for (int o = 0; o < sp.noff; ++o) {
       const int i0 = wrapi(c0 + sp.offs[o][0], g.n0), i1 = wrapi(c1 + sp.offs[o][1], g.n1);
       const int i2 = D == 3 ? wrapi(c2 + sp.offs[o][2], g.n2) : 0;
       const int64_t nd = D == 3 ? ((int64_t)i0 * g.n1 + i1) * g.n2 + i2 : (int64_t)i0 * g.n1 + i1;
 #pragma unroll
-      for (int k = 0; k < C; ++k) uv[o][k] = a.u[k * np + nd];
+      for (int k = 0; k < C; ++k) uv[o][k] = a.u[k * nodes + nd];
+    }
+    if (sp.nn == 2) {
+#pragma unroll
+      for (int k = 0; k < C; ++k) uv[8][k] = a.u[k * nodes + np + p];
     }
     const int ph = a.phase[p];
     const NLModel md = a.models[ph];
@@ -442,8 +452,11 @@ template <int D>
 __global__ void __launch_bounds__(kBlock) k_bounds_nodes(const Grid g, const __grid_constant__ StencilParams sp,
                                                           const double* qmin, const double* qmax, int c,
                                                           double* lower, double* upper) {
-  const int64_t np = g.np;
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < np; n += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t np = g.np, nodes = np * sp.nn;
+  for (int64_t nd = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; nd < nodes;
+       nd += (int64_t)gridDim.x * blockDim.x) {
+    const int type = (int)(nd / np);
+    const int64_t n = nd - (int64_t)type * np;
     int c0, c1, c2 = 0;
     if (D == 3) {
       c2 = (int)(n % g.n2);
@@ -455,22 +468,22 @@ __global__ void __launch_bounds__(kBlock) k_bounds_nodes(const Grid g, const __g
       c0 = (int)(n / g.n1);
     }
     double mn = INFINITY, mx = 0.0;
-    for (int o = 0; o < sp.noff; ++o) {
+    for (int o = 0; o < (type ? 1 : sp.noff); ++o) {
       const int e0 = wrapi(c0 - sp.offs[o][0], g.n0), e1 = wrapi(c1 - sp.offs[o][1], g.n1);
       const int e2 = D == 3 ? wrapi(c2 - sp.offs[o][2], g.n2) : 0;
       const int64_t ep = D == 3 ? ((int64_t)e0 * g.n1 + e1) * g.n2 + e2 : (int64_t)e0 * g.n1 + e1;
       for (int q = 0; q < sp.nq; ++q) {
         bool sup = false;
         for (int en = 0; en < sp.ne[q]; ++en)
-          if (sp.off[q][en] == o) sup = true;
+          if (sp.off[q][en] == o && sp.node[q][en] == type) sup = true;
         if (!sup) continue;
         mn = fmin(mn, qmin[ep * sp.nq + q]);
         mx = fmax(mx, qmax[ep * sp.nq + q]);
       }
     }
     for (int k = 0; k < c; ++k) {
-      lower[n * c + k] = mn;
-      upper[n * c + k] = mx;
+      lower[nd * c + k] = mn;
+      upper[nd * c + k] = mx;
     }
   }
 }
@@ -529,14 +542,16 @@ int bounds_device(const Grid& g, const StencilParams& sp, const double* d_tangen
 void launch_sweep(const Grid& g, const StencilParams& sp, const NLArgs& a, cudaStream_t s) {
   if (g.d == 2 && g.c == 2) k_sweep<2, 2><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a);
   else if (g.d == 3 && g.c == 3) k_sweep<3, 3><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a);
-  else throw ValidationError("J2 path: mechanical grids only");
+  else if (g.d == 2 && g.c == 1) k_sweep<2, 1><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a);
+  else k_sweep<3, 1><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a);
   HB_CUDA(cudaGetLastError());
 }
 
 void launch_tan_stress(const Grid& g, const StencilParams& sp, const NLArgs& a, const PcgState* st, cudaStream_t s) {
   if (g.d == 2 && g.c == 2) k_tan_stress<2, 2><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, st);
   else if (g.d == 3 && g.c == 3) k_tan_stress<3, 3><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, st);
-  else throw ValidationError("J2 path: mechanical grids only");
+  else if (g.d == 2 && g.c == 1) k_tan_stress<2, 1><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, st);
+  else k_tan_stress<3, 1><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, st);
   HB_CUDA(cudaGetLastError());
 }
 

@@ -132,17 +132,22 @@ __global__ void __launch_bounds__(kBlock) k_apply_elem(const Grid g, const ElemA
 // --------------------------------------------------------- quadrature loop
 // One thread per pixel: gather the element corners, evaluate the Mandel
 // gradient rows at every quadrature point (operators.cpp:16-32, 122-149).
+// uv slots: corner offsets 0..noff-1 (node type 0), slot 8 = the pixel's
+// centre node (type 1, FourTrianglesTwoNode)
+__device__ __forceinline__ int uv_slot(const StencilParams& sp, int q, int en) {
+  return sp.node[q][en] ? 8 : sp.off[q][en];
+}
+
 template <int D, int C>
-__device__ __forceinline__ void quad_grad(const StencilParams& sp, int q, const double (&uv)[8][3],
+__device__ __forceinline__ void quad_grad(const StencilParams& sp, int q, const double (&uv)[9][3],
                                           double* gq) {
   constexpr int M = C == 1 ? D : (D == 2 ? 3 : 6);
   const double s2 = 0.70710678118654752440;
 #pragma unroll
   for (int k = 0; k < M; ++k) gq[k] = 0.0;
   for (int en = 0; en < sp.ne[q]; ++en) {
-    const int loc = sp.off[q][en];
     const double* dp = sp.dphi[q][en];
-    const double* v = uv[loc];
+    const double* v = uv[uv_slot(sp, q, en)];
     if (C == 1) {
 #pragma unroll
       for (int k = 0; k < D; ++k) gq[k] += dp[k] * v[0];
@@ -188,7 +193,8 @@ __global__ void __launch_bounds__(kBlock) k_quad(const Grid g, const __grid_cons
     const int u0 = (c0 + 1 == g.n0 && !g.dist) ? 0 : c0 + 1;
     const int u1 = c1 + 1 == g.n1 ? 0 : c1 + 1;
     const int u2 = D == 3 ? (c2 + 1 == g.n2 ? 0 : c2 + 1) : 0;
-    double uv[8][3];
+    double uv[9][3];
+    const int64_t nodes = np * sp.nn;
     for (int o = 0; o < sp.noff; ++o) {
       const int i0 = sp.offs[o][0] ? u0 : c0;
       const int i1 = sp.offs[o][1] ? u1 : c1;
@@ -202,7 +208,11 @@ __global__ void __launch_bounds__(kBlock) k_quad(const Grid g, const __grid_cons
       }
       const int64_t nd = D == 3 ? ((int64_t)i0 * g.n1 + i1) * g.n2 + i2 : (int64_t)i0 * g.n1 + i1;
 #pragma unroll
-      for (int k = 0; k < C; ++k) uv[o][k] = a.u ? a.u[k * np + nd] : 0.0;
+      for (int k = 0; k < C; ++k) uv[o][k] = a.u ? a.u[k * nodes + nd] : 0.0;
+    }
+    if (sp.nn == 2) {
+#pragma unroll
+      for (int k = 0; k < C; ++k) uv[8][k] = a.u ? a.u[k * nodes + np + p] : 0.0;
     }
     const double* cm = MODE == kQuadStress ? a.cmat + (size_t)a.phase[p] * M * M : nullptr;
     for (int q = 0; q < sp.nq; ++q) {
@@ -240,9 +250,11 @@ __global__ void __launch_bounds__(kBlock) k_divergence(const Grid g, const __gri
   constexpr int M = C == 1 ? D : (D == 2 ? 3 : 6);
   constexpr int NL = 1 << D;
   const double s2 = 0.70710678118654752440;
-  const int64_t np = g.np;
-  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < np;
-       n += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t np = g.np, nodes = np * sp.nn;
+  for (int64_t nd = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; nd < nodes;
+       nd += (int64_t)gridDim.x * blockDim.x) {
+    const int type = (int)(nd / np);  // node type (1 = pixel centre, FourTrianglesTwoNode)
+    const int64_t n = nd - (int64_t)type * np;
     int c0, c1, c2 = 0;
     if (D == 3) {
       c2 = (int)(n % g.n2);
@@ -256,8 +268,8 @@ __global__ void __launch_bounds__(kBlock) k_divergence(const Grid g, const __gri
     double acc[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) acc[k] = 0.0;
-    for (int o = 0; o < NL; ++o) {
-      // element whose corner `o` is this node
+    for (int o = 0; o < (type ? 1 : NL); ++o) {
+      // element whose corner `o` is this node (the centre node: its own pixel)
       const int e0 = wrap(c0 - sp.offs[o][0], g.n0);
       const int e1 = wrap(c1 - sp.offs[o][1], g.n1);
       const int e2 = D == 3 ? wrap(c2 - sp.offs[o][2], g.n2) : 0;
@@ -266,7 +278,7 @@ __global__ void __launch_bounds__(kBlock) k_divergence(const Grid g, const __gri
         const double w = weighted ? sp.w[q] : 1.0;
         const double* sv = s + (ep * sp.nq + q) * M;
         for (int en = 0; en < sp.ne[q]; ++en) {
-          if (sp.off[q][en] != o) continue;
+          if (sp.off[q][en] != o || sp.node[q][en] != type) continue;
           const double* dp = sp.dphi[q][en];
           if (C == 1) {
             double t = 0.0;
@@ -285,7 +297,7 @@ __global__ void __launch_bounds__(kBlock) k_divergence(const Grid g, const __gri
       }
     }
 #pragma unroll
-    for (int k = 0; k < C; ++k) out[k * np + n] = acc[k];
+    for (int k = 0; k < C; ++k) out[k * nodes + nd] = acc[k];
   }
 }
 
@@ -560,7 +572,7 @@ void launch_quad(const Grid& g, const StencilParams& sp, int mode, const QuadArg
 
 void launch_divergence(const Grid& g, const StencilParams& sp, const double* sf, bool weighted, double* out,
                        cudaStream_t s) {
-  const int blocks = grid_for(g.np);
+  const int blocks = grid_for(g.np * sp.nn);
   if (g.d == 2 && g.c == 1) k_divergence<2, 1><<<blocks, kBlock, 0, s>>>(g, sp, sf, weighted, out);
   else if (g.d == 2 && g.c == 2) k_divergence<2, 2><<<blocks, kBlock, 0, s>>>(g, sp, sf, weighted, out);
   else if (g.d == 3 && g.c == 1) k_divergence<3, 1><<<blocks, kBlock, 0, s>>>(g, sp, sf, weighted, out);

@@ -72,6 +72,10 @@ void launch_qshift_norm2(const double* x, const double* e, int64_t nq, int m, do
 int bounds_device(const Grid& g, const StencilParams& sp, const double* d_tangent, int pixel_constant,
                   const double* linv_rowmajor, int c, double* d_lower, double* d_upper, cudaStream_t s);
 void launch_tan_stress(const Grid& g, const StencilParams& sp, const NLArgs& a, const PcgState* st, cudaStream_t s);
+// impulse-probed block preconditioner (probe.cu), Nn = 2 stencils
+void launch_probe_store(const double2* spec, int b, int64_t nf, int col, double2* blocks, cudaStream_t s);
+void launch_probe_invert(double2* blocks, int64_t nf, int b, int nn, int* status, cudaStream_t s);
+void launch_probe_apply(double2* spec, const double2* blocks, int64_t nf, int b, double scale, cudaStream_t s);
 void launch_phase_counts(const uint8_t* ph, int64_t n, unsigned long long* counts, cudaStream_t s);
 // mode 0: sum_q w |D u + e|^2 / h^3 (1 partial per block); 1: sum_q w C (D u + e) / h^3 (m per block)
 bool launch_hex_quad(const Grid& g, int mode, const double* u, const double* halo_hi, const double* e,

@@ -237,7 +237,8 @@ __global__ void __launch_bounds__(256) k_elem2d(const Grid g, const ElemArgs a, 
 
 bool elem2d_eligible(const Grid& g) {
   // small (L2-resident) grids have too few strips: the generic pixel-parallel kernel wins
-  return g.d == 2 && (g.c == 1 || g.c == 2) && !g.dist && g.n1 >= 2 && g.n0 >= 2 && g.np >= (1 << 20);
+  return g.d == 2 && (g.c == 1 || g.c == 2) && !g.dist && g.n1 >= 2 && g.n0 >= 2 && g.np >= (1 << 20) &&
+         g.nn == 1;
 }
 
 // Per-phase triangle tables (TwoTriangles): scalar A_ij = w C_ij / (h_i h_j);

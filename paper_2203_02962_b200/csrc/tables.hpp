@@ -18,6 +18,7 @@ namespace hb {
 inline StencilParams make_stencil(int kind, int d, const double* h) {
   StencilParams s;
   std::memset(&s, 0, sizeof(s));
+  s.nn = 1;
   const double vp = d == 2 ? h[0] * h[1] : h[0] * h[1] * h[2];
   static const int quad_off[4][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {1, 1, 0}};
   static const int hex_off[8][3] = {{0, 0, 0}, {0, 0, 1}, {0, 1, 0}, {0, 1, 1},
@@ -88,7 +89,27 @@ inline StencilParams make_stencil(int kind, int d, const double* h) {
         }
     return s;
   }
-  if (kind == 2) throw ValidationError("stencil: four-triangles-two-node is not supported on the GPU path");
+  if (kind == 2) {  // FourTrianglesTwoNode: four triangles fanned around the centre node
+    if (d != 2) throw ValidationError("stencil: four-triangles-two-node requires a 2d cell");
+    s.nq = 4;
+    s.noff = 4;
+    s.nn = 2;
+    std::memcpy(s.offs, quad_off, sizeof(quad_off));
+    const double h0 = h[0], h1 = h[1];
+    auto tri = [&](int q, int o0, double a0, double a1, int o1, double b0, double b1, double c0, double c1) {
+      s.w[q] = vp / 4.0;
+      s.ne[q] = 3;
+      set_entry(q, 0, o0, a0, a1, 0.0);
+      set_entry(q, 1, o1, b0, b1, 0.0);
+      set_entry(q, 2, 0, c0, c1, 0.0);
+      s.node[q][2] = 1;
+    };
+    tri(0, 0, -1.0 / h0, -1.0 / h1, 1, 1.0 / h0, -1.0 / h1, 0.0, 2.0 / h1);   // bottom
+    tri(1, 1, 1.0 / h0, -1.0 / h1, 3, 1.0 / h0, 1.0 / h1, -2.0 / h0, 0.0);    // right
+    tri(2, 3, 1.0 / h0, 1.0 / h1, 2, -1.0 / h0, 1.0 / h1, 0.0, -2.0 / h1);    // top
+    tri(3, 2, -1.0 / h0, 1.0 / h1, 0, -1.0 / h0, -1.0 / h1, 2.0 / h0, 0.0);   // left
+    return s;
+  }
   throw ValidationError("stencil: invalid kind");
 }
 
