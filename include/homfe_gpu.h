@@ -158,7 +158,7 @@ int homfe_gpu_solve_state(homfe_ctx* ctx, const double* e, const homfe_solve_cfg
                           const double* warm_u, const double* g0, double* u_out, double* g_out,
                           double* avg_stress_out, homfe_report* report);
 /* NewtonOutcome::stress of the last solve (num_quads x m, quad-interleaved
-   QuadField layout, fields.hpp:40-62). Mechanical contexts. */
+   QuadField layout, fields.hpp:40-62): stress (elasticity) or flux (thermal). */
 int homfe_gpu_stress_field(homfe_ctx* ctx, double* out);
 
 /* ---- strain-based scheme and spectral bounds --------------- */

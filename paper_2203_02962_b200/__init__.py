@@ -504,6 +504,7 @@ def _report_dict(rep):
              for i in range(min(rep.n_steps, 32))]
     return dict(cause=_CAUSES[rep.cause], newton_steps=rep.n_steps, cg_total=rep.total_cg, steps=steps,
                 seconds_total=rep.seconds_total, seconds_cg=rep.seconds_cg, seconds_assembly=rep.seconds_assembly,
+                seconds_constitutive=rep.seconds_constitutive,
                 cg_device_ms=rep.cg_device_ms, assemblies=rep.assemblies, kernel_launches=rep.kernel_launches)
 
 
@@ -622,7 +623,7 @@ def newton_solve(grid, materials, phases, e, eta_newton=1e-5, eta_cg=1e-5, max_n
     Python signature of proj/src/bindings/module.cpp:299-328)."""
     s = Solver(grid, materials, phases, eta_newton, eta_cg, max_newton, max_cg, reassembly_threshold, reference,
                reference_scale, reference_matrix, criterion)
-    return s.solve(e, stress=not s.ctx.c == 1)
+    return s.solve(e, stress=True)
 
 
 def sb_newton_solve(grid, materials, phases, e, c_ref, internal=None, warm_strain=None, eta_newton=1e-5,
@@ -682,7 +683,7 @@ def run_load_program(grid, materials, phases, loads, eta_newton=1e-5, eta_cg=1e-
     g = np.zeros((grid.num_quads, 7)) if s.nonlinear else None
     warm = None
     for e in loads:
-        out = s.solve(e, warm_start=warm, internal=g)
+        out = s.solve(e, warm_start=warm, internal=g, stress=True)
         if out["converged"] and s.nonlinear:
             g = out["internal"]
         results.append(dict(load=np.asarray(e, dtype=float), **out))

@@ -1783,7 +1783,6 @@ int homfe_gpu_stress_field(homfe_ctx* c, double* out) {
     HB_CUDA(cudaSetDevice(c->device));
     require_material(c);
     if (c->dist) throw ValidationError("stress_field: single-GPU contexts only");
-    if (c->g.c == 1 && !c->sig_valid) throw ValidationError("stress_field: mechanical contexts only");
     if (!c->sig_valid) {
       // linear solve: sigma = C (e + D u) at the last solution (solver.cpp:321-324)
       ensure_nl_buffers(c);
