@@ -417,7 +417,8 @@ __device__ __forceinline__ void z_issue(const HexArgs& a, const int* its, int u,
 }
 
 template <int C, bool ISO, int KZ, bool FE, int NXT>
-__global__ void __launch_bounds__(256, C == 3 ? HB_HEXZ_MINB3 : 2) k_hex_z(const HexArgs a, const ZRun run) {
+__global__ void __launch_bounds__(NXT == 512 ? 512 : 256, NXT == 512 ? 1 : (C == 3 ? HB_HEXZ_MINB3 : 2))
+    k_hex_z(const HexArgs a, const ZRun run) {
   if (a.st && a.st->done) return;
   constexpr int MS = mat_stride<C, ISO>();
   constexpr int D = kZDepth;
@@ -723,7 +724,11 @@ __global__ void __launch_bounds__(256) k_hex_quad(const HexQArgs a) {
 }
 }  // namespace
 
-static int hex_kz(const Grid& g) { return g.c == 3 ? HB_HEXZ_KZ3 : 16; }
+// z-block depth: bounded by the per-thread row buffer (KZ x C x nx doubles)
+static int hex_kz(const Grid& g) {
+  if (g.n2 > 256) return g.c == 3 ? 4 : 8;  // 512-wide rows: one 512-thread block per SM
+  return g.c == 3 ? HB_HEXZ_KZ3 : 16;
+}
 
 static bool hex_v2(const Grid& g) {
   const char* e = std::getenv("HOMFE_HEX_V1");
@@ -750,7 +755,8 @@ bool hex_fast_eligible(const Grid& g) {
   if (g.d != 3 || g.kind != 3 || (g.c != 1 && g.c != 3)) return false;
   int ty, tz;
   hex_tile(g, ty, tz);
-  if (g.n2 % 32 != 0 || g.n2 > 256) return false;
+  if (g.n2 % 32 != 0 || g.n2 > 512 || (g.n2 > 256 && g.n2 != 512)) return false;
+  if (g.n2 == 512 && !hex_v2(g)) return false;
   if (!hex_v2(g) && (g.n1 % ty != 0 || g.n0 % tz != 0)) return false;
   if (g.h[0] != g.h[1] || g.h[1] != g.h[2]) return false;
   return true;
@@ -847,6 +853,10 @@ static void launch_hex_z_nx(const Grid& g, const HexArgs& a, int n_phases, cudaS
 
 template <int C, bool ISO, int KZ, bool FE>
 static void launch_hex_z(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
+  if (g.n2 == 512) {
+    launch_hex_z_nx<C, ISO, C == 3 ? 4 : 8, FE, 512>(g, a, n_phases, s);
+    return;
+  }
   if (g.n2 == 256) launch_hex_z_nx<C, ISO, KZ, FE, 256>(g, a, n_phases, s);
   else if (g.n2 == 128) launch_hex_z_nx<C, ISO, KZ, FE, 128>(g, a, n_phases, s);
   else launch_hex_z_nx<C, ISO, KZ, FE, 0>(g, a, n_phases, s);

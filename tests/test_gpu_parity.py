@@ -367,7 +367,8 @@ def test_hashin_coated_sphere_neutrality(hb):
 
 @pytest.mark.parametrize("dims,c,iso", [((16, 8, 32), 3, True), ((16, 8, 32), 3, False), ((32, 16, 64), 1, True),
                                         ((16, 16, 32), 1, False), ((32, 32, 32), 3, True),
-                                        ((16, 8, 256), 3, True)])
+                                        ((16, 8, 256), 3, True), ((8, 4, 512), 3, True), ((8, 4, 512), 3, False),
+                                        ((16, 4, 512), 1, True)])
 def test_hex_fast_path_matches_oracle(hb, oracle_mod, dims, c, iso, monkeypatch):
     """The element-centric modal kernel (hexfast.cu) on eligible grids, against
     the oracle and against the generic node-centric kernel."""
