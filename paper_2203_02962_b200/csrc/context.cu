@@ -112,6 +112,8 @@ struct homfe_ctx {
          *d_tpart = nullptr;
   int* d_status = nullptr;
   bool sig_valid = false;           // d_sig holds the last solve's stress
+  bool qt_ok = false;               // J2 operator on the modal hex kernel (all phases iso or J2)
+  double* d_qtab = nullptr;         // per phase (linear flag, bulk, shear)
   // impulse-probed block preconditioner (probe.cu), node types per pixel > 1
   double2* d_blocks = nullptr;      // inverted blocks (nf x b x b)
   double2* d_blocks_raw = nullptr;  // K_ref_hat before inversion (reference_blocks hook)
@@ -295,6 +297,14 @@ NLArgs nl_args(homfe_ctx* c, const double* u) {
 
 void apply_K(homfe_ctx* c, const double* u, double* out, const double* fe, double scale, double* partials,
              const PcgState* st, cudaStream_t s) {
+  if (c->nl_op && c->qt_ok && c->hex_fast) {
+    // J2 tangent operator on the modal hex kernel (per-Gauss-point compact tangents)
+    ElemArgs ea{u, nullptr, nullptr, nullptr, out, c->d_phase, c->d_ke, c->n_phases, nullptr, scale, partials, st};
+    if (launch_hex_fast_qt(c->g, ea, c->d_qtab, c->d_tanc, s)) {
+      c->launches += 1;
+      return;
+    }
+  }
   if (c->nl_op || c->g.nn > 1) {  // two node types: the quadrature-point path
     // tangent operator of the current Newton state: sigma_q = C_q (D u)_q,
     // then the weighted divergence (operators.cpp:197-257 in two passes)
@@ -1535,6 +1545,7 @@ int homfe_gpu_destroy(homfe_ctx* c) {
   for (double* b : bufs)
     if (b) cudaFree(b);
   if (c->d_models) cudaFree(c->d_models);
+  if (c->d_qtab) cudaFree(c->d_qtab);
   if (c->d_blocks) cudaFree(c->d_blocks);
   if (c->d_blocks_raw) cudaFree(c->d_blocks_raw);
   if (c->d_phase0) cudaFree(c->d_phase0);
@@ -1577,6 +1588,8 @@ int homfe_gpu_sizes(const homfe_ctx* c, int64_t* np, int64_t* nq, int32_t* m, in
 int homfe_gpu_set_material(homfe_ctx* c, int32_t n_phases, const double* t, const uint8_t* phase) {
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
+    c->nonlinear = false;
+    c->qt_ok = false;
     set_material(c, n_phases, t, phase, false);
   });
 }
@@ -1644,6 +1657,37 @@ int homfe_gpu_set_material_models(homfe_ctx* c, int32_t n_phases, const homfe_ma
     c->models = nm;
     HB_CUDA(cudaMemcpy(c->d_models, nm.data(), nm.size() * sizeof(NLModel), cudaMemcpyHostToDevice));
     c->nonlinear = nonlinear;
+    // modal-kernel table for the J2 operator: isotropic linear phases as
+    // (1, lambda + 2 mu / 3, mu), J2 phases as (0, k, G)
+    bool qt_ok = nonlinear && c->g.c == 3 && c->g.d == 3;
+    std::vector<double> qtab((size_t)n_phases * 3, 0.0);
+    for (int ph = 0; ph < n_phases && qt_ok; ++ph) {
+      if (nm[ph].kind == 1) {
+        qtab[ph * 3 + 0] = 0.0;
+        qtab[ph * 3 + 1] = nm[ph].k;
+        qtab[ph * 3 + 2] = nm[ph].g;
+        continue;
+      }
+      const double* cm = &eff[(size_t)ph * m * m];
+      auto C = [&](int i, int j) { return cm[j * m + i]; };
+      const double lam = C(0, 1), twomu = C(3, 3);
+      const double tol = 8e-16 * (std::fabs(lam) + std::fabs(twomu));
+      for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 6; ++j) {
+          const double want = (i < 3 && j < 3) ? (i == j ? lam + twomu : lam) : (i == j ? twomu : 0.0);
+          if (std::fabs(C(i, j) - want) > tol) qt_ok = false;
+        }
+      qtab[ph * 3 + 0] = 1.0;
+      qtab[ph * 3 + 1] = lam + twomu / 3.0;
+      qtab[ph * 3 + 2] = 0.5 * twomu;
+    }
+    if (const char* env = std::getenv("HOMFE_J2_FAST")) qt_ok = qt_ok && env[0] != '0';
+    if (qt_ok) {
+      if (!c->d_qtab) c->d_qtab = dalloc<double>((size_t)kMaxPhases * 3);
+      HB_CUDA(cudaMemcpy(c->d_qtab, qtab.data(), qtab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    if (qt_ok != c->qt_ok) destroy_graphs(c);
+    c->qt_ok = qt_ok;
   });
 }
 

@@ -162,6 +162,72 @@ def gen_fold(elastic, iso):
     return "\n".join(out)
 
 
+def gen_qt():
+    """Per-Gauss-point tangents (J2 consistent tangents, compact form
+    C_q = 3k V + 2G a Dev - b n n^T): modal strain rows -> strain at the 8
+    Gauss points (sign patterns of the quad modes) -> stress -> projected
+    back onto the modes -> residual contributions (same incidence as the
+    linear mode code). Inputs V[k][v], qs[6] (mode scale x Mandel factor),
+    qw[6] (= w qs), kq, gq (phase bulk / shear), lin (no per-point tangent),
+    tq (8 x 8 compact tangents of this element)."""
+    out = []
+    terms = {}  # (md, row) -> raw expression
+    for md, inc in enumerate(INC3):
+        for e in sorted({e for e, _, _ in inc}):
+            terms[(md, e)] = " + ".join(f"V[{k}][{v}]" for (ee, k, v) in inc if ee == e)
+    out.append("  {")
+    for (md, e), expr in terms.items():
+        idx = CLASS[md] * 2 + (1 if e >= 3 else 0)
+        out.append(f"    const double E{md}_{e} = qs[{idx}] * ({expr});")
+    for (md, e) in terms:
+        out.append(f"    double S{md}_{e} = 0.0;")
+    # quad sign patterns: mode name letters per axis (0, 1, 2)
+    for q in range(8):
+        i, j, k = (q >> 2) & 1, (q >> 1) & 1, q & 1
+        sg = [1 if i else -1, 1 if j else -1, 1 if k else -1]
+
+        def phi(md):
+            v = 1
+            for a, ch in enumerate(MODES[md]):
+                if ch == "a":
+                    v *= sg[a]
+            return v
+        out.append(f"    {{  /* Gauss point ({i},{j},{k}) */")
+        for r in range(6):
+            parts = []
+            for (md, e) in terms:
+                if e != r:
+                    continue
+                parts.append(("+" if phi(md) > 0 else "-") + f" E{md}_{e}")
+            expr = " ".join(parts).lstrip("+ ").strip()
+            if expr.startswith("- "):
+                expr = "-" + expr[2:]
+            out.append(f"      const double ep{r} = {expr if expr else '0.0'};")
+        out.append("      double ca = 1.0, cb = 0.0, n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0, n4 = 0.0, n5 = 0.0;")
+        out.append(f"      if (!lin) {{ const double* t = tq + {q * 8}; ca = t[0]; cb = t[1]; n0 = t[2]; n1 = t[3]; "
+                   "n2 = t[4]; n3 = t[5]; n4 = t[6]; n5 = t[7]; }")
+        out.append("      const double tr = ep0 + ep1 + ep2, t3 = tr * (1.0 / 3.0);")
+        out.append("      const double ne = n0 * ep0 + n1 * ep1 + n2 * ep2 + n3 * ep3 + n4 * ep4 + n5 * ep5;")
+        out.append("      const double g2 = 2.0 * gq * ca, kt = kq * tr, bn = cb * ne;")
+        for r in range(6):
+            if r < 3:
+                out.append(f"      const double sg{r} = fma(g2, ep{r} - t3, kt) - bn * n{r};")
+            else:
+                out.append(f"      const double sg{r} = fma(g2, ep{r}, -bn * n{r});")
+        for (md, e) in terms:
+            out.append(f"      S{md}_{e} {'+' if phi(md) > 0 else '-'}= sg{e};")
+        out.append("    }")
+    for (md, e) in terms:
+        idx = CLASS[md] * 2 + (1 if e >= 3 else 0)
+        out.append(f"    {{ const double tt = qw[{idx}] * S{md}_{e};")
+        for (ee, k, v) in INC3[md]:
+            if ee == e:
+                out.append(f"      HB_ACC({k}, {v}, tt);")
+        out.append("    }")
+    out.append("  }")
+    return "\n".join(out)
+
+
 def gen_norm(elastic):
     """sum_q |eps_q + E|^2 / (8 w) over the quad modes (orthogonal patterns):
     mode m contributes sum_rows (sc * e_row (+ E_row for sss))^2, with
@@ -203,6 +269,7 @@ def main():
                        ("SCALAR_ISO", gen_scalar(True)), ("SCALAR_GEN", gen_scalar(False)),
                        ("FOLD_ELASTIC_ISO", gen_fold(True, True)), ("FOLD_ELASTIC_GEN", gen_fold(True, False)),
                        ("FOLD_SCALAR_ISO", gen_fold(False, True)), ("FOLD_SCALAR_GEN", gen_fold(False, False)),
+                       ("QT_ELASTIC", gen_qt()),
                        ("NRM_ELASTIC", gen_norm(True)), ("NRM_SCALAR", gen_norm(False)),
                        ("SSS_ELASTIC", gen_sss(True)), ("SSS_SCALAR", gen_sss(False))):
         if name != "ELASTIC_ISO":

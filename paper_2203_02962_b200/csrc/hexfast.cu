@@ -160,6 +160,10 @@ struct HexArgs {
   const PcgState* st;
   int n0, n1, n2;
   int tiles_y, tiles_z;
+  // per-Gauss-point tangents (J2 path): compact (a, b, n[6]) per point,
+  // mat = per phase (linear flag, bulk, shear); qs / qw mode scales
+  const double* tanc;
+  double qs[6], qw[6];
 };
 
 template <int C, bool ISO, int kTY, int kTZ>
@@ -416,11 +420,11 @@ __device__ __forceinline__ void z_issue(const HexArgs& a, const int* its, int u,
   }
 }
 
-template <int C, bool ISO, int KZ, bool FE, int NXT>
-__global__ void __launch_bounds__(NXT == 512 ? 512 : 256, NXT == 512 ? 1 : (C == 3 ? HB_HEXZ_MINB3 : 2))
+template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT = false>
+__global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1 : (C == 3 ? HB_HEXZ_MINB3 : 2))
     k_hex_z(const HexArgs a, const ZRun run) {
   if (a.st && a.st->done) return;
-  constexpr int MS = mat_stride<C, ISO>();
+  constexpr int MS = QT ? 3 : mat_stride<C, ISO>();
   constexpr int D = kZDepth;
   extern __shared__ __align__(16) unsigned char zsm[];
   const int nx = NXT ? NXT : blockDim.x;  // == n2 (compile-time for the common sizes: immediate smem offsets)
@@ -518,7 +522,22 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, NXT == 512 ? 1 : (C ==
 #pragma unroll
           for (int m = 0; m < 4; ++m) A[k][m] = zc[k][m];
         const double* mat = matp + ph * MS;
-        if constexpr (C == 3) {
+        if constexpr (QT && C == 3) {
+#pragma unroll
+          for (int k = 0; k < C; ++k)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) B[k][m] = 0.0;
+          const bool lin = mat[0] != 0.0;
+          const double kq = mat[1], gq = mat[2];
+          int ze = zb * KZ - 2 + j;
+          ze = ze < 0 ? ze + a.n0 : ze;
+          const double* tq = a.tanc + (((int64_t)ze * a.n1 + y) * nx + x) * 64;
+          const double* qs = a.qs;
+          const double* qw = a.qw;
+#define HB_ACC(k, v, t) acc_fold<v>(A[k], B[k], (t))
+          HB_HEX_MODES_QT_ELASTIC
+#undef HB_ACC
+        } else if constexpr (C == 3) {
           if constexpr (ISO) {
             HB_HEX_MODES_FOLD_ELASTIC_ISO
           } else {
@@ -815,9 +834,9 @@ bool hex_fast_tables(const Grid& g, int n_phases, const double* cmats, std::vect
   return all_iso;
 }
 
-template <int C, bool ISO, int KZ, bool FE, int NXT>
+template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT = false>
 static void launch_hex_z_nx(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
-  constexpr int MS = mat_stride<C, ISO>();
+  constexpr int MS = QT ? 3 : mat_stride<C, ISO>();
   const int nx = g.n2, nw = nx / 32;
   const int rows_total = g.n1 * (g.n0 / KZ);
   auto smem_for = [&](int grid) {
@@ -835,20 +854,20 @@ static void launch_hex_z_nx(const Grid& g, const HexArgs& a, int n_phases, cudaS
     HB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   size_t smem = smem_for(2 * sms);
-  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hex_z<C, ISO, KZ, FE, NXT>, nx, smem));
+  HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hex_z<C, ISO, KZ, FE, NXT, QT>, nx, smem));
   if (per_sm < 1) per_sm = 1;
   int grid = per_sm * sms;
   if (grid > rows_total) grid = rows_total;
   if (grid > kRedBlocks) grid = kRedBlocks;
   smem = smem_for(grid);
-  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ZRun run;
   run.rows_total = rows_total;
   run.grid = grid;
   run.list_cap = 2 * ((rows_total + grid - 1) / grid) + 4;
-  k_hex_z<C, ISO, KZ, FE, NXT><<<grid, nx, smem, s>>>(a, run);
+  k_hex_z<C, ISO, KZ, FE, NXT, QT><<<grid, nx, smem, s>>>(a, run);
 }
 
 template <int C, bool ISO, int KZ, bool FE>
@@ -961,6 +980,44 @@ bool launch_hex_quad(const Grid& g, int mode, const double* u, const double* hal
     if (g.c == 3) k_hex_quad<3, true><<<kRedBlocks, 256, 0, s>>>(a);
     else k_hex_quad<1, true><<<kRedBlocks, 256, 0, s>>>(a);
   }
+  HB_CUDA(cudaGetLastError());
+  return true;
+}
+
+// K u with per-Gauss-point compact tangents (J2 Newton path, C = 3): the
+// z-march kernel with the mode contraction replaced by strain at the 8 Gauss
+// points, the compact consistent tangent and the projection back onto the
+// modes. qtab: per phase (linear flag, bulk, shear).
+bool launch_hex_fast_qt(const Grid& g, const ElemArgs& ea, const double* d_qtab, const double* d_tanc,
+                        cudaStream_t s) {
+  if (!hex_fast_eligible(g) || g.c != 3 || !hex_v2(g) || g.dist) return false;
+  HexArgs a{};
+  a.u = ea.u;
+  a.dist = 0;
+  a.out = ea.out;
+  a.phase = ea.phase;
+  a.mat = d_qtab;
+  a.fe = nullptr;
+  a.n_phases = ea.n_phases;
+  a.scale = ea.scale;
+  a.partials = ea.partials;
+  a.nred = kRedBlocks;
+  a.st = ea.st;
+  a.n0 = g.n0;
+  a.n1 = g.n1;
+  a.n2 = g.n2;
+  a.tanc = d_tanc;
+  const double h = g.h[0], r2 = 0.70710678118654752440, w = h * h * h / 8.0;
+  const double s0 = 1.0 / (4.0 * h), s1 = 1.0 / (4.0 * std::sqrt(3.0) * h), s2 = 1.0 / (12.0 * h);
+  const double qs[6] = {s0, s0 * r2, s1, s1 * r2, s2, s2 * r2};
+  for (int i = 0; i < 6; ++i) {
+    a.qs[i] = qs[i];
+    a.qw[i] = w * qs[i];
+  }
+  if (g.n2 == 512) launch_hex_z_nx<3, true, 4, false, 512, true>(g, a, ea.n_phases, s);
+  else if (g.n2 == 256) launch_hex_z_nx<3, true, HB_HEXZ_KZ3, false, 256, true>(g, a, ea.n_phases, s);
+  else if (g.n2 == 128) launch_hex_z_nx<3, true, HB_HEXZ_KZ3, false, 128, true>(g, a, ea.n_phases, s);
+  else launch_hex_z_nx<3, true, HB_HEXZ_KZ3, false, 0, true>(g, a, ea.n_phases, s);
   HB_CUDA(cudaGetLastError());
   return true;
 }

@@ -77,6 +77,9 @@ void launch_probe_store(const double2* spec, int b, int64_t nf, int col, double2
 void launch_probe_invert(double2* blocks, int64_t nf, int b, int nn, int* status, cudaStream_t s);
 void launch_probe_apply(double2* spec, const double2* blocks, int64_t nf, int b, double scale, cudaStream_t s);
 void launch_phase_counts(const uint8_t* ph, int64_t n, unsigned long long* counts, cudaStream_t s);
+// J2 path: K u with per-Gauss-point compact tangents (false if not eligible)
+bool launch_hex_fast_qt(const Grid& g, const ElemArgs& a, const double* d_qtab, const double* d_tanc,
+                        cudaStream_t s);
 // mode 0: sum_q w |D u + e|^2 / h^3 (1 partial per block); 1: sum_q w C (D u + e) / h^3 (m per block)
 bool launch_hex_quad(const Grid& g, int mode, const double* u, const double* halo_hi, const double* e,
                      const uint8_t* phase, const double* cmat, double* partials, cudaStream_t s);

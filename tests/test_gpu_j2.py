@@ -75,6 +75,30 @@ def test_j2_hex_mixed_catalog_matches_oracle(hb, oracle_mod):
     assert np.abs(got["internal"] - oi).max() <= 1e-9 * max(np.abs(oi).max(), 1e-30)
 
 
+@pytest.mark.parametrize("fast", ["1", "0"])
+def test_j2_hex_modal_operator_matches_oracle(hb, oracle_mod, fast, monkeypatch):
+    """Hex grid eligible for the modal kernel: the J2 tangent operator runs on
+    the z-march kernel with per-Gauss-point compact tangents (fast = 1) or on
+    the generic two-pass path (0); both against the oracle."""
+    monkeypatch.setenv("HOMFE_J2_FAST", fast)
+    c0 = hb.isotropic_stiffness(1.0, 0.6, 3)
+    gpu = [hb.Material.linear_elastic(c0), hb.Material.j2_plastic(2.0, 1.2, 4e-3, 0.1, 3)]
+    orc = [oracle_mod.material("linear", c0), oracle_mod.material("j2", bulk=2.0, shear=1.2, yield_stress=4e-3,
+                                                                  hardening=0.1)]
+    dims = (16, 8, 32)
+    ph = (oracle_mod.uniform(98, 16 * 8 * 32, 0.0, 1.0) < 0.4).astype(np.uint8)
+    e = np.array([4e-3, -1e-3, 0.0, 0.0, 2e-3, 3e-3])
+    got, ref = _pair(hb, oracle_mod, dims, "trilinear-hex", gpu, orc, ph, e, eta_newton=1e-10, eta_cg=1e-12)
+    assert got["converged"] and ref["converged"]
+    assert len(got["report"]["steps"]) == len(ref["steps"])
+    assert all(abs(a["cg_iterations"] - b["cg_iterations"]) <= 1 for a, b in zip(got["report"]["steps"], ref["steps"]))
+    assert _rel(got["u"], ref["u"]) < 1e-8
+    assert _rel(got["average_stress"], ref["average_stress"]) < 1e-9
+    oi = ref["internal"].reshape(-1, 7)
+    assert oi[:, 6].max() > 0.0
+    assert np.abs(got["internal"] - oi).max() <= 1e-9 * np.abs(oi).max()
+
+
 def test_j2_load_program_commits_state(hb, oracle_mod):
     """run_load_program (solver.cpp:298-319): warm start + committed state."""
     gpu, orc = _j2_pair(hb, oracle_mod, 2, [(1.0, 0.5, 1e-3, 0.05), (10.0, 5.0, 2e-3, 0.5)])
