@@ -10,6 +10,9 @@
 #include <cufft.h>
 #include <nccl.h>
 #include <cub/cub.cuh>
+#include <condition_variable>
+#include <mutex>
+#include <map>
 
 #include <algorithm>
 #include <random>
@@ -83,6 +86,15 @@ T* dalloc(size_t n) {
 
 }  // namespace
 
+struct SimGroup {
+  int world = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0, generation = 0;
+  std::vector<const void*> ptr;      // per rank: published buffer
+  std::vector<double> red;           // per rank: reduction staging (<= 256 values)
+  std::vector<uint64_t> ured;
+};
 struct homfe_ctx {
   int device = 0;
   Grid g{};
@@ -159,6 +171,7 @@ struct homfe_ctx {
   // slab decomposition (homfe_gpu_create_dist): NCCL communicator, halo planes
   bool dist = false;
   ncclComm_t comm = nullptr;
+  SimGroup* sim = nullptr;          // in-process slab transport (tests on one GPU), see sim_*
   double* d_hlo = nullptr;          // plane z0-1 of the vector being stenciled, [c][plane]
   double* d_hhi = nullptr;          // plane z0+nz
   uint8_t* d_ph_lo = nullptr;       // phase plane z0-1
@@ -183,12 +196,101 @@ void destroy_graphs(homfe_ctx* c) {
 
 void sync(homfe_ctx* c) { HB_CUDA(cudaStreamSynchronize(c->stream)); }
 
+// ---- in-process slab transport (tests) ------------------------------------
+// W contexts of one process on one device, driven by W host threads, with the
+// collectives done as device-to-device copies between host barriers. The
+// kernels never wait on each other on the device (all waiting is on the
+// host), so this validates the slab layouts, halos and reduction order of
+// the multi-GPU path on one GPU. Selected by an id blob starting "HBSIMGRP".
+static std::mutex g_sim_mu;
+static std::map<uint64_t, std::shared_ptr<SimGroup>> g_sim;
+
+void sim_barrier(SimGroup* g) {
+  std::unique_lock<std::mutex> lk(g->m);
+  const int gen = g->generation;
+  if (++g->arrived == g->world) {
+    g->arrived = 0;
+    ++g->generation;
+    g->cv.notify_all();
+  } else {
+    g->cv.wait(lk, [&] { return g->generation != gen; });
+  }
+}
+
+// publish my pointer, wait for everyone, run `body` (pulls from peers), wait again
+template <class F>
+void sim_exchange(homfe_ctx* c, const void* mine, F body) {
+  SimGroup* G = c->sim;
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  G->ptr[c->g.rank] = mine;
+  sim_barrier(G);
+  body(G);
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  sim_barrier(G);
+}
+
+void sim_halo(homfe_ctx* c, const void* v, size_t elem, int comps, int64_t comp_stride, void* lo, void* hi) {
+  const Grid& g = c->g;
+  const int prev = (g.rank - 1 + g.world) % g.world, next = (g.rank + 1) % g.world;
+  const size_t plane = (size_t)g.n1 * g.n2;
+  sim_exchange(c, v, [&](SimGroup* G) {
+    for (int k = 0; k < comps; ++k) {
+      const char* pv = static_cast<const char*>(G->ptr[prev]) + (size_t)k * comp_stride * elem;
+      const char* nx = static_cast<const char*>(G->ptr[next]) + (size_t)k * comp_stride * elem;
+      if (lo)
+        HB_CUDA(cudaMemcpyAsync(static_cast<char*>(lo) + k * plane * elem, pv + (size_t)(g.n0 - 1) * plane * elem,
+                                plane * elem, cudaMemcpyDeviceToDevice, c->stream));
+      if (hi)
+        HB_CUDA(cudaMemcpyAsync(static_cast<char*>(hi) + k * plane * elem, nx, plane * elem,
+                                cudaMemcpyDeviceToDevice, c->stream));
+    }
+  });
+}
+
+void sim_all_to_all(homfe_ctx* c, const double2* send, double2* recv, int64_t chunk) {
+  sim_exchange(c, send, [&](SimGroup* G) {
+    for (int q = 0; q < c->g.world; ++q)
+      HB_CUDA(cudaMemcpyAsync(recv + q * chunk, static_cast<const double2*>(G->ptr[q]) + (int64_t)c->g.rank * chunk,
+                              chunk * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+// sum over ranks in rank order (a fixed order, like NCCL's for a given communicator)
+template <class T>
+void sim_allreduce(homfe_ctx* c, T* dptr, int n) {
+  SimGroup* G = c->sim;
+  std::vector<T> mine(n);
+  HB_CUDA(cudaMemcpyAsync(mine.data(), dptr, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+  {
+    std::lock_guard<std::mutex> lk(G->m);
+    for (int i = 0; i < n; ++i) {
+      if constexpr (std::is_same<T, double>::value) G->red[(size_t)c->g.rank * 256 + i] = mine[i];
+      else G->ured[(size_t)c->g.rank * 256 + i] = mine[i];
+    }
+  }
+  sim_barrier(G);
+  std::vector<T> tot(n, T(0));
+  for (int r = 0; r < G->world; ++r)
+    for (int i = 0; i < n; ++i) {
+      if constexpr (std::is_same<T, double>::value) tot[i] += G->red[(size_t)r * 256 + i];
+      else tot[i] += G->ured[(size_t)r * 256 + i];
+    }
+  sim_barrier(G);
+  HB_CUDA(cudaMemcpyAsync(dptr, tot.data(), n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+  HB_CUDA(cudaStreamSynchronize(c->stream));
+}
+
 // ---- slab-mode exchanges (NCCL over NVLink / NVSwitch) --------------------
 // halo planes of a component-planar vector: my first plane goes to the
 // previous rank (its upper halo), my last plane to the next rank (its lower
 // halo); periodic ring, so world == 1 exchanges with itself.
 void exchange_halo(homfe_ctx* c, const double* v, cudaStream_t s) {
   const Grid& g = c->g;
+  if (c->sim) {
+    sim_halo(c, v, sizeof(double), g.c, g.np, c->d_hlo, c->d_hhi);
+    return;
+  }
   const int prev = (g.rank - 1 + g.world) % g.world, next = (g.rank + 1) % g.world;
   const size_t plane = (size_t)g.n1 * g.n2;
   HB_NCCL(ncclGroupStart());
@@ -209,6 +311,10 @@ void all_to_all(homfe_ctx* c, const double2* send, double2* recv, int64_t chunk,
       HB_CUDA(cudaMemcpyAsync(recv, send, chunk * sizeof(double2), cudaMemcpyDeviceToDevice, s));
     return;
   }
+  if (c->sim) {
+    sim_all_to_all(c, send, recv, chunk);
+    return;
+  }
   HB_NCCL(ncclGroupStart());
   for (int q = 0; q < c->g.world; ++q) {
     HB_NCCL(ncclSend(send + q * chunk, 2 * chunk, ncclDouble, q, c->comm, s));
@@ -221,7 +327,8 @@ void all_to_all(homfe_ctx* c, const double2* send, double2* recv, int64_t chunk,
 // ranks (NCCL's fixed ring/tree order: identical on every rank and run).
 double* reduce_global(homfe_ctx* c, int nvals, int slot, cudaStream_t s) {
   launch_final_sum(c->d_partials, kRedBlocks, nvals, c->d_red + slot, s);
-  HB_NCCL(ncclAllReduce(c->d_red + slot, c->d_red + slot, nvals, ncclDouble, ncclSum, c->comm, s));
+  if (c->sim) sim_allreduce<double>(c, c->d_red + slot, nvals);
+  else HB_NCCL(ncclAllReduce(c->d_red + slot, c->d_red + slot, nvals, ncclDouble, ncclSum, c->comm, s));
   return c->d_red + slot;
 }
 
@@ -706,7 +813,8 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
   std::vector<int64_t> counts(256, 0);
   if (c->dist) {
     // global phase counts (volume-mean reference) over the slabs
-    HB_NCCL(ncclAllReduce(c->d_red, c->d_red, 256, ncclUint64, ncclSum, c->comm, c->stream));
+    if (c->sim) sim_allreduce<uint64_t>(c, reinterpret_cast<uint64_t*>(c->d_red), 256);
+    else HB_NCCL(ncclAllReduce(c->d_red, c->d_red, 256, ncclUint64, ncclSum, c->comm, c->stream));
   }
   HB_CUDA(cudaMemcpyAsync(counts.data(), c->d_red, 256 * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
@@ -724,10 +832,14 @@ void set_material(homfe_ctx* c, int n_phases, const double* tangents, const uint
     const Grid& g = c->g;
     const int prev = (g.rank - 1 + g.world) % g.world, next = (g.rank + 1) % g.world;
     const size_t plane = (size_t)g.n1 * g.n2;
-    HB_NCCL(ncclGroupStart());
-    HB_NCCL(ncclSend(c->d_phase + (int64_t)(g.n0 - 1) * plane, plane, ncclUint8, next, c->comm, c->stream));
-    HB_NCCL(ncclRecv(c->d_ph_lo, plane, ncclUint8, prev, c->comm, c->stream));
-    HB_NCCL(ncclGroupEnd());
+    if (c->sim) {
+      sim_halo(c, c->d_phase, 1, 1, 0, c->d_ph_lo, nullptr);
+    } else {
+      HB_NCCL(ncclGroupStart());
+      HB_NCCL(ncclSend(c->d_phase + (int64_t)(g.n0 - 1) * plane, plane, ncclUint8, next, c->comm, c->stream));
+      HB_NCCL(ncclRecv(c->d_ph_lo, plane, ncclUint8, prev, c->comm, c->stream));
+      HB_NCCL(ncclGroupEnd());
+    }
   }
   // per-phase tables in buffers sized for the full catalog (stable pointers:
   // captured graphs stay valid unless the kernel configuration changes)
@@ -1377,9 +1489,26 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     HB_CUDA(cudaEventCreate(&ctx->ev0));
     HB_CUDA(cudaEventCreate(&ctx->ev1));
     if (dist) {
-      ncclUniqueId id;
-      std::memcpy(&id, nccl_id, sizeof(id));
-      HB_NCCL(ncclCommInitRank(&ctx->comm, world, id, rank));
+      if (std::memcmp(nccl_id, "HBSIMGRP", 8) == 0) {
+        uint64_t gid = 0;
+        std::memcpy(&gid, static_cast<const char*>(nccl_id) + 8, 8);
+        std::lock_guard<std::mutex> lk(g_sim_mu);
+        auto& grp = g_sim[gid];
+        if (!grp) {
+          grp = std::make_shared<SimGroup>();
+          grp->world = world;
+          grp->ptr.assign(world, nullptr);
+          grp->red.assign((size_t)world * 256, 0.0);
+          grp->ured.assign((size_t)world * 256, 0);
+        }
+        if (grp->world != world) throw ValidationError("slab sim: world mismatch");
+        ctx->sim = grp.get();
+        ctx->body_eager = true;  // host barriers cannot be captured
+      } else {
+        ncclUniqueId id;
+        std::memcpy(&id, nccl_id, sizeof(id));
+        HB_NCCL(ncclCommInitRank(&ctx->comm, world, id, rank));
+      }
       const size_t plane = (size_t)g.n1 * g.n2;
       ctx->d_hlo = dalloc<double>(c * plane);
       ctx->d_hhi = dalloc<double>(c * plane);

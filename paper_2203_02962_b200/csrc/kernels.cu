@@ -93,7 +93,9 @@ __global__ void __launch_bounds__(kBlock) k_apply_elem(const Grid g, const ElemA
         a0 = e & 1; a1 = (e >> 1) & 1;
       }
       const int64_t eidx = flat(w0[1 - a0], w1[1 - a1], w2[1 - a2]);
-      const int ph = a.phase[eidx];
+      // slab mode: the element below plane 0 lives on the previous rank
+      const bool elo = D == 3 && g.dist && c0 - a0 < 0;
+      const int ph = elo ? a.ph_lo[(int64_t)w1[1 - a1] * g.n2 + w2[1 - a2]] : a.phase[eidx];
       const double* row = ke + (size_t)ph * NE * NE + (size_t)(e * C) * NE;
 #pragma unroll
       for (int j = 0; j < NL; ++j) {
@@ -104,9 +106,20 @@ __global__ void __launch_bounds__(kBlock) k_apply_elem(const Grid g, const ElemA
           b0 = j & 1; b1 = (j >> 1) & 1;
         }
         const int64_t nidx = flat(w0[1 - a0 + b0], w1[1 - a1 + b1], w2[1 - a2 + b2]);
+        // slab mode: node planes -1 / n0 come from the halo planes ([c][plane])
+        const double* ub = a.u;
+        int64_t cs = np, ni = nidx;
+        if (D == 3 && g.dist) {
+          const int z = c0 - a0 + b0;
+          if (z < 0 || z >= g.n0) {
+            ub = z < 0 ? a.halo_lo : a.halo_hi;
+            cs = (int64_t)g.n1 * g.n2;
+            ni = (int64_t)w1[1 - a1 + b1] * g.n2 + w2[1 - a2 + b2];
+          }
+        }
 #pragma unroll
         for (int cj = 0; cj < C; ++cj) {
-          const double v = __ldg(a.u + cj * np + nidx);
+          const double v = __ldg(ub + cj * cs + ni);
 #pragma unroll
           for (int ci = 0; ci < C; ++ci) acc[ci] = fma(row[ci * NE + j * C + cj], v, acc[ci]);
         }

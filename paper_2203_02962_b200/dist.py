@@ -72,6 +72,13 @@ def nccl_unique_id():
     return bytes(buf)
 
 
+def sim_group_id(group):
+    """Id blob selecting the in-process slab transport (host barriers and
+    device-to-device copies between the W contexts of one process on one
+    GPU): validates the multi-rank layouts without NCCL. Test use only."""
+    return b"HBSIMGRP" + int(group).to_bytes(8, "little") + bytes(112)
+
+
 class SlabContext:
     """Device context for one slab (wraps homfe_gpu_create_dist)."""
 

@@ -49,3 +49,68 @@ def test_slab_world1_matches_single_device(hb, dims, c):
     assert out["report"]["steps"][0]["cg_iterations"] == ref["report"]["steps"][0]["cg_iterations"]
     assert _rel(out["u"], ref["u"]) < 1e-12
     assert _rel(out["average_stress"], ref["average_stress"]) < 1e-12
+
+
+@pytest.mark.parametrize("world,dims,c", [(2, (64, 128, 128), 3), (2, (128, 128, 128), 3), (4, (128, 128, 128), 1), (8, (128, 256, 256), 3)])
+def test_slab_multi_rank_in_process_matches_single_device(hb, world, dims, c):
+    """World > 1 on one GPU through the in-process transport (host barriers +
+    device copies instead of NCCL; no device-side waiting between ranks): the
+    halo ring, both peer-chunk transposes of the fused passes, the pencil
+    frequency offsets and the rank-ordered reductions against the
+    single-device context."""
+    import threading
+    from paper_2203_02962_b200 import dist, inputs
+    ph, _ = inputs.rsa_balls(dims, radius=6.0, seed=5, fraction=0.25)
+    if c == 1:
+        cm = np.stack([np.eye(3), 100.0 * np.eye(3)])
+        e = [1.0, 0.0, 0.0]
+    else:
+        cm = np.stack([hb.isotropic_stiffness(0.8333, 0.3846, 3), hb.isotropic_stiffness(555.5, 416.7, 3)])
+        e = [0, 0, 0, 0, 0, np.sqrt(2.0) * 0.01]
+    g = hb.Grid(dims, [1.0, 1.0, 1.0], "trilinear-hex")
+    mats = [hb.Material(t, c == 1, 3) for t in cm]
+    single = hb.Solver(g, mats, ph, eta_cg=1e-6, reference="explicit", reference_matrix=cm[0])
+    ref = single.solve(e)
+    rng = np.random.default_rng(2)
+    u = rng.uniform(-1, 1, (c, g.num_nodes))
+    ku_ref = hb.apply_operator(g, cm[np.repeat(ph, 8)], u)
+    r = u - u.mean(axis=1, keepdims=True)
+    z_ref = hb.apply_preconditioner(g, hb.assemble_preconditioner(g, cm[0], c), r)
+    plane = dims[1] * dims[2]
+    gid = 1000 + world * 10 + c
+    res = [None] * world
+    errors = []
+
+    def rank_main(rank):
+        try:
+            sc = dist.SlabContext(g, c, rank, world, dist.sim_group_id(gid))
+            z0, nz = sc.z0, sc.nz
+            sl = slice(z0 * plane, (z0 + nz) * plane)
+            sc.set_material(cm, ph[sl])
+            ku = sc.apply_K(u[:, sl])
+            sc.set_reference(cm[0])
+            z = sc.apply_minv(r[:, sl])
+            out = sc.solve(e, single.cfg)
+            res[rank] = (sl, ku, z, out)
+        except Exception as ex:  # noqa: BLE001
+            errors.append(repr(ex))
+
+    threads = [threading.Thread(target=rank_main, args=(k,)) for k in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not errors, errors
+    ku = np.zeros_like(u)
+    z = np.zeros_like(u)
+    uu = np.zeros_like(u)
+    for sl, kl, zl, out in res:
+        ku[:, sl], z[:, sl], uu[:, sl] = kl, zl, out["u"]
+    assert _rel(ku, ku_ref) < 1e-15, _rel(ku, ku_ref)
+    np.testing.assert_array_equal(ku, ku_ref)
+    assert _rel(z, z_ref) < 1e-13, _rel(z, z_ref)
+    for sl, kl, zl, out in res:
+        assert out["converged"]
+        assert out["report"]["steps"][0]["cg_iterations"] == ref["report"]["steps"][0]["cg_iterations"]
+        assert _rel(out["average_stress"], ref["average_stress"]) < 1e-12
+    assert _rel(uu, ref["u"]) < 1e-11
