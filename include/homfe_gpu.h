@@ -114,6 +114,11 @@ int homfe_gpu_destroy(homfe_ctx* ctx);
 int homfe_nccl_unique_id(void* out128);
 int homfe_gpu_create_dist(const homfe_grid_desc* desc, int32_t rank, int32_t world, const void* nccl_id,
                           homfe_ctx** out);
+/* Slab transport in use: 0 single device (or world 1), 1 all-to-all + halo
+   sends (NCCL, HOMFE_P2P=0), 2 peer pull (passes 2/3 and the K halo read
+   the peers' fields over NVLink; stream barriers only). No reference
+   counterpart (the reference is single-process). */
+int homfe_gpu_slab_transport(const homfe_ctx* ctx, int32_t* kind);
 
 /* MaterialMap for linear models (material.hpp:100-118): per-phase m x m
    column-major tangents (conductivity d x d, or Mandel stiffness) and the

@@ -78,6 +78,7 @@ def _load():
         "homfe_gpu_kernel_times": (C.c_int, [vp, i32, P(d)]),
         "homfe_nccl_unique_id": (C.c_int, [vp]),
         "homfe_gpu_create_dist": (C.c_int, [P(GridDesc), i32, i32, vp, P(vp)]),
+        "homfe_gpu_slab_transport": (C.c_int, [vp, P(i32)]),
         "homfe_random_normal": (C.c_int, [C.c_uint64, i64, P(d)]),
         "homfe_gpu_set_material_models": (C.c_int, [vp, i32, P(MaterialModel), P(C.c_uint8)]),
         "homfe_gpu_internal_width": (C.c_int, [vp, P(i32), P(i64)]),
@@ -102,6 +103,6 @@ EXPORTED = ("homfe_gpu_last_error", "homfe_isotropic_stiffness", "homfe_gpu_crea
             "homfe_gpu_reference_blocks", "homfe_gpu_gradient", "homfe_gpu_divergence",
             "homfe_gpu_volume_average", "homfe_gpu_pcg", "homfe_gpu_index_maps", "homfe_gpu_sizes",
             "homfe_random_uniform", "homfe_random_normal", "homfe_gpu_kernel_times",
-            "homfe_nccl_unique_id", "homfe_gpu_create_dist", "homfe_gpu_set_material_models",
+            "homfe_nccl_unique_id", "homfe_gpu_create_dist", "homfe_gpu_slab_transport", "homfe_gpu_set_material_models",
             "homfe_gpu_internal_width", "homfe_gpu_solve_state", "homfe_gpu_stress_field",
             "homfe_gpu_gamma_apply", "homfe_gpu_sb_solve", "homfe_gpu_eigenvalue_bounds")

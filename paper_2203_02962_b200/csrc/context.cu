@@ -178,6 +178,13 @@ struct homfe_ctx {
   double* d_red = nullptr;          // globally reduced scalars
   double2* d_spec_r = nullptr;      // all-to-all receive buffers of the fused passes
   double2* d_spec2_r = nullptr;
+  // peer pull (slab mode over NVLink): passes 2 / 3 and the K halo planes read
+  // the peers' fields in place (IPC mappings, or the in-process transport's
+  // own pointers); the all-to-alls and halo sends become stream barriers
+  bool peer = false;
+  double* peer_p[FusedFft::kMaxPeers] = {};  // every rank's p (d_p)
+  std::vector<void*> ipc_open;               // IPC mappings to close
+  double* d_bar = nullptr;                   // barrier all-reduce scratch
 
   int64_t nvec() const { return (int64_t)g.c * g.nn * g.np; }
   int64_t nodes() const { return (int64_t)g.nn * g.np; }
@@ -323,6 +330,34 @@ void all_to_all(homfe_ctx* c, const double2* send, double2* recv, int64_t chunk,
   HB_NCCL(ncclGroupEnd());
 }
 
+// Stream barrier over the slab ranks: on return (in stream order) every
+// rank's preceding work is complete. NCCL: a 1-element all-reduce (its
+// completion needs every rank's contribution, queued after that rank's
+// preceding kernels); in-process: host barrier after a stream drain.
+void peer_barrier(homfe_ctx* c, cudaStream_t s) {
+  if (c->sim) {
+    HB_CUDA(cudaStreamSynchronize(s));
+    sim_barrier(c->sim);
+    return;
+  }
+  HB_NCCL(ncclAllReduce(c->d_bar, c->d_bar, 1, ncclDouble, ncclSum, c->comm, s));
+}
+
+// pass 1 -> pass 2: all-to-all of T, or (peer pull) a barrier after which
+// pass 2 reads every peer's T chunk for this rank over NVLink
+void xfer_t(homfe_ctx* c, cudaStream_t s) {
+  if (c->peer) peer_barrier(c, s);
+  else all_to_all(c, c->ff.T, c->ff.Trecv, c->ff.chunk_t(), s);
+}
+// pass 2 -> pass 3; `synced`: an all-reduce was queued after pass 2 already
+void xfer_t2(homfe_ctx* c, cudaStream_t s, bool synced) {
+  if (c->peer) {
+    if (!synced) peer_barrier(c, s);
+  } else {
+    all_to_all(c, c->ff.T2, c->ff.T2recv, c->ff.chunk_t2(), s);
+  }
+}
+
 // partials -> d_red[slot..slot+n): fixed-order local sum, then a sum over
 // ranks (NCCL's fixed ring/tree order: identical on every rank and run).
 double* reduce_global(homfe_ctx* c, int nvals, int slot, cudaStream_t s) {
@@ -372,9 +407,9 @@ void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st,
   }
   if (c->fused) {
     fused_forward(c->ff, c->spp, const_cast<double*>(r), nullptr, nullptr, partials, s, 1);
-    all_to_all(c, c->ff.T, c->ff.Trecv, c->ff.chunk_t(), s);
+    xfer_t(c, s);
     fused_forward(c->ff, c->spp, const_cast<double*>(r), nullptr, nullptr, partials, s, 2);
-    all_to_all(c, c->ff.T2, c->ff.T2recv, c->ff.chunk_t2(), s);
+    xfer_t2(c, s, false);
     fused_inverse(c->ff, nullptr, nullptr, z, nullptr, 0, s);
     c->launches += 3;
     return;
@@ -425,8 +460,19 @@ void apply_K(homfe_ctx* c, const double* u, double* out, const double* fe, doubl
     c->launches += 3;
     return;
   }
-  if (c->dist) exchange_halo(c, u, s);
   ElemArgs a{u, c->d_hlo, c->d_hhi, c->d_ph_lo, out, c->d_phase, c->d_ke, c->n_phases, fe, scale, partials, st};
+  if (c->peer && u == c->d_p) {
+    // halo planes read in place from the neighbours' p (after a barrier: their
+    // last write of p, pass 3 or an upload, is complete)
+    const Grid& g = c->g;
+    const int prev = (g.rank - 1 + g.world) % g.world, next = (g.rank + 1) % g.world;
+    peer_barrier(c, s);
+    a.halo_lo = c->peer_p[prev] + (int64_t)(g.n0 - 1) * g.n1 * g.n2;
+    a.halo_hi = c->peer_p[next];
+    a.halo_cs = g.np;
+  } else if (c->dist) {
+    exchange_halo(c, u, s);
+  }
   if (c->hex_fast) launch_hex_fast(c->g, a, c->d_hexmat, c->hex_iso, s);
   else if (elem2d_eligible(c->g) && !c->no_fast2d) launch_elem2d(c->g, a, c->d_tri, s);
   else launch_apply_elem(c->g, a, s);
@@ -555,11 +601,11 @@ void capture_init(homfe_ctx* c, cudaStream_t s) {
   HB_CUDA(cudaMemsetAsync(c->d_x, 0, n * sizeof(double), s));
   if (c->fused) {
     fused_forward(c->ff, c->spp, c->d_r, nullptr, nullptr, c->d_partials, s, 1);
-    all_to_all(c, c->ff.T, c->ff.Trecv, c->ff.chunk_t(), s);
+    xfer_t(c, s);
     fused_forward(c->ff, c->spp, c->d_r, nullptr, nullptr, c->d_partials, s, 2);
     if (c->dist) launch_pcg_init(c->d_st, reduce_global(c, 1, 1, s), c->d_hist, s, 1);
     else launch_pcg_init(c->d_st, c->d_partials, c->d_hist, s);
-    all_to_all(c, c->ff.T2, c->ff.T2recv, c->ff.chunk_t2(), s);
+    xfer_t2(c, s, c->dist);
     fused_inverse(c->ff, c->d_p, nullptr, nullptr, nullptr, 1, s);  // p = z_0
     return;
   }
@@ -593,12 +639,12 @@ void body_sequence(homfe_ctx* c, cudaStream_t s, bool cond, cudaGraphConditional
     if (c->dist) launch_pcg_alpha(c->d_st, reduce_global(c, 1, 2, s), s, 1);
     else launch_pcg_alpha(c->d_st, c->d_partials, s);
     fused_forward(c->ff, c->spp, c->d_r, c->d_ap, c->d_st, c->d_partials, s, 1);
-    all_to_all(c, c->ff.T, c->ff.Trecv, c->ff.chunk_t(), s);
+    xfer_t(c, s);
     fused_forward(c->ff, c->spp, c->d_r, c->d_ap, c->d_st, c->d_partials, s, 2);
     if (c->dist) launch_pcg_beta(c->d_st, reduce_global(c, 1, 3, s), c->d_hist, s, 1);
     else if (cond) launch_pcg_beta_cond(c->d_st, c->d_partials, c->d_hist, h, s);
     else launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
-    all_to_all(c, c->ff.T2, c->ff.T2recv, c->ff.chunk_t2(), s);
+    xfer_t2(c, s, c->dist);
     fused_inverse(c->ff, c->d_p, c->d_x, nullptr, c->d_st, 0, s);
     return;
   }
@@ -1431,6 +1477,78 @@ namespace {
 
 // Shared constructor. world == 0: single device (periodic grid on one GPU);
 // world >= 1: slab `rank` of `world` along axis 0 with NCCL exchanges.
+// Peer pull setup (slab mode, 2..8 ranks): every rank's T, T2 and p
+// pointers, through CUDA IPC handles gathered over NCCL (or the in-process
+// transport's pointer exchange). On any IPC failure the context keeps the
+// all-to-all transport.
+void setup_peers(homfe_ctx* c) {
+  const int G = c->g.world, me = c->g.rank;
+  void* mine[3] = {c->ff.T, c->ff.T2, c->d_p};
+  void* ptrs[3][FusedFft::kMaxPeers] = {};
+  if (c->sim) {
+    for (int k = 0; k < 3; ++k)
+      sim_exchange(c, mine[k], [&](SimGroup* S) {
+        for (int q = 0; q < G; ++q) ptrs[k][q] = const_cast<void*>(S->ptr[q]);
+      });
+  } else {
+    std::vector<cudaIpcMemHandle_t> h((size_t)G * 3);
+    bool ok = true;
+    for (int k = 0; k < 3; ++k) ok = ok && cudaIpcGetMemHandle(&h[(size_t)me * 3 + k], mine[k]) == cudaSuccess;
+    // every rank takes part in the gather (a failed rank contributes zeros)
+    char* d_h = dalloc<char>(h.size() * sizeof(cudaIpcMemHandle_t));
+    const size_t per = 3 * sizeof(cudaIpcMemHandle_t);
+    if (!ok) std::memset(&h[(size_t)me * 3], 0, per);
+    HB_CUDA(cudaMemcpy(d_h + me * per, &h[(size_t)me * 3], per, cudaMemcpyHostToDevice));
+    HB_NCCL(ncclAllGather(d_h + me * per, d_h, per, ncclChar, c->comm, c->stream));
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+    HB_CUDA(cudaMemcpy(h.data(), d_h, h.size() * sizeof(cudaIpcMemHandle_t), cudaMemcpyDeviceToHost));
+    cudaFree(d_h);
+    // agree on the outcome: all ranks pull, or none
+    int flag = ok ? 1 : 0;
+    for (int q = 0; q < G && flag; ++q) {
+      if (q == me) {
+        for (int k = 0; k < 3; ++k) ptrs[k][q] = mine[k];
+        continue;
+      }
+      for (int k = 0; k < 3 && flag; ++k) {
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, h[(size_t)q * 3 + k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          cudaGetLastError();
+          flag = 0;
+          break;
+        }
+        c->ipc_open.push_back(p);
+        ptrs[k][q] = p;
+      }
+    }
+    int* d_flag = dalloc<int>(1);
+    HB_CUDA(cudaMemcpy(d_flag, &flag, sizeof(int), cudaMemcpyHostToDevice));
+    HB_NCCL(ncclAllReduce(d_flag, d_flag, 1, ncclInt, ncclMin, c->comm, c->stream));
+    HB_CUDA(cudaStreamSynchronize(c->stream));
+    HB_CUDA(cudaMemcpy(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost));
+    cudaFree(d_flag);
+    if (!flag) {
+      for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
+      c->ipc_open.clear();
+      return;
+    }
+  }
+  FusedFft& f = c->ff;
+  const int64_t ct = f.chunk_t(), ct2 = f.chunk_t2();
+  for (int q = 0; q < FusedFft::kMaxPeers; ++q) {
+    const int qq = q < G ? q : 0;
+    // base[q] + t(q, ...) == T_q + t(me, ...): T_q + (me - q) chunk (address arithmetic)
+    const auto tq = reinterpret_cast<uintptr_t>(ptrs[0][qq]);
+    const auto t2q = reinterpret_cast<uintptr_t>(ptrs[1][qq]);
+    f.tpull[q] = reinterpret_cast<const double2*>(tq + (intptr_t)(me - qq) * ct * (intptr_t)sizeof(double2));
+    f.t2pull[q] = reinterpret_cast<const double2*>(t2q + (intptr_t)(me - qq) * ct2 * (intptr_t)sizeof(double2));
+    c->peer_p[q] = static_cast<double*>(ptrs[2][qq]);
+  }
+  c->d_bar = dalloc<double>(1);
+  HB_CUDA(cudaMemset(c->d_bar, 0, sizeof(double)));
+  c->peer = true;
+}
+
 homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const void* nccl_id) {
   if (!desc) throw ValidationError("create: null argument");
   const int d = desc->dim;
@@ -1611,7 +1729,9 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
       f.T = ctx->d_spec;
       ctx->d_spec2 = dalloc<double2>(fused_sz);
       f.T2 = ctx->d_spec2;
-      if (G > 1) {
+      const char* penv = std::getenv("HOMFE_P2P");
+      if (G > 1 && G <= FusedFft::kMaxPeers && !(penv && penv[0] == '0')) setup_peers(ctx);
+      if (G > 1 && !ctx->peer) {
         ctx->d_spec_r = dalloc<double2>(fused_sz);
         ctx->d_spec2_r = dalloc<double2>(fused_sz);
         f.Trecv = ctx->d_spec_r;
@@ -1620,6 +1740,11 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
         f.Trecv = f.T;
         f.T2recv = f.T2;
       }
+      if (!ctx->peer)
+        for (int q = 0; q < FusedFft::kMaxPeers; ++q) {
+          f.tpull[q] = f.Trecv;
+          f.t2pull[q] = f.T2recv;
+        }
       f.tw_plane = ctx->d_tw;
       f.tw0 = ctx->d_tw + n1;
       fused_make_maps(f);
@@ -1661,6 +1786,13 @@ int homfe_gpu_create_dist(const homfe_grid_desc* desc, int32_t rank, int32_t wor
   });
 }
 
+int homfe_gpu_slab_transport(const homfe_ctx* c, int32_t* kind) {
+  return guarded([&] {
+    if (!c || !kind) throw ValidationError("slab_transport: null argument");
+    *kind = c->peer ? 2 : (c->dist && c->g.world > 1 ? 1 : 0);
+  });
+}
+
 int homfe_gpu_destroy(homfe_ctx* c) {
   if (!c) return HOMFE_OK;
   cudaSetDevice(c->device);
@@ -1688,6 +1820,8 @@ int homfe_gpu_destroy(homfe_ctx* c) {
   if (c->d_spec2) cudaFree(c->d_spec2);
   if (c->d_spec_r) cudaFree(c->d_spec_r);
   if (c->d_spec2_r) cudaFree(c->d_spec2_r);
+  for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
+  if (c->d_bar) cudaFree(c->d_bar);
   if (c->d_hlo) cudaFree(c->d_hlo);
   if (c->d_hhi) cudaFree(c->d_hhi);
   if (c->d_ph_lo) cudaFree(c->d_ph_lo);
@@ -1993,6 +2127,7 @@ int homfe_gpu_apply_K(homfe_ctx* c, const double* u, double* ku) {
     HB_CUDA(cudaSetDevice(c->device));
     require_material(c);
     const int64_t n = c->nvec();
+    if (c->peer) peer_barrier(c, c->stream);  // no peer still reads the previous d_p
     HB_CUDA(cudaMemcpyAsync(c->d_p, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, nullptr, nullptr, c->stream);
     HB_CUDA(cudaMemcpyAsync(ku, c->d_ap, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -21,6 +21,8 @@
 // Per component and voxel this moves 32 + 16 + 40 = 88 bytes, against 8
 // streaming passes (~216 bytes) for cuFFT + separate kernels.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -99,6 +101,7 @@ struct PlaneArgs {
   const PcgState* st;  // PCG mode
   int mode;
   int dbg;             // profiling only: bit mask of skipped phases
+  const double2* t2p[FusedFft::kMaxPeers];  // pass 3: chunk bases per source peer (FusedFft::t2pull)
 };
 
 template <int NP>
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
 #define HB_INV_GROUPUPD 1
 #endif
 template <int NP>
-__global__ void __launch_bounds__(NP, HB_INV_MINB) k_plane_inv(const PlaneArgs a) {
+__global__ void __launch_bounds__(NP, HB_INV_MINB) k_plane_inv(const __grid_constant__ PlaneArgs a) {
   constexpr int P = NP / 2 + 1;
   constexpr int CL = NP / 32;
   constexpr int TPF = tpf<NP>();
@@ -296,7 +299,8 @@ __global__ void __launch_bounds__(NP, HB_INV_MINB) k_plane_inv(const PlaneArgs a
     const int col = rank * 16 + jc;
     constexpr int PITCH = t_blocks(NP) * kTB;
     // rows k = 32 warp + 2 i + yo share one peer (n1l is a multiple of 32)
-    const double2* src = a.T2 + (int64_t)a.L.row2(comp, i0, 32 * warp + yo) * PITCH + col;
+    // (local receive buffer, or the source peer's own T2 over NVLink)
+    const double2* src = a.t2p[a.L.p1(32 * warp)] + (int64_t)a.L.row2(comp, i0, 32 * warp + yo) * PITCH + col;
     double2 v[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
@@ -455,7 +459,7 @@ struct PencilArgs {
   TLayout L;
   int P;                   // NP/2 + 1
   int ntk;                 // k2 tiles per k1
-  double2* T;
+  const double2* tp[FusedFft::kMaxPeers];  // chunk bases per source peer (FusedFft::tpull)
   double2* T2;
   const double2* tw;       // W_N0 four-step table
   const PcgState* st;      // nullable
@@ -478,7 +482,8 @@ template <int N0, int C>
 #define HB_PENCIL_MINB 2
 #endif
 __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB)
-    k_pencil(const __grid_constant__ SpecParams sp, const PencilArgs a, const __grid_constant__ CUtensorMap t2map) {
+    k_pencil(const __grid_constant__ SpecParams sp, const __grid_constant__ PencilArgs a,
+             const __grid_constant__ CUtensorMap t2map) {
   // Persistent blocks; tile = (k1 row, BK columns) for all C components.
   // Each tile's T data (BK/4 column groups x C components x peers, each a
   // contiguous run) is bulk-copied (TMA) into one of two stages while the
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
         if (c0 / kTG + gg >= a.L.ng) continue;
         for (int q = 0; q < world; ++q)
           fft::bulk_g2s(stage0 + st * STAGE + ((c * NGB + gg) * N0 + q * nzl) * kTG,
-                        a.T + a.L.t(q, c, k1l, c0 + gg * kTG, 0), nzl * kTG * (uint32_t)sizeof(double2),
+                        a.tp[q] + a.L.t(q, c, k1l, c0 + gg * kTG, 0), nzl * kTG * (uint32_t)sizeof(double2),
                         &full[st]);
       }
   };
@@ -698,6 +703,14 @@ void launch_cluster(K kernel, int grid, int block, int cl, size_t smem, cudaStre
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  static bool shown = false;
+  if (!shown && std::getenv("HOMFE_FFT_OCC")) {
+    shown = true;
+    int ncl = 0;
+    HB_CUDA(cudaOccupancyMaxActiveClusters(&ncl, kernel, &cfg));
+    std::fprintf(stderr, "plane kernel: cluster %d, smem %zu, max active clusters %d, grid clusters %d\n", cl, smem,
+                 ncl, grid / cl);
+  }
   HB_CUDA(cudaLaunchKernelEx(&cfg, kernel, a));
 }
 
@@ -721,7 +734,7 @@ void run_pencils_c(const FusedFft& f, const SpecParams& sp, const PcgState* st, 
   a.L = layout_of(f);
   a.P = f.np_plane / 2 + 1;
   a.ntk = (a.P + BK - 1) / BK;
-  a.T = f.Trecv;
+  for (int q = 0; q < FusedFft::kMaxPeers; ++q) a.tp[q] = f.tpull[q];
   a.T2 = f.T2;
   a.tw = f.tw0;
   a.st = st;
@@ -832,7 +845,7 @@ void fused_inverse(const FusedFft& f, double* p, double* x, double* z, const Pcg
   a.np = f.np;
   a.L = layout_of(f);
   a.T = f.T;
-  a.T2 = f.T2recv;
+  for (int q = 0; q < FusedFft::kMaxPeers; ++q) a.t2p[q] = f.t2pull[q];
   a.tw = f.tw_plane;
   a.p = p;
   a.x = x;

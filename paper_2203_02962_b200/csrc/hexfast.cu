@@ -148,6 +148,7 @@ struct HexArgs {
   const double* u;
   const double* halo_lo, *halo_hi;  // dist mode: neighbour planes [c][plane]
   const uint8_t* ph_lo;             // dist mode: phase plane z0-1
+  int64_t halo_cs;                  // dist mode: component stride of the halo planes
   int dist;
   double* out;
   const uint8_t* phase;
@@ -202,9 +203,9 @@ __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
       int64_t cs[2];
       if (a.dist) {
         up[0] = z < 0 ? a.halo_lo : a.u + (int64_t)z * plane;
-        cs[0] = z < 0 ? plane : np;
+        cs[0] = z < 0 ? a.halo_cs : np;
         up[1] = z1 >= a.n0 ? a.halo_hi : a.u + (int64_t)z1 * plane;
-        cs[1] = z1 >= a.n0 ? plane : np;
+        cs[1] = z1 >= a.n0 ? a.halo_cs : np;
       } else {
         z = z < 0 ? z + a.n0 : z;
         z1 = z + 1 == a.n0 ? 0 : z + 1;
@@ -394,7 +395,7 @@ __device__ __forceinline__ void z_issue(const HexArgs& a, const int* its, int u,
   int64_t cs;
   if (a.dist) {
     src = pz < 0 ? a.halo_lo : (pz >= a.n0 ? a.halo_hi : a.u + (int64_t)pz * plane);
-    cs = (pz < 0 || pz >= a.n0) ? plane : np;
+    cs = (pz < 0 || pz >= a.n0) ? a.halo_cs : np;  // exchanged planes or a peer's field
   } else {
     pz = pz < 0 ? pz + a.n0 : (pz >= a.n0 ? pz - a.n0 : pz);
     src = a.u + (int64_t)pz * plane;
@@ -887,6 +888,7 @@ void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, boo
   a.halo_lo = ea.halo_lo;
   a.halo_hi = ea.halo_hi;
   a.ph_lo = ea.ph_lo;
+  a.halo_cs = ea.halo_cs ? ea.halo_cs : (int64_t)g.n1 * g.n2;
   a.dist = g.dist;
   a.out = ea.out;
   a.phase = ea.phase;

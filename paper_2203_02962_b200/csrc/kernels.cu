@@ -106,14 +106,14 @@ __global__ void __launch_bounds__(kBlock) k_apply_elem(const Grid g, const ElemA
           b0 = j & 1; b1 = (j >> 1) & 1;
         }
         const int64_t nidx = flat(w0[1 - a0 + b0], w1[1 - a1 + b1], w2[1 - a2 + b2]);
-        // slab mode: node planes -1 / n0 come from the halo planes ([c][plane])
+        // slab mode: node planes -1 / n0 come from the halo planes (exchanged, or a peer's field)
         const double* ub = a.u;
         int64_t cs = np, ni = nidx;
         if (D == 3 && g.dist) {
           const int z = c0 - a0 + b0;
           if (z < 0 || z >= g.n0) {
             ub = z < 0 ? a.halo_lo : a.halo_hi;
-            cs = (int64_t)g.n1 * g.n2;
+            cs = a.halo_cs ? a.halo_cs : (int64_t)g.n1 * g.n2;
             ni = (int64_t)w1[1 - a1 + b1] * g.n2 + w2[1 - a2 + b2];
           }
         }

@@ -25,6 +25,8 @@ struct ElemArgs {
   double scale;           // out = scale * (K u + f)
   double* partials;       // nullable: per-block sum of u . out
   const PcgState* st;     // nullable: skip when st->done
+  int64_t halo_cs;        // component stride of the halo planes (0: one plane, i.e.
+                          // exchanged buffers; np when they point into a peer's field)
 };
 
 // Node-centric K u (+ f) from per-phase element matrices; any grid size.
@@ -150,6 +152,13 @@ struct FusedFft {
   const double2* tw0;         // W_{n0g} table
   int dbg;                    // profiling: skipped phases (HOMFE_FFT_DBG)
   alignas(64) unsigned char t2map[128];  // CUtensorMap of T2 (pass-2 TMA stores), fused_make_maps
+  // where pass 2 / pass 3 read the chunk of source peer q: base pointers such
+  // that base[q] + TLayout::t(q, ...) (resp. t2) addresses it. Exchanged
+  // receive buffers: base[q] = Trecv. Peer pull (NVLink, no all-to-all):
+  // base[q] = T of rank q + (rank - q) * chunk, i.e. q's send-side chunk for me.
+  static constexpr int kMaxPeers = 8;
+  const double2* tpull[kMaxPeers];
+  const double2* t2pull[kMaxPeers];
   int64_t chunk_t() const { return (int64_t)c * n1l * ((np_plane / 2 + 4) / 4) * n0 * 4; }
   int64_t chunk_t2() const { return (int64_t)c * n0 * n1l * (((np_plane / 2 + 16) / 16) * 16); }
 };

@@ -65,6 +65,13 @@ class slab_layout:
     def t2(self, peer, comp, i0l, k1l, k2):
         return (((peer * self.c + comp) * self.nzl + i0l) * self.n1l + k1l) * (self.nb * self.TB) + k2
 
+    @staticmethod
+    def pull_offset(me, q, chunk):
+        """Peer pull (context.cu setup_peers): rank `me` reads source q's
+        element t(q, ...) at q's own send buffer + (me - q) * chunk + t(q, ...),
+        i.e. q's send-side chunk addressed to `me`."""
+        return (me - q) * chunk
+
 
 def nccl_unique_id():
     buf = (C.c_uint8 * 128)()
@@ -99,6 +106,14 @@ class SlabContext:
         self.m = grid.dim if components == 1 else mandel_dim(grid.dim)
         self.z0, self.nz = slab_range(grid.dims[0], rank, world)
         self.n_local = self.nz * grid.dims[1] * grid.dims[2]
+
+    @property
+    def transport(self):
+        """'single', 'all_to_all' (NCCL exchanges) or 'peer_pull' (passes 2/3
+        and the K halo read the peers' fields in place; HOMFE_P2P=0 disables)."""
+        k = C.c_int32()
+        _check(lib.homfe_gpu_slab_transport(self.h, C.byref(k)))
+        return ("single", "all_to_all", "peer_pull")[k.value]
 
     def __del__(self):
         h = getattr(self, "h", None)

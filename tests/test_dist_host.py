@@ -99,21 +99,46 @@ def _worker(rank, world, port, out):
             for k1 in range(n1):
                 row = np.array([T2r[L.t2(k1 // L.n1l, comp, i0l, k1 % L.n1l, k2)] for k2 in range(P)])
                 ok_t2 &= np.array_equal(row, Y[comp, z0 + i0l, k1])
+    # ---- peer pull (no all-to-all): every rank's send buffers readable in
+    # place (all_gather stands in for the NVLink mappings); passes 2 and 3
+    # address source q's chunk for this rank through the pull offsets
+    def gather(buf):
+        t = torch.from_numpy(buf.view(np.float64).copy())
+        allb = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allb, t)
+        return [b.numpy().view(np.complex128) for b in allb]
+    Tall, T2all = gather(T), gather(T2)
+    ok_pull = True
+    for comp in range(c):
+        for k1l in range(L.n1l):
+            for k2 in range(P):
+                pencil = []
+                for i0 in range(n0):
+                    q = i0 // L.nzl
+                    off = L.pull_offset(rank, q, L.chunk_t())
+                    pencil.append(Tall[q][off + L.t(q, comp, k1l, k2, i0 % L.nzl)])
+                ok_pull &= np.array_equal(np.array(pencil), X[comp, :, rank * L.n1l + k1l, k2])
+        for i0l in range(nz):
+            for k1 in range(n1):
+                q = k1 // L.n1l
+                off = L.pull_offset(rank, q, L.chunk_t2())
+                row = np.array([T2all[q][off + L.t2(q, comp, i0l, k1 % L.n1l, k2)] for k2 in range(P)])
+                ok_pull &= np.array_equal(row, Y[comp, z0 + i0l, k1])
     # ---- scalar all-reduction of per-rank partial sums
     part = torch.tensor([float(np.sum(local ** 2))], dtype=torch.float64)
     dist.all_reduce(part)
     ok_red = abs(part.item() - float(np.sum(glob ** 2))) <= 1e-12 * float(np.sum(glob ** 2))
-    out[rank] = (bool(ok_halo), bool(ok_t), bool(ok_t2), bool(ok_red))
+    out[rank] = (bool(ok_halo), bool(ok_t), bool(ok_t2), bool(ok_red), bool(ok_pull))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [1, 2])
+@pytest.mark.parametrize("world", [1, 2, 4])
 def test_slab_exchanges_gloo(world):
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     for r in range(world):
-        assert out[r] == (True, True, True, True), (r, out[r])
+        assert out[r] == (True, True, True, True, True), (r, out[r])
 
 
 def test_slab_ranges_and_halos_match_reference_wrap(oracle_mod):

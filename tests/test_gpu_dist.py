@@ -51,15 +51,21 @@ def test_slab_world1_matches_single_device(hb, dims, c):
     assert _rel(out["average_stress"], ref["average_stress"]) < 1e-12
 
 
-@pytest.mark.parametrize("world,dims,c", [(2, (64, 128, 128), 3), (2, (128, 128, 128), 3), (4, (128, 128, 128), 1), (8, (128, 256, 256), 3)])
-def test_slab_multi_rank_in_process_matches_single_device(hb, world, dims, c):
-    """World > 1 on one GPU through the in-process transport (host barriers +
-    device copies instead of NCCL; no device-side waiting between ranks): the
-    halo ring, both peer-chunk transposes of the fused passes, the pencil
-    frequency offsets and the rank-ordered reductions against the
+@pytest.mark.parametrize("world,dims,c,transport", [
+    (2, (64, 128, 128), 3, "peer_pull"), (2, (128, 128, 128), 3, "peer_pull"), (4, (128, 128, 128), 1, "peer_pull"),
+    (8, (128, 256, 256), 3, "peer_pull"), (2, (128, 128, 128), 3, "all_to_all"), (4, (128, 128, 128), 1, "all_to_all"),
+    (8, (128, 256, 256), 3, "all_to_all")])
+def test_slab_multi_rank_in_process_matches_single_device(hb, world, dims, c, transport, monkeypatch):
+    """World > 1 on one GPU through the in-process transport (host barriers
+    instead of NCCL; no device-side waiting between ranks): the halo ring (sent
+    planes, or the neighbours' p read in place by the K kernels), both
+    peer-chunk transposes of the fused passes (all-to-all copies, or passes 2
+    and 3 pulling the source ranks' chunks straight from their buffers), the
+    pencil frequency offsets and the rank-ordered reductions against the
     single-device context."""
     import threading
     from paper_2203_02962_b200 import dist, inputs
+    monkeypatch.setenv("HOMFE_P2P", "1" if transport == "peer_pull" else "0")
     ph, _ = inputs.rsa_balls(dims, radius=6.0, seed=5, fraction=0.25)
     if c == 1:
         cm = np.stack([np.eye(3), 100.0 * np.eye(3)])
@@ -77,13 +83,14 @@ def test_slab_multi_rank_in_process_matches_single_device(hb, world, dims, c):
     r = u - u.mean(axis=1, keepdims=True)
     z_ref = hb.apply_preconditioner(g, hb.assemble_preconditioner(g, cm[0], c), r)
     plane = dims[1] * dims[2]
-    gid = 1000 + world * 10 + c
+    gid = 1000 + world * 10 + c + (0 if transport == "peer_pull" else 500) + dims[0]
     res = [None] * world
     errors = []
 
     def rank_main(rank):
         try:
             sc = dist.SlabContext(g, c, rank, world, dist.sim_group_id(gid))
+            assert sc.transport == transport
             z0, nz = sc.z0, sc.nz
             sl = slice(z0 * plane, (z0 + nz) * plane)
             sc.set_material(cm, ph[sl])
