@@ -147,6 +147,8 @@ def run_gpu(args, rank, world, local_rank):
         if world > 1:
             torch.distributed.broadcast_object_list(obj, src=0)
         sc = hdist.SlabContext(g, cfg.components, rank, world, obj[0], device=local_rank)
+        transport = {"peer_pull": "peer pull over NVLink + barrier all-reduces",
+                     "all_to_all": "NCCL halo + all-to-all", "single": "one rank"}[sc.transport]
         z0, nz = hdist.slab_range(g.dims[0], rank, world)
         plane = g.dims[1] * g.dims[2]
         ph_local = np.ascontiguousarray(phases[z0 * plane:(z0 + nz) * plane])
@@ -202,6 +204,7 @@ def run_gpu(args, rank, world, local_rank):
     # per-kernel breakdown of one PCG iteration (CUDA events, live)
     ms = np.zeros(8)
     hb._check(lib.homfe_gpu_kernel_times(ctx_h, 20, ms.ctypes.data_as(C.POINTER(C.c_double))))
+    fused_planes = bool(ms[2] < 0)  # the fused passes report no separate FFT kernels
 
     # e2e: host buffers through the C ABI, copies inside the timed region
     # pinned host buffers (the contract's H2D/D2H from page-locked memory)
@@ -254,8 +257,9 @@ def run_gpu(args, rank, world, local_rank):
         "data": "synthetic: seeded RSA inclusions / GRF per SURVEY 8(d) (no dataset in the reference)",
         "config": {"workload": WORKLOADS[args.config], "dims": list(cfg.dims), "dof": dof,
                    "pcg_iterations_per_step": iters // args.steps, "newton_steps": rep.n_steps,
-                   "parallelism": f"slab decomposition over {world} GPUs (NCCL halo + all-to-all)" if world > 1
-                   else "1 GPU",
+                   "parallelism": (f"slab decomposition over {world} GPUs ({transport}, "
+                                   f"{'fused FFT passes' if fused_planes else 'slab spectra: cuFFT + transposes'})")
+                   if slab else "1 GPU",
                    "l2": f"inputs exceed L2: {cfg.components * g.num_pixels * 8 / 1e6:.0f} MB per vector vs 126 MB"
                    if cfg.components * g.num_pixels * 8 > 126e6 else "L2-resident working set (no flush)"},
         "time_to_solution_s": wall_max / args.steps,
@@ -339,7 +343,20 @@ def run_reference(args, rank, world):
             "note": "reference not buildable in this image (Eigen3, FFTW3, vendor/ absent); CPU oracle port timed"}
 
 
+def _emit(out):
+    """The one JSON line, on the real stdout (see main: fd 1 is stderr while
+    libraries run, so banners such as NCCL's cannot interleave with it)."""
+    os.write(_JSON_FD, (json.dumps(out) + "\n").encode())
+
+
+_JSON_FD = 1
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -369,7 +386,7 @@ def main():
     if args.impl == "reference":
         out = run_reference(args, rank, world)
         if out is not None:
-            print(json.dumps(out), flush=True)
+            _emit(out)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
@@ -380,7 +397,7 @@ def main():
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_baseline(args)
             out["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        print(json.dumps(out), flush=True)
+        _emit(out)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -183,6 +183,16 @@ struct homfe_ctx {
   // own pointers); the all-to-alls and halo sends become stream barriers
   bool peer = false;
   double* peer_p[FusedFft::kMaxPeers] = {};  // every rank's p (d_p)
+  void* peer_a[FusedFft::kMaxPeers] = {};    // every rank's T (fused) / W (slab spectra)
+  void* peer_b[FusedFft::kMaxPeers] = {};    // every rank's T2 (fused) / S (slab spectra)
+  // slab spectra for plane sizes outside the fused passes (slabfft.cu)
+  bool slab_fft = false;
+  SlabDims sd{};
+  cufftHandle p2f = 0, p2i = 0, p1 = 0;      // 2-D D2Z / Z2D of the local planes; 1-D Z2Z along axis 0
+  double2* d_S = nullptr;                    // [c][n0l][n1][nh]
+  double2* d_W = nullptr;                    // [c][n0][n1l][nh]
+  double2* d_send = nullptr;                 // all-to-all chunks (push == 0)
+  double2* d_recv = nullptr;
   std::vector<void*> ipc_open;               // IPC mappings to close
   double* d_bar = nullptr;                   // barrier all-reduce scratch
 
@@ -392,6 +402,69 @@ void fft_inverse(homfe_ctx* c, double* out, cudaStream_t s) {
   HB_CUFFT(cufftExecZ2D(c->inv, reinterpret_cast<cufftDoubleComplex*>(c->d_spec), out));
 }
 
+// ---- slab spectra for any plane size (slabfft.cu) ------------------------
+// forward: 2-D r2c of the local planes, transpose to k1 rows (pushed into the
+// owners' W, or all-to-all), 1-D transform along axis 0 per component
+void slab_forward(homfe_ctx* c, const double* in, cudaStream_t s) {
+  const SlabDims& d = c->sd;
+  HB_CUFFT(cufftSetStream(c->p2f, s));
+  HB_CUFFT(cufftExecD2Z(c->p2f, const_cast<double*>(in), reinterpret_cast<cufftDoubleComplex*>(c->d_S)));
+  double2* dst[FusedFft::kMaxPeers];
+  if (c->peer || d.world == 1) {  // world 1: the "transpose" lands in the own W
+    for (int q = 0; q < d.world; ++q) dst[q] = static_cast<double2*>(c->peer_a[q]);
+    launch_slab_pack_fwd(d, c->d_S, dst, 1, s);
+    if (c->peer) peer_barrier(c, s);
+  } else {
+    for (int q = 0; q < d.world; ++q) dst[q] = c->d_send + q * d.chunk();
+    launch_slab_pack_fwd(d, c->d_S, dst, 0, s);
+    all_to_all(c, c->d_send, c->d_recv, d.chunk(), s);
+    launch_slab_unpack_fwd(d, c->d_recv, c->d_W, s);
+  }
+  HB_CUFFT(cufftSetStream(c->p1, s));
+  const int64_t per = (int64_t)d.n0 * d.n1l * d.nh;
+  for (int k = 0; k < d.c; ++k) {
+    auto* w = reinterpret_cast<cufftDoubleComplex*>(c->d_W + k * per);
+    HB_CUFFT(cufftExecZ2Z(c->p1, w, w, CUFFT_FORWARD));
+  }
+  c->launches += 3 + d.c;
+}
+
+// z_hat = K_ref_hat^+ r_hat / N_p on this rank's k1 rows (global frequencies)
+void slab_solve(homfe_ctx* c, const PcgState* st, double* partials, cudaStream_t s) {
+  SpecParams p = c->spp;
+  p.nf = (int64_t)c->sd.n0 * c->sd.n1l * c->sd.nh;
+  p.n1r = c->sd.n1l;
+  p.k1off = c->sd.me * c->sd.n1l;
+  launch_spectral(p, c->d_W, st, partials, s);
+  c->launches += 1;
+}
+
+// inverse: 1-D along axis 0, transpose back to planes, 2-D c2r
+void slab_inverse(homfe_ctx* c, double* out, cudaStream_t s) {
+  const SlabDims& d = c->sd;
+  HB_CUFFT(cufftSetStream(c->p1, s));
+  const int64_t per = (int64_t)d.n0 * d.n1l * d.nh;
+  for (int k = 0; k < d.c; ++k) {
+    auto* w = reinterpret_cast<cufftDoubleComplex*>(c->d_W + k * per);
+    HB_CUFFT(cufftExecZ2Z(c->p1, w, w, CUFFT_INVERSE));
+  }
+  double2* dst[FusedFft::kMaxPeers];
+  if (c->peer || d.world == 1) {
+    // peers finished reading their S (their pack_fwd) before the forward barrier
+    for (int q = 0; q < d.world; ++q) dst[q] = static_cast<double2*>(c->peer_b[q]);
+    launch_slab_pack_inv(d, c->d_W, dst, 1, s);
+    if (c->peer) peer_barrier(c, s);
+  } else {
+    for (int q = 0; q < d.world; ++q) dst[q] = c->d_send + q * d.chunk();
+    launch_slab_pack_inv(d, c->d_W, dst, 0, s);
+    all_to_all(c, c->d_send, c->d_recv, d.chunk(), s);
+    launch_slab_unpack_inv(d, c->d_recv, c->d_S, s);
+  }
+  HB_CUFFT(cufftSetStream(c->p2i, s));
+  HB_CUFFT(cufftExecZ2D(c->p2i, reinterpret_cast<cufftDoubleComplex*>(c->d_S), out));
+  c->launches += 3 + d.c;
+}
+
 // z = M^-1 r; optional Parseval r.z partials.
 void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st, double* partials,
                    cudaStream_t s) {
@@ -403,6 +476,12 @@ void precond_apply(homfe_ctx* c, const double* r, double* z, const PcgState* st,
     fft_inverse(c, z, s);
     if (partials) launch_dot_partials(r, z, c->nvec(), partials, s);
     c->launches += 4;
+    return;
+  }
+  if (c->slab_fft) {
+    slab_forward(c, r, s);
+    slab_solve(c, st, partials, s);
+    slab_inverse(c, z, s);
     return;
   }
   if (c->fused) {
@@ -610,7 +689,8 @@ void capture_init(homfe_ctx* c, cudaStream_t s) {
     return;
   }
   precond_apply(c, c->d_r, c->d_z, nullptr, c->d_partials, s);
-  launch_pcg_init(c->d_st, c->d_partials, c->d_hist, s);
+  if (c->dist) launch_pcg_init(c->d_st, reduce_global(c, 1, 1, s), c->d_hist, s, 1);
+  else launch_pcg_init(c->d_st, c->d_partials, c->d_hist, s);
   HB_CUDA(cudaMemcpyAsync(c->d_p, c->d_z, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
 }
 
@@ -646,6 +726,19 @@ void body_sequence(homfe_ctx* c, cudaStream_t s, bool cond, cudaGraphConditional
     else launch_pcg_beta(c->d_st, c->d_partials, c->d_hist, s);
     xfer_t2(c, s, c->dist);
     fused_inverse(c->ff, c->d_p, c->d_x, nullptr, c->d_st, 0, s);
+    return;
+  }
+  if (c->slab_fft) {
+    // slab spectra for other plane sizes: the cuFFT-path sequence with the
+    // scalars reduced over the ranks
+    apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s);
+    launch_pcg_alpha(c->d_st, reduce_global(c, 1, 2, s), s, 1);
+    launch_update_r(c->d_r, c->d_ap, n, c->d_st, s);
+    slab_forward(c, c->d_r, s);
+    slab_solve(c, c->d_st, c->d_partials, s);
+    launch_pcg_beta(c->d_st, reduce_global(c, 1, 3, s), c->d_hist, s, 1);
+    slab_inverse(c, c->d_z, s);
+    launch_update_xp(c->d_x, c->d_p, c->d_z, n, c->d_st, s);
     return;
   }
   apply_K(c, c->d_p, c->d_ap, nullptr, 1.0, c->d_partials, c->d_st, s);
@@ -1477,13 +1570,18 @@ namespace {
 
 // Shared constructor. world == 0: single device (periodic grid on one GPU);
 // world >= 1: slab `rank` of `world` along axis 0 with NCCL exchanges.
-// Peer pull setup (slab mode, 2..8 ranks): every rank's T, T2 and p
-// pointers, through CUDA IPC handles gathered over NCCL (or the in-process
-// transport's pointer exchange). On any IPC failure the context keeps the
-// all-to-all transport.
-void setup_peers(homfe_ctx* c) {
+bool p2p_wanted(int world) {
+  const char* penv = std::getenv("HOMFE_P2P");
+  return world > 1 && world <= FusedFft::kMaxPeers && !(penv && penv[0] == '0');
+}
+
+// Peer access setup (slab mode, 2..8 ranks): every rank's two spectrum
+// buffers (fused: T, T2; slab spectra: W, S) and p, through CUDA IPC handles
+// gathered over NCCL (or the in-process transport's pointer exchange). On
+// any IPC failure on any rank the context keeps the all-to-all transport.
+void setup_peers(homfe_ctx* c, void* buf_a, void* buf_b) {
   const int G = c->g.world, me = c->g.rank;
-  void* mine[3] = {c->ff.T, c->ff.T2, c->d_p};
+  void* mine[3] = {buf_a, buf_b, c->d_p};
   void* ptrs[3][FusedFft::kMaxPeers] = {};
   if (c->sim) {
     for (int k = 0; k < 3; ++k)
@@ -1533,15 +1631,10 @@ void setup_peers(homfe_ctx* c) {
       return;
     }
   }
-  FusedFft& f = c->ff;
-  const int64_t ct = f.chunk_t(), ct2 = f.chunk_t2();
   for (int q = 0; q < FusedFft::kMaxPeers; ++q) {
     const int qq = q < G ? q : 0;
-    // base[q] + t(q, ...) == T_q + t(me, ...): T_q + (me - q) chunk (address arithmetic)
-    const auto tq = reinterpret_cast<uintptr_t>(ptrs[0][qq]);
-    const auto t2q = reinterpret_cast<uintptr_t>(ptrs[1][qq]);
-    f.tpull[q] = reinterpret_cast<const double2*>(tq + (intptr_t)(me - qq) * ct * (intptr_t)sizeof(double2));
-    f.t2pull[q] = reinterpret_cast<const double2*>(t2q + (intptr_t)(me - qq) * ct2 * (intptr_t)sizeof(double2));
+    c->peer_a[q] = ptrs[0][qq];
+    c->peer_b[q] = ptrs[1][qq];
     c->peer_p[q] = static_cast<double*>(ptrs[2][qq]);
   }
   c->d_bar = dalloc<double>(1);
@@ -1643,7 +1736,8 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     // spectrum scratch: cuFFT layout, or the tile-major layout of the fused
     // passes (16-column blocks, fftfused.cu) when that is larger
     const int64_t pitch = ((int64_t)(g.n2 / 2 + 1) + 15) / 16 * 16;
-    const int64_t fused_sz = d == 3 ? (int64_t)c * g.n0 * g.n1 * pitch : 0;
+    const bool fz = d == 3 && (!dist || (fused_fft_eligible(g) && g.n1 % G == 0));  // slab spectra: own buffers
+    const int64_t fused_sz = fz ? (int64_t)c * g.n0 * g.n1 * pitch : 0;
     ctx->d_spec = dalloc<double2>(std::max<int64_t>(dist ? 0 : (int64_t)c * g.nn * ctx->nf, fused_sz));
     ctx->d_phase = dalloc<uint8_t>(g.np);
     ctx->d_partials = dalloc<double>((size_t)kRedBlocks * 8);
@@ -1670,6 +1764,8 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     p.c = c;
     p.n0 = g.n0g;
     p.n1 = g.n1;
+    p.n1r = g.n1;
+    p.k1off = 0;
     p.n2 = g.n2;
     p.nh = nh;
     p.nf = ctx->nf;
@@ -1692,7 +1788,33 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     if (const char* env = std::getenv("HOMFE_FAST2D")) ctx->no_fast2d = env[0] == '0';
     const char* fenv = std::getenv("HOMFE_FUSED_FFT");
     const bool fused_ok = fused_fft_eligible(g) && g.n1 % G == 0;
-    if (dist && !fused_ok) throw ValidationError("slab mode: plane size must be 128 or 256 and n0 in {64,128,256}");
+    if (dist && !fused_ok) {
+      // slab spectra for any plane size: cuFFT per rank + transposes (slabfft.cu)
+      SlabDims& sd = ctx->sd;
+      sd = SlabDims{c, g.n0g, g.n0, g.n1, g.n1 / G, g.n2 / 2 + 1, g.rank, G};
+      const int nh2 = sd.nh;
+      int n2d[2] = {g.n1, g.n2};
+      HB_CUFFT(cufftPlanMany(&ctx->p2f, 2, n2d, nullptr, 1, g.n1 * g.n2, nullptr, 1, g.n1 * nh2, CUFFT_D2Z,
+                             c * g.n0));
+      HB_CUFFT(cufftPlanMany(&ctx->p2i, 2, n2d, nullptr, 1, g.n1 * nh2, nullptr, 1, g.n1 * g.n2, CUFFT_Z2D,
+                             c * g.n0));
+      int n1d[1] = {g.n0g};
+      const int rs = sd.n1l * nh2;  // axis-0 stride of W
+      HB_CUFFT(cufftPlanMany(&ctx->p1, 1, n1d, n1d, rs, 1, n1d, rs, 1, CUFFT_Z2Z, rs));
+      const int64_t tot = sd.chunk() * G;
+      ctx->d_S = dalloc<double2>(tot);
+      ctx->d_W = dalloc<double2>(tot);
+      if (p2p_wanted(G)) setup_peers(ctx, ctx->d_W, ctx->d_S);
+      if (G == 1) {
+        ctx->peer_a[0] = ctx->d_W;
+        ctx->peer_b[0] = ctx->d_S;
+      }
+      if (!ctx->peer && G > 1) {
+        ctx->d_send = dalloc<double2>(tot);
+        ctx->d_recv = dalloc<double2>(tot);
+      }
+      ctx->slab_fft = true;
+    }
     if (fused_ok && (dist || !(fenv && fenv[0] == '0'))) {
       const int n1 = g.n1, n0 = g.n0g;
       // twiddles: N <= 256 in the four-step layout tw[k2 * (N/16) + n1] =
@@ -1729,8 +1851,20 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
       f.T = ctx->d_spec;
       ctx->d_spec2 = dalloc<double2>(fused_sz);
       f.T2 = ctx->d_spec2;
-      const char* penv = std::getenv("HOMFE_P2P");
-      if (G > 1 && G <= FusedFft::kMaxPeers && !(penv && penv[0] == '0')) setup_peers(ctx);
+      if (p2p_wanted(G)) setup_peers(ctx, f.T, f.T2);
+      if (ctx->peer) {
+        // pass 2 / 3 read source q's chunk for this rank in place:
+        // base[q] + t(q, ...) == T_q + t(me, ...), i.e. base[q] = T_q + (me - q) chunk
+        const int me = g.rank;
+        for (int q = 0; q < FusedFft::kMaxPeers; ++q) {
+          const int qq = q < G ? q : 0;
+          const auto tq = reinterpret_cast<uintptr_t>(ctx->peer_a[q]);
+          const auto t2q = reinterpret_cast<uintptr_t>(ctx->peer_b[q]);
+          f.tpull[q] = reinterpret_cast<const double2*>(tq + (intptr_t)(me - qq) * f.chunk_t() * (intptr_t)sizeof(double2));
+          f.t2pull[q] =
+              reinterpret_cast<const double2*>(t2q + (intptr_t)(me - qq) * f.chunk_t2() * (intptr_t)sizeof(double2));
+        }
+      }
       if (G > 1 && !ctx->peer) {
         ctx->d_spec_r = dalloc<double2>(fused_sz);
         ctx->d_spec2_r = dalloc<double2>(fused_sz);
@@ -1822,6 +1956,11 @@ int homfe_gpu_destroy(homfe_ctx* c) {
   if (c->d_spec2_r) cudaFree(c->d_spec2_r);
   for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
   if (c->d_bar) cudaFree(c->d_bar);
+  if (c->p2f) cufftDestroy(c->p2f);
+  if (c->p2i) cufftDestroy(c->p2i);
+  if (c->p1) cufftDestroy(c->p1);
+  for (double2* b : {c->d_S, c->d_W, c->d_send, c->d_recv})
+    if (b) cudaFree(b);
   if (c->d_hlo) cudaFree(c->d_hlo);
   if (c->d_hhi) cudaFree(c->d_hhi);
   if (c->d_ph_lo) cudaFree(c->d_ph_lo);
@@ -2303,9 +2442,15 @@ int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
       return;
     }
     ms[1] = timeit([&] { launch_update_r(c->d_r, c->d_ap, n, c->d_st, s); });
-    ms[2] = timeit([&] { fft_forward(c, c->d_r, s); });
-    ms[3] = timeit([&] { launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s); });
-    ms[4] = timeit([&] { fft_inverse(c, c->d_z, s); });
+    if (c->slab_fft) {  // with the transposes (exchange included)
+      ms[2] = timeit([&] { slab_forward(c, c->d_r, s); });
+      ms[3] = timeit([&] { slab_solve(c, c->d_st, c->d_partials, s); });
+      ms[4] = timeit([&] { slab_inverse(c, c->d_z, s); });
+    } else {
+      ms[2] = timeit([&] { fft_forward(c, c->d_r, s); });
+      ms[3] = timeit([&] { launch_spectral(c->spp, c->d_spec, c->d_st, c->d_partials, s); });
+      ms[4] = timeit([&] { fft_inverse(c, c->d_z, s); });
+    }
     ms[5] = timeit([&] { launch_update_xp(c->d_x, c->d_p, c->d_z, n, c->d_st, s); });
     ms[6] = timeit([&] {
       launch_pcg_alpha(c->d_st, c->d_partials, s);

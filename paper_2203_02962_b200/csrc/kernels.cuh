@@ -134,9 +134,24 @@ struct SpecParams {
   int iso;              // C_ref isotropic: K_hat = (lam + mu) M + mu tr(M) I (c = d) / kappa tr(M)
   double lam, mu;       // isotropic reference moduli (mu = kappa for c = 1)
   const double4* tab[3];  // per axis: (sin, cos, sin(t/2), cos(t/2))
+  int n1r, k1off;         // 3-D: axis-1 rows held (n1, or a slab rank's n1/W) and the first one's k1
 };
 void launch_spectral(const SpecParams& p, double2* spec, const PcgState* st, double* partials,
                      cudaStream_t s);
+
+// Slab-decomposed spectra for any plane size (slabfft.cu): planes S
+// [c][n0l][n1][nh] (2-D cuFFT of the local planes) <-> k1 rows W
+// [c][n0][n1l][nh] (1-D cuFFT along axis 0). `dst[q]` is either a send chunk
+// (all-to-all layout [q][c][i0l][k1l][k2], `push` = 0) or peer q's own W / S
+// (`push` = 1: the transpose is stored straight into the peer over NVLink).
+struct SlabDims {
+  int c, n0, n0l, n1, n1l, nh, me, world;
+  __host__ __device__ int64_t chunk() const { return (int64_t)c * n0l * n1l * nh; }
+};
+void launch_slab_pack_fwd(const SlabDims& d, const double2* S, double2* const* dst, int push, cudaStream_t s);
+void launch_slab_unpack_fwd(const SlabDims& d, const double2* recv, double2* W, cudaStream_t s);
+void launch_slab_pack_inv(const SlabDims& d, const double2* W, double2* const* dst, int push, cudaStream_t s);
+void launch_slab_unpack_inv(const SlabDims& d, const double2* recv, double2* S, cudaStream_t s);
 
 // Fused three-pass preconditioner (fftfused.cu): 3-D grids with square
 // 128^2 / 256^2 planes. T has the cuFFT D2Z layout [c][n0][n1][n2/2+1].

@@ -59,12 +59,12 @@ __global__ void __launch_bounds__(kBlock) k_spectral(const __grid_constant__ Spe
 #pragma unroll
     for (int i = 0; i < C; ++i) r[i] = spec[i * nf + k];
     double2 z[C];
-    if (k == 0) {
+    int f[3];
+    freq_index<D>(p, k, f);
+    if (f[0] == 0 && f[1] == 0 && f[2] == 0) {  // zero frequency (a slab rank may not hold it)
 #pragma unroll
       for (int i = 0; i < C; ++i) z[i] = make_double2(0.0, 0.0);
     } else {
-      int f[3];
-      freq_index<D>(p, k, f);
       double M[3][3], K[3][3], I[3][3];
       gram<D>(p, f, M);
       symbol<D, C>(p, M, K);

@@ -13,8 +13,8 @@ __device__ __forceinline__ void freq_index(const SpecParams& p, int64_t k, int (
   if (D == 3) {
     f[2] = (int)(k % p.nh);
     const int64_t t = k / p.nh;
-    f[1] = (int)(t % p.n1);
-    f[0] = (int)(t / p.n1);
+    f[1] = p.k1off + (int)(t % p.n1r);
+    f[0] = (int)(t / p.n1r);
   } else {
     f[1] = (int)(k % p.nh);
     f[0] = (int)(k / p.nh);

@@ -20,7 +20,7 @@ def _rel(a, b):
     return float(np.linalg.norm(np.ravel(a) - np.ravel(b)) / np.linalg.norm(np.ravel(b)))
 
 
-@pytest.mark.parametrize("dims,c", [((64, 128, 128), 3), ((128, 128, 128), 1)])
+@pytest.mark.parametrize("dims,c", [((64, 128, 128), 3), ((128, 128, 128), 1), ((32, 64, 64), 3)])
 def test_slab_world1_matches_single_device(hb, dims, c):
     from paper_2203_02962_b200 import _native, dist, inputs
     ph, _ = inputs.rsa_balls(dims, radius=6.0, seed=3, fraction=0.25)
@@ -54,7 +54,10 @@ def test_slab_world1_matches_single_device(hb, dims, c):
 @pytest.mark.parametrize("world,dims,c,transport", [
     (2, (64, 128, 128), 3, "peer_pull"), (2, (128, 128, 128), 3, "peer_pull"), (4, (128, 128, 128), 1, "peer_pull"),
     (8, (128, 256, 256), 3, "peer_pull"), (2, (128, 128, 128), 3, "all_to_all"), (4, (128, 128, 128), 1, "all_to_all"),
-    (8, (128, 256, 256), 3, "all_to_all")])
+    (8, (128, 256, 256), 3, "all_to_all"),
+    # plane sizes outside the fused passes: slab spectra (cuFFT per rank + transposes, slabfft.cu)
+    (2, (32, 64, 64), 3, "peer_pull"), (2, (32, 64, 64), 3, "all_to_all"), (4, (64, 96, 96), 1, "peer_pull"),
+    (2, (16, 512, 512), 3, "peer_pull")])
 def test_slab_multi_rank_in_process_matches_single_device(hb, world, dims, c, transport, monkeypatch):
     """World > 1 on one GPU through the in-process transport (host barriers
     instead of NCCL; no device-side waiting between ranks): the halo ring (sent
@@ -120,4 +123,5 @@ def test_slab_multi_rank_in_process_matches_single_device(hb, world, dims, c, tr
         assert out["converged"]
         assert out["report"]["steps"][0]["cg_iterations"] == ref["report"]["steps"][0]["cg_iterations"]
         assert _rel(out["average_stress"], ref["average_stress"]) < 1e-12
-    assert _rel(uu, ref["u"]) < 1e-11
+    # 1e-10 (north_star): the slab spectra use 2-D + 1-D cuFFT plans instead of one 3-D plan
+    assert _rel(uu, ref["u"]) < 1e-10
