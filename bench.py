@@ -237,8 +237,27 @@ def run_gpu(args, rank, world, local_rank):
 
     hbm, peak_kind = peaks()
     c = cfg.components
-    bytes_k = (16 * c + 1) * (n_local if slab else g.num_pixels)
-    achieved = bytes_k / (ms[0] / 1e3) / 1e9
+    npx = n_local if slab else g.num_pixels
+    # dominant kernel of the iteration (largest live CUDA-event time) and its
+    # algorithmic bytes per launch
+    if fused_planes:
+        cands = [("k_hex_z" if cfg.stencil == "trilinear-hex" else "k_apply_elem", "stencil K apply",
+                  ms[0], (16 * c + 1) * npx),
+                 ("k_plane_fwd", "pass 1: r -= alpha Ap + plane r2c FFTs", ms[1], 32 * c * npx),
+                 ("k_pencil", "pass 2: axis-0 FFTs + spectral solve + r.z", ms[3], 16 * c * npx),
+                 ("k_plane_inv", "pass 3: plane c2r FFTs + x/p updates", ms[5], 40 * c * npx)]
+    else:
+        kname = {"trilinear-hex": "k_hex_z", "two-triangles": "k_elem2d"}.get(cfg.stencil, "k_apply_elem")
+        cands = [(kname, "stencil K apply", ms[0], (16 * c + 1) * npx)]
+    kname, kdesc, kms, bytes_k = max(cands, key=lambda t: t[2])
+    achieved = bytes_k / (kms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "r01_c3_ncu_traffic.json")
+    if os.path.exists(tp) and world == 1:
+        with open(tp) as f:
+            tj = json.load(f)
+        if list(tj.get("dims", [])) == list(cfg.dims):
+            traffic = tj["bytes_per_launch"].get(kname)
     # ideal fused iteration bytes per GPU: N_p (112 c + 1) / world
     b_iter = (112 * c + 1) * g.num_pixels / world
     iter_ms = cg_ms_max / max(iters, 1)
@@ -265,10 +284,11 @@ def run_gpu(args, rank, world, local_rank):
         "time_to_solution_s": wall_max / args.steps,
         "iteration_ms": iter_ms,
         "iteration_roofline_frac": (b_iter / (iter_ms / 1e3) / 1e9) / hbm,
-        "roofline": {"kernel": "stencil K apply (k_hex_fast)" if cfg.stencil == "trilinear-hex" else
-                     "stencil K apply (k_apply_elem)", "bound": "hbm", "achieved": achieved,
-                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": None,
-                     "peak_source": peak_kind, "bytes_per_launch": bytes_k},
+        "roofline": {"kernel": f"{kdesc} ({kname})", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
+                     "traffic_source": "profiles/r01_c3_ncu_traffic.json (ncu --set full, per launch)"
+                     if traffic else None,
+                     "peak_source": peak_kind, "bytes_per_launch": bytes_k, "kernel_ms": kms},
         "kernel_ms": ({"apply_K": ms[0], "update_r": ms[1], "fft_fwd": ms[2], "spectral": ms[3],
                        "fft_inv": ms[4], "update_xp": ms[5], "scalars": ms[6], "sum": ms[7]} if ms[2] >= 0 else
                       {"apply_K": ms[0], "pass1_r_update_plane_fft": ms[1], "pass2_pencil_fft_solve": ms[3],
