@@ -115,8 +115,11 @@ constexpr int rows_slots() {
   return 32 * P > 16 * (NP + 1) ? 32 * P : 16 * (NP + 1);
 }
 
+#ifndef HB_FWD_MINB
+#define HB_FWD_MINB 3  // 80 registers, no spill of note: 48 instead of 33 resident clusters
+#endif
 template <int NP>
-__global__ void __launch_bounds__(NP, 2) k_plane_fwd(const PlaneArgs a) {
+__global__ void __launch_bounds__(NP, HB_FWD_MINB) k_plane_fwd(const PlaneArgs a) {
   constexpr int P = NP / 2 + 1;
   constexpr int CL = NP / 32;
   constexpr int TPF = tpf<NP>();
