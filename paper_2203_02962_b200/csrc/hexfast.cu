@@ -357,6 +357,11 @@ constexpr int kZDepth = 3;
 #ifndef HB_HEXZ_KZ3
 #define HB_HEXZ_KZ3 8
 #endif
+// scalar z-block depth: 16, or 8 on small grids (fewer than ~8 element rows
+// per resident block at 16: warm-up rows dominate); HB_HEXZ_KZ1 forces one
+#ifndef HB_HEXZ_KZ1
+#define HB_HEXZ_KZ1 0
+#endif
 
 template <int C>
 __host__ __device__ constexpr int zslot_bytes(int nx) {
@@ -747,7 +752,9 @@ __global__ void __launch_bounds__(256) k_hex_quad(const HexQArgs a) {
 // z-block depth: bounded by the per-thread row buffer (KZ x C x nx doubles)
 static int hex_kz(const Grid& g) {
   if (g.n2 > 256) return g.c == 3 ? 4 : 8;  // 512-wide rows: one 512-thread block per SM
-  return g.c == 3 ? HB_HEXZ_KZ3 : 16;
+  if (g.c == 3) return HB_HEXZ_KZ3;
+  if (HB_HEXZ_KZ1) return HB_HEXZ_KZ1;
+  return ((int64_t)g.n1 * (g.n0 / 16) >= 2048 && g.n0 % 16 == 0) ? 16 : 8;
 }
 
 static bool hex_v2(const Grid& g) {
@@ -912,8 +919,13 @@ void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, boo
       if (iso) HB_HEXZ(3, true, HB_HEXZ_KZ3);
       else HB_HEXZ(3, false, HB_HEXZ_KZ3);
     } else {
-      if (iso) HB_HEXZ(1, true, 16);
-      else HB_HEXZ(1, false, 16);
+      if (hex_kz(g) == 16) {
+        if (iso) HB_HEXZ(1, true, 16);
+        else HB_HEXZ(1, false, 16);
+      } else {
+        if (iso) HB_HEXZ(1, true, 8);
+        else HB_HEXZ(1, false, 8);
+      }
     }
 #undef HB_HEXZ
     HB_CUDA(cudaGetLastError());
