@@ -664,8 +664,20 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     __shared__ double red[32];
     const int lane = tid & 31, warp = tid >> 5;
     constexpr int NWP = (NT + 31) / 32;
+    if constexpr (NT % 32 == 0) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) rz += __shfl_xor_sync(0xffffffffu, rz, o);
+      for (int o = 16; o > 0; o >>= 1) rz += __shfl_xor_sync(0xffffffffu, rz, o);
+    } else {
+      // the last warp is partial (NT = 48 for 64-plane elastic pencils): only
+      // existing lanes take part, lanes past the end contribute nothing
+      const int wn = min(32, NT - 32 * warp);
+      const unsigned mask = wn == 32 ? 0xffffffffu : ((1u << wn) - 1u);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double t = __shfl_down_sync(mask, rz, o);
+        if (lane + o < wn) rz += t;
+      }
+    }
     __syncthreads();
     if (lane == 0) red[warp] = rz;
     __syncthreads();
