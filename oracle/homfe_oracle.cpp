@@ -20,6 +20,13 @@
 //     Cholesky, Gauss-Jordan and cyclic Jacobi on the real 2n x 2n embedding
 //     of the Hermitian block.
 // Both replacements agree with the originals up to rounding only.
+//
+// Threads (or_set_threads, default 1): with 1 thread every loop runs in the
+// reference's order. With more, the same algorithm runs with OpenMP over
+// independent work (two-colour plane sweep of the fused operator, FFT lines,
+// frequencies, vector entries; std::thread): the reference itself is single-threaded
+// (homog.cpp:41-43); this variant only exists to time the reference
+// algorithm on every host core (bench.py --impl reference).
 
 #include "homfe_oracle.h"
 
@@ -35,6 +42,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -53,6 +61,23 @@ struct NonConvergence : std::runtime_error {
 };
 
 thread_local std::string g_last_error;
+int g_threads = 1;
+
+// f(lo, hi, worker) over [0, n) split into g_threads contiguous chunks (the
+// timing variant only; with one thread f(0, n, 0) runs on the caller).
+template <class F>
+void par_range(int64_t n, F&& f) {
+  const int nt = static_cast<int>(std::min<int64_t>(g_threads, std::max<int64_t>(n, 1)));
+  if (nt <= 1) {
+    f(int64_t(0), n, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(nt - 1);
+  for (int t = 1; t < nt; ++t) th.emplace_back([&, t] { f(n * t / nt, n * (t + 1) / nt, t); });
+  f(int64_t(0), n / nt, 0);
+  for (auto& x : th) x.join();
+}
 
 template <class F>
 int guarded(F&& f) {
@@ -346,6 +371,49 @@ void fused(const Layout& l, int c, const double* u, bool weighted, TangentAt&& t
   const int m = grad_components(l.d, c), nq = l.nq();
   const Index nn = l.num_nodes();
   std::fill(out, out + c * nn, 0.0);
+  if (g_threads > 1 && l.N[0] % 2 == 0 && l.N[0] >= 4) {
+    // threaded variant: the pixels of plane i0 scatter into node planes i0
+    // and i0 + 1 only, so the even planes and then the odd planes are
+    // independent sets
+    const Index per = l.np / l.N[0];
+    for (int colour = 0; colour < 2; ++colour) {
+      par_range(l.N[0] / 2, [&](Index lo, Index hi, int) {
+      for (Index i0 = 2 * lo + colour; i0 < 2 * hi; i0 += 2) {
+        Walker wt(l);
+        wt.coords[0] = i0;
+        double gt[6], tt[6];
+        for (Index p = i0 * per; p < (i0 + 1) * per; ++p) {
+          wt.neighbors();
+          for (int lq = 0; lq < nq; ++lq) {
+            const QuadSpec& q = l.quads[lq];
+            for (int k = 0; k < m; ++k) gt[k] = 0.0;
+            for (const Entry& e : q.entries) {
+              const Index node = static_cast<Index>(e.node) * l.np + wt.nbr[e.off];
+              double uv[3];
+              for (int k = 0; k < c; ++k) uv[k] = u[k * nn + node];
+              add_rows(l.d, c, e.dphi, uv, gt);
+            }
+            const double* cm = tan_at(p * nq + lq);
+            for (int i = 0; i < m; ++i) {
+              double acc = 0.0;
+              for (int j = 0; j < m; ++j) acc += cm[j * m + i] * gt[j];
+              tt[i] = acc;
+            }
+            const double wt_q = weighted ? q.w : 1.0;
+            for (const Entry& e : q.entries) {
+              const Index node = static_cast<Index>(e.node) * l.np + wt.nbr[e.off];
+              double acc[3] = {0.0, 0.0, 0.0};
+              adj_rows(l.d, c, e.dphi, tt, wt_q, acc);
+              for (int k = 0; k < c; ++k) out[k * nn + node] += acc[k];
+            }
+          }
+          wt.advance();
+        }
+      }
+      });
+    }
+    return;
+  }
   Walker w(l);
   double g[6], t[6];
   for (Index p = 0; p < l.np; ++p) {
@@ -533,6 +601,18 @@ struct FftGrid {
       Index stride = 1;
       for (int b = ax + 1; b < rank; ++b) stride *= dims[b];
       const Index outer = real_size / (n * stride);
+      if (g_threads > 1) {
+        par_range(outer * stride, [&](Index lo, Index hi, int) {
+          std::vector<cplx> ln(n), rs(n);
+          for (Index os = lo; os < hi; ++os) {
+            cplx* base = a.data() + (os / stride) * n * stride + os % stride;
+            for (Index i = 0; i < n; ++i) ln[i] = base[i * stride];
+            plans[ax].exec(ln.data(), rs.data(), inv);
+            for (Index i = 0; i < n; ++i) base[i * stride] = rs[i];
+          }
+        });
+        continue;
+      }
       line.resize(n);
       res.resize(n);
       for (Index o = 0; o < outer; ++o)
@@ -546,18 +626,23 @@ struct FftGrid {
   }
   void forward(const double* in, cplx* out) const {
     std::vector<cplx> a(real_size);
-    for (Index i = 0; i < real_size; ++i) a[i] = cplx(in[i], 0.0);
+    par_range(real_size, [&](Index lo, Index hi, int) {
+      for (Index i = lo; i < hi; ++i) a[i] = cplx(in[i], 0.0);
+    });
     c2c(a, false);
     const Index nl = dims.back(), sl = spec.back();
     const Index rows = real_size / nl;
-    for (Index r = 0; r < rows; ++r)
-      for (Index k = 0; k < sl; ++k) out[r * sl + k] = a[r * nl + k];
+    par_range(rows, [&](Index lo, Index hi, int) {
+      for (Index r = lo; r < hi; ++r)
+        for (Index k = 0; k < sl; ++k) out[r * sl + k] = a[r * nl + k];
+    });
   }
   void inverse(const cplx* in, double* out) const {
     std::vector<cplx> a(real_size);
     const Index nl = dims.back(), sl = spec.back();
-    Index idx[3] = {0, 0, 0};
-    for (Index f = 0; f < real_size; ++f) {
+    par_range(real_size, [&](Index lo, Index hi, int) {
+    for (Index f = lo; f < hi; ++f) {
+      Index idx[3] = {0, 0, 0};
       Index t = f;
       for (int ax = rank - 1; ax >= 0; --ax) { idx[ax] = t % dims[ax]; t /= dims[ax]; }
       if (idx[rank - 1] < sl) {
@@ -573,8 +658,11 @@ struct FftGrid {
         a[f] = std::conj(in[h]);
       }
     }
+    });
     c2c(a, true);
-    for (Index i = 0; i < real_size; ++i) out[i] = a[i].real();
+    par_range(real_size, [&](Index lo, Index hi, int) {
+      for (Index i = lo; i < hi; ++i) out[i] = a[i].real();
+    });
   }
   std::array<Index, 3> frequency(Index k) const {
     std::array<Index, 3> f{0, 0, 0};
@@ -764,8 +852,9 @@ void precond_apply(const Layout& l, const or_precond* b, const double* r, double
   const Index np = l.np, nf = b->nf;
   std::vector<cplx> spectra(nf * bdim);  // column s at s*nf
   for (int s = 0; s < bdim; ++s) b->fft->forward(r + static_cast<Index>(s) * np, spectra.data() + s * nf);
-  std::vector<cplx> rhs(bdim), sol(bdim);
-  for (Index k = 0; k < nf; ++k) {
+  par_range(nf, [&](Index lo, Index hi, int) {
+  for (Index k = lo; k < hi; ++k) {
+    cplx rhs[8], sol[8];
     for (int s = 0; s < bdim; ++s) rhs[s] = spectra[s * nf + k];
     const cplx* blk = b->block(k);
     for (int i = 0; i < bdim; ++i) {
@@ -775,9 +864,12 @@ void precond_apply(const Layout& l, const or_precond* b, const double* r, double
     }
     for (int s = 0; s < bdim; ++s) spectra[s * nf + k] = sol[s];
   }
+  });
   for (int s = 0; s < bdim; ++s) b->fft->inverse(spectra.data() + s * nf, out + static_cast<Index>(s) * np);
   const double sc = 1.0 / static_cast<double>(np);
-  for (Index i = 0; i < bdim * np; ++i) out[i] *= sc;
+  par_range(bdim * np, [&](Index lo, Index hi, int) {
+    for (Index i = lo; i < hi; ++i) out[i] *= sc;
+  });
 }
 
 // ----------------------------------------------------------------- fields
@@ -794,6 +886,16 @@ void remove_means(double* u, int c, Index nodes) {
 
 double dot(const double* a, const double* b, Index n) {
   double s = 0.0;
+  if (g_threads > 1) {
+    std::vector<double> part(g_threads, 0.0);
+    par_range(n, [&](Index lo, Index hi, int t) {
+      double acc = 0.0;
+      for (Index i = lo; i < hi; ++i) acc += a[i] * b[i];
+      part[t] = acc;
+    });
+    for (double v : part) s += v;
+    return s;
+  }
   for (Index i = 0; i < n; ++i) s += a[i] * b[i];
   return s;
 }
@@ -851,8 +953,10 @@ PcgOut pcg(const Op& apply_a, const Op& apply_minv, const double* b, Index n, in
     const double pap = dot(p.data(), ap.data(), n);
     if (pap <= 0.0) throw NumericalError("pcg: non-positive curvature, operator is not positive definite");
     const double alpha = rz / pap;
-    for (Index i = 0; i < n; ++i) x[i] += alpha * p[i];
-    for (Index i = 0; i < n; ++i) r[i] -= alpha * ap[i];
+    par_range(n, [&](Index lo, Index hi, int) {
+      for (Index i = lo; i < hi; ++i) x[i] += alpha * p[i];
+      for (Index i = lo; i < hi; ++i) r[i] -= alpha * ap[i];
+    });
     apply_minv(r.data(), z.data());
     const double rzn = std::max(dot(r.data(), z.data(), n), 0.0);
     out.iterations = k;
@@ -862,7 +966,9 @@ PcgOut pcg(const Op& apply_a, const Op& apply_minv, const double* b, Index n, in
       break;
     }
     const double beta = rzn / rz;
-    for (Index i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
+    par_range(n, [&](Index lo, Index hi, int) {
+      for (Index i = lo; i < hi; ++i) p[i] = z[i] + beta * p[i];
+    });
     rz = rzn;
   }
   remove_means(x, c, nodes);
@@ -1050,6 +1156,11 @@ int or_volume_average(const or_grid* g, int32_t m, const double* s, double* out)
 
 int or_weighted_dot(const or_grid* g, int32_t m, const double* a, const double* b, double* out) {
   return guarded([&] { *out = weighted_dot(make_layout(g), m, a, b); });
+}
+
+int or_set_threads(int32_t n) {
+  g_threads = n < 1 ? 1 : n;
+  return 0;
 }
 
 int or_uniform(uint64_t seed, int64_t n, double lo, double hi, double* out) {

@@ -166,6 +166,8 @@ int or_weighted_dot(const or_grid* g, int32_t m, const double* a, const double* 
 
 /* Deterministic RNG convention (tests/support/oracles.hpp:154-160):
    std::mt19937_64(seed), u = lo + (hi-lo)*(gen()>>11)*2^-53. */
+// Worker threads of the timing variant (1 = the reference's serial loop order).
+int or_set_threads(int32_t n);
 int or_uniform(uint64_t seed, int64_t n, double lo, double hi, double* out);
 
 #ifdef __cplusplus

@@ -470,3 +470,17 @@ def uniform(seed, n, lo=-1.0, hi=1.0):
     out = np.zeros(int(n))
     _check(lib().or_uniform(C.c_uint64(seed), C.c_int64(int(n)), C.c_double(lo), C.c_double(hi), _ptr(out)))
     return out
+
+
+def set_threads(n):
+    """Worker threads of the oracle's timing variant (1 = the reference's
+    serial loop order, the default; bench.py --impl reference uses all host
+    cores). Returns the previous setting."""
+    global _threads
+    prev = _threads
+    lib().or_set_threads(C.c_int32(int(n)))
+    _threads = int(n)
+    return prev
+
+
+_threads = 1

@@ -320,3 +320,25 @@ def test_thermal_bounds_match_support_sweep(oracle_mod, golden):
         bhi.append(max(kap[q] for q in sup))
     assert np.abs(lo - np.sort(blo)).max() < 1e-12
     assert np.abs(hi - np.sort(bhi)).max() < 1e-12
+
+
+def test_threaded_timing_variant_matches_serial(oracle_mod):
+    """The oracle's threaded variant (bench.py --impl reference on all host
+    cores) runs the same algorithm: equal to the serial loop order up to
+    summation order; the serial path is unchanged (bitwise repeatable)."""
+    dims = (16, 12, 10)
+    og = oracle_mod.Grid(dims, [1.0, 1.0, 1.0], "trilinear-hex")
+    cm = np.stack([oracle_mod.isotropic_stiffness(0.83, 0.38, 3), oracle_mod.isotropic_stiffness(55.5, 41.7, 3)])
+    ph = (oracle_mod.uniform(3, og.num_pixels, 0.0, 1.0) < 0.3).astype(np.uint8)
+    pre = oracle_mod.Preconditioner(og, cm[0], 3)
+    s = oracle_mod.uniform(4, og.num_quads * 6).reshape(og.num_quads, 6)
+    b = -oracle_mod.divergence(og, 3, s)
+    serial = oracle_mod.pcg(og, 3, cm, ph, pre, b, 0.0, 5)["x"]
+    prev = oracle_mod.set_threads(4)
+    try:
+        threaded = oracle_mod.pcg(og, 3, cm, ph, pre, b, 0.0, 5)["x"]
+    finally:
+        oracle_mod.set_threads(prev)
+    again = oracle_mod.pcg(og, 3, cm, ph, pre, b, 0.0, 5)["x"]
+    assert np.array_equal(serial, again)
+    assert np.linalg.norm(threaded - serial) <= 1e-12 * np.linalg.norm(serial)
