@@ -357,6 +357,11 @@ constexpr int kZDepth = 3;
 #ifndef HB_HEXZ_KZ3
 #define HB_HEXZ_KZ3 8
 #endif
+// z-block depth of 512-wide rows (one 512-thread block per SM; KZ = 8 at
+// c = 3 needs ~221 KB of shared memory)
+#ifndef HB_HEXZ_KZ512
+#define HB_HEXZ_KZ512 8
+#endif
 // scalar z-block depth: 16, or 8 on small grids (fewer than ~8 element rows
 // per resident block at 16: warm-up rows dominate); HB_HEXZ_KZ1 forces one
 #ifndef HB_HEXZ_KZ1
@@ -751,7 +756,7 @@ __global__ void __launch_bounds__(256) k_hex_quad(const HexQArgs a) {
 
 // z-block depth: bounded by the per-thread row buffer (KZ x C x nx doubles)
 static int hex_kz(const Grid& g) {
-  if (g.n2 > 256) return g.c == 3 ? 4 : 8;  // 512-wide rows: one 512-thread block per SM
+  if (g.n2 > 256) return g.c == 3 ? HB_HEXZ_KZ512 : 8;  // 512-wide rows: one 512-thread block per SM
   if (g.c == 3) return HB_HEXZ_KZ3;
   if (HB_HEXZ_KZ1) return HB_HEXZ_KZ1;
   return ((int64_t)g.n1 * (g.n0 / 16) >= 2048 && g.n0 % 16 == 0) ? 16 : 8;
@@ -881,7 +886,7 @@ static void launch_hex_z_nx(const Grid& g, const HexArgs& a, int n_phases, cudaS
 template <int C, bool ISO, int KZ, bool FE>
 static void launch_hex_z(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
   if (g.n2 == 512) {
-    launch_hex_z_nx<C, ISO, C == 3 ? 4 : 8, FE, 512>(g, a, n_phases, s);
+    launch_hex_z_nx<C, ISO, C == 3 ? HB_HEXZ_KZ512 : 8, FE, 512>(g, a, n_phases, s);
     return;
   }
   if (g.n2 == 256) launch_hex_z_nx<C, ISO, KZ, FE, 256>(g, a, n_phases, s);
