@@ -1772,6 +1772,7 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     p.w = ctx->sp.w[0];
     p.inv_np = 1.0 / (double)g.npg;
     for (int a = 0; a < 3; ++a) p.h[a] = g.h[a];
+    set_gram_factors(p);
     for (int a = 0; a < d; ++a) {
       const int nfull = a == 0 ? g.n0g : (a == 1 ? g.n1 : g.n2);
       const int len = a == d - 1 ? nh : nfull;

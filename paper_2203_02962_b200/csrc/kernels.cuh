@@ -135,7 +135,16 @@ struct SpecParams {
   double lam, mu;       // isotropic reference moduli (mu = kappa for c = 1)
   const double4* tab[3];  // per axis: (sin, cos, sin(t/2), cos(t/2))
   int n1r, k1off;         // 3-D: axis-1 rows held (n1, or a slab rank's n1/W) and the first one's k1
+  // division-free Gram factors (set_gram_factors): cd[a] = 8 w / h_a^2,
+  // co[a][b] = 4 w / (h_a h_b)
+  double cd[3], co[3][3];
 };
+inline void set_gram_factors(SpecParams& p) {
+  for (int a = 0; a < 3; ++a) {
+    p.cd[a] = 8.0 * p.w / (p.h[a] * p.h[a]);
+    for (int b = 0; b < 3; ++b) p.co[a][b] = 4.0 * p.w / (p.h[a] * p.h[b]);
+  }
+}
 void launch_spectral(const SpecParams& p, double2* spec, const PcgState* st, double* partials,
                      cudaStream_t s);
 

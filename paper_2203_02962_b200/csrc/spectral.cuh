@@ -10,6 +10,22 @@ namespace spec {
 
 template <int D>
 __device__ __forceinline__ void freq_index(const SpecParams& p, int64_t k, int (&f)[3]) {
+  if (p.nf < (int64_t(1) << 31)) {  // 32-bit index arithmetic (every single-GPU config)
+    const unsigned kk = (unsigned)k, nh = (unsigned)p.nh;
+    if (D == 3) {
+      const unsigned t = kk / nh, n1r = (unsigned)p.n1r;
+      f[2] = (int)(kk - t * nh);
+      const unsigned t0 = t / n1r;
+      f[1] = p.k1off + (int)(t - t0 * n1r);
+      f[0] = (int)t0;
+    } else {
+      const unsigned t = kk / nh;
+      f[1] = (int)(kk - t * nh);
+      f[0] = (int)t;
+      f[2] = 0;
+    }
+    return;
+  }
   if (D == 3) {
     f[2] = (int)(k % p.nh);
     const int64_t t = k / p.nh;
@@ -34,23 +50,23 @@ __device__ __forceinline__ void gram(const SpecParams& p, const int (&f)[3], dou
     ch[a] = t.w;
     S2[a] = 2.0 - (4.0 / 3.0) * sh[a] * sh[a];
   }
-  const double w = p.w;
+  // (host-precomputed factors: no divisions per frequency)
   if (p.kind == 3) {  // trilinear hex
-    M[0][0] = 8.0 * w * sh[0] * sh[0] / (p.h[0] * p.h[0]) * S2[1] * S2[2];
-    M[1][1] = 8.0 * w * sh[1] * sh[1] / (p.h[1] * p.h[1]) * S2[0] * S2[2];
-    M[2][2] = 8.0 * w * sh[2] * sh[2] / (p.h[2] * p.h[2]) * S2[0] * S2[1];
-    M[0][1] = M[1][0] = 4.0 * w * sn[0] * sn[1] / (p.h[0] * p.h[1]) * S2[2];
-    M[0][2] = M[2][0] = 4.0 * w * sn[0] * sn[2] / (p.h[0] * p.h[2]) * S2[1];
-    M[1][2] = M[2][1] = 4.0 * w * sn[1] * sn[2] / (p.h[1] * p.h[2]) * S2[0];
+    M[0][0] = p.cd[0] * sh[0] * sh[0] * S2[1] * S2[2];
+    M[1][1] = p.cd[1] * sh[1] * sh[1] * S2[0] * S2[2];
+    M[2][2] = p.cd[2] * sh[2] * sh[2] * S2[0] * S2[1];
+    M[0][1] = M[1][0] = p.co[0][1] * sn[0] * sn[1] * S2[2];
+    M[0][2] = M[2][0] = p.co[0][2] * sn[0] * sn[2] * S2[1];
+    M[1][2] = M[2][1] = p.co[1][2] * sn[1] * sn[2] * S2[0];
   } else if (p.kind == 0) {  // bilinear quad
-    M[0][0] = 8.0 * w * sh[0] * sh[0] / (p.h[0] * p.h[0]) * S2[1];
-    M[1][1] = 8.0 * w * sh[1] * sh[1] / (p.h[1] * p.h[1]) * S2[0];
-    M[0][1] = M[1][0] = 4.0 * w * sn[0] * sn[1] / (p.h[0] * p.h[1]);
+    M[0][0] = p.cd[0] * sh[0] * sh[0] * S2[1];
+    M[1][1] = p.cd[1] * sh[1] * sh[1] * S2[0];
+    M[0][1] = M[1][0] = p.co[0][1] * sn[0] * sn[1];
   } else {  // two triangles
     const double sd = sh[0] * ch[1] - ch[0] * sh[1];  // sin((t0 - t1)/2)
-    M[0][0] = 8.0 * w * sh[0] * sh[0] / (p.h[0] * p.h[0]);
-    M[1][1] = 8.0 * w * sh[1] * sh[1] / (p.h[1] * p.h[1]);
-    M[0][1] = M[1][0] = 4.0 * w * (sh[0] * sh[0] + sh[1] * sh[1] - sd * sd) / (p.h[0] * p.h[1]);
+    M[0][0] = p.cd[0] * sh[0] * sh[0];
+    M[1][1] = p.cd[1] * sh[1] * sh[1];
+    M[0][1] = M[1][0] = p.co[0][1] * (sh[0] * sh[0] + sh[1] * sh[1] - sd * sd);
   }
 }
 
