@@ -261,6 +261,21 @@ def run_gpu(args, rank, world, local_rank):
     # ideal fused iteration bytes per GPU: N_p (112 c + 1) / world
     b_iter = (112 * c + 1) * g.num_pixels / world
     iter_ms = cg_ms_max / max(iters, 1)
+    nvlink = None
+    if slab:
+        # algorithmic interconnect bytes per iteration and GPU:
+        # two halo planes of p for K, and the forward and inverse spectrum
+        # transposes ((G-1)/G of the rank's c N_f / G complex values each)
+        nh = g.dims[-1] // 2 + 1
+        nf = int(np.prod(g.dims[:-1])) * nh
+        halo = 2 * c * g.dims[1] * g.dims[2] * 8 if world > 1 else 0
+        a2a = 2 * c * 16 * (nf / world) * (world - 1) / world
+        nbytes = halo + a2a
+        nv_peak = 900.0  # GB/s per direction, NVLink 5 (B200 datasheet)
+        floor_ms = max(b_iter / hbm / 1e6, nbytes / nv_peak / 1e6)
+        nvlink = {"bytes_per_iteration_per_gpu": nbytes, "halo_bytes": halo, "transpose_bytes": a2a,
+                  "peak_gbs": nv_peak, "peak_source": "NVLink 5 nominal, per direction",
+                  "hbm_nvlink_roofline_ms": floor_ms, "frac": floor_ms / iter_ms}
     out = {
         "metric": "DOF·PCG-iterations/s",
         "value": value,
@@ -297,6 +312,7 @@ def run_gpu(args, rank, world, local_rank):
                 "h2d_bytes_per_step": int(world * (ph_host.nbytes + cm.nbytes + e.nbytes)),
                 "d2h_bytes_per_step": int(world * (u_host.nbytes + avg.nbytes)), "steps": e2e_steps},
         "clocks": clocks,
+        **({"interconnect": nvlink} if nvlink else {}),
         "gpu_launches": int(launches),
         "input_generation_s": t_inputs,
     }
