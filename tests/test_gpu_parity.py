@@ -451,3 +451,43 @@ def test_cpp_drop_in_j2_example_runs(hb):
         r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.count("converged 1") == 3, r.stdout
+
+
+@pytest.mark.parametrize("dims,stencil,c", [((2, 2), "two-triangles", 1), ((2, 5), "two-triangles", 2),
+                                            ((3, 4), "bilinear-quad", 2), ((6, 5), "bilinear-quad", 1),
+                                            ((2, 3), "four-triangles-two-node", 2),
+                                            ((2, 2, 2), "trilinear-hex", 3), ((2, 3, 4), "trilinear-hex", 1),
+                                            ((5, 2, 3), "trilinear-hex", 3), ((3, 6, 2), "trilinear-hex", 1)])
+def test_tiny_grids_match_oracle(hb, oracle_mod, dims, stencil, c):
+    """Axis lengths 2-6 as in the reference's preconditioner tests
+    (test_precond.cpp:34-43): with n = 2 the +1 and -1 neighbours coincide.
+    K (1e-12), M^-1 (1e-10) and a tolerance-mode PCG (|dk| <= 1) against the
+    oracle, unequal cell lengths."""
+    lengths = [1.0 + 0.15 * a for a in range(len(dims))]
+    g = hb.Grid(dims, lengths, stencil)
+    og = oracle_mod.Grid(dims, lengths, stencil)
+    cm = _two_phase_iso(hb, g.dim, c, 20.0)
+    ph = (np.arange(g.num_pixels) % 3 == 1).astype(np.uint8)
+    u = oracle_mod.uniform(41, c * g.num_nodes).reshape(c, -1)
+    ref = oracle_mod.apply_phase(og, c, cm, ph, u)
+    got = hb.apply_operator(g, cm[np.repeat(ph, g.quads_per_pixel)], u).ravel()
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    c_ref = cm[0]
+    pre = hb.assemble_preconditioner(g, c_ref, c)
+    r = oracle_mod.uniform(43, c * g.num_nodes).reshape(c, -1)
+    r -= r.mean(axis=1, keepdims=True)
+    opre = oracle_mod.Preconditioner(og, c_ref, c)
+    z = hb.apply_preconditioner(g, pre, r)
+    zo = opre.apply(r.ravel())
+    assert np.abs(z.ravel() - zo).max() < 1e-10 * max(1.0, np.abs(zo).max())
+    m = cm.shape[1]
+    s = oracle_mod.uniform(47, g.num_quads * m).reshape(g.num_quads, m)
+    b = -oracle_mod.divergence(og, c, s)
+    if np.abs(b).max() < 1e-12:
+        return
+    tol = oracle_mod.pcg(og, c, cm, ph, opre, b, 1e-10, 500)
+    mats = [hb.Material(t, c == 1, g.dim) for t in cm]
+    gpu = hb.pcg_solve(g, mats, ph, pre, b.reshape(c, -1), 1e-10, 500)
+    assert tol["converged"] and gpu["converged"]
+    assert abs(gpu["iterations"] - tol["iterations"]) <= 1
+    assert _rel(gpu["x"], tol["x"]) <= 1e-8
