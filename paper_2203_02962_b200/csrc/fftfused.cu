@@ -144,50 +144,80 @@ __global__ void __launch_bounds__(NP, HB_FWD_MINB) k_plane_fwd(const PlaneArgs a
   }
   __syncthreads();
   const bool noio = a.dbg & 128;  // profiling: no r / Ap traffic
-  if (tid == 0) {
+  // PCG mode: r and Ap go straight from HBM into the row-FFT register layout
+  // (thread t of group g: columns t + TPF i of rows 2g, 2g+1; each group
+  // reads 2 x 128-byte row segments per step), r - alpha Ap is written back
+  // from registers and fed to the FFT: no shared-memory staging of the rows
+  // (measured: 128^2 planes 0.031 -> 0.026 ms; 256^2 planes 0.468 -> 0.505 ms,
+  // there the TMA-staged rows win: HB_FWD_REGLOAD = largest plane size using it)
+#ifndef HB_FWD_REGLOAD
+#define HB_FWD_REGLOAD 128
+#endif
+  const bool regload = NP <= HB_FWD_REGLOAD && pcg && !noio;
+  if (tid == 0 && !regload) {
     fft::mbar_expect_tx(&bar, noio ? 0 : 32 * ROWB);
     if (!noio)
       for (int y = 0; y < 32; ++y) fft::bulk_g2s(rows + y * P, a.r + plane + (int64_t)y * NP, ROWB, &bar);
   }
   for (int i = tid; i < NP; i += NP) tws[i] = a.tw[i];
-  double2 apv[PT];
-  if (pcg && !noio) {
-    const double2* ap2 = reinterpret_cast<const double2*>(a.ap + plane);
-#pragma unroll
-    for (int i = 0; i < PT; ++i) apv[i] = ap2[tid + i * NP];
-  }
-  fft::mbar_wait(&bar, 0);
-  if (pcg && !noio) {
+  double2 vr[16];  // row pair values in the FFT register layout
+  if (regload) {
     const double alpha = a.st->alpha;
+    double* ra = a.r + plane + (int64_t)(2 * g) * NP;
+    double* rb = ra + NP;
+    const double* pa = a.ap + plane + (int64_t)(2 * g) * NP;
+    const double* pb = pa + NP;
 #pragma unroll
-    for (int i = 0; i < PT; ++i) {
-      const int idx = tid + i * NP, row = idx / H, c2 = idx % H;
-      double2 v = rows[row * P + c2];
-      v.x = fma(-alpha, apv[i].x, v.x);
-      v.y = fma(-alpha, apv[i].y, v.y);
-      rows[row * P + c2] = v;
+    for (int i = 0; i < 16; ++i) {
+      const int n = t + i * TPF;
+      double x0 = ra[n], x1 = rb[n];
+      x0 = fma(-alpha, __ldg(pa + n), x0);
+      x1 = fma(-alpha, __ldg(pb + n), x1);
+      ra[n] = x0;
+      rb[n] = x1;
+      vr[i] = make_double2(x0, x1);
     }
-    __syncthreads();
-    // r written back by TMA bulk stores (async proxy: no generic stores left
-    // in flight at the cluster barriers below)
-    if (tid == 0 && !noio) {
-      fft::fence_proxy_async();
-      for (int y = 0; y < 32; ++y) fft::bulk_s2g(a.r + plane + (int64_t)y * NP, rows + y * P, ROWB);
-      fft::bulk_commit();
-      fft::bulk_wait_read();
+  } else {
+    double2 apv[PT];
+    if (pcg && !noio) {
+      const double2* ap2 = reinterpret_cast<const double2*>(a.ap + plane);
+#pragma unroll
+      for (int i = 0; i < PT; ++i) apv[i] = ap2[tid + i * NP];
+    }
+    fft::mbar_wait(&bar, 0);
+    if (pcg && !noio) {
+      const double alpha = a.st->alpha;
+#pragma unroll
+      for (int i = 0; i < PT; ++i) {
+        const int idx = tid + i * NP, row = idx / H, c2 = idx % H;
+        double2 w = rows[row * P + c2];
+        w.x = fma(-alpha, apv[i].x, w.x);
+        w.y = fma(-alpha, apv[i].y, w.y);
+        rows[row * P + c2] = w;
+      }
+      __syncthreads();
+      // r written back by TMA bulk stores (async proxy: no generic stores left
+      // in flight at the cluster barriers below)
+      if (tid == 0) {
+        fft::fence_proxy_async();
+        for (int y = 0; y < 32; ++y) fft::bulk_s2g(a.r + plane + (int64_t)y * NP, rows + y * P, ROWB);
+        fft::bulk_commit();
+        fft::bulk_wait_read();
+      }
     }
   }
   __syncthreads();
   // row r2c: group g transforms the row pair (2g, 2g+1) in place
   if (!(a.dbg & 1)) {
     double2* buf = rows + (2 * g) * P;
-    const double* xa = reinterpret_cast<const double*>(rows + (2 * g) * P);
-    const double* xb = reinterpret_cast<const double*>(rows + (2 * g + 1) * P);
-    double2 v[16];
+    if (!regload) {
+      const double* xa = reinterpret_cast<const double*>(rows + (2 * g) * P);
+      const double* xb = reinterpret_cast<const double*>(rows + (2 * g + 1) * P);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = make_double2(xa[t + i * TPF], xb[t + i * TPF]);
+      for (int i = 0; i < 16; ++i) vr[i] = make_double2(xa[t + i * TPF], xb[t + i * TPF]);
+    }
     fft::group_sync();
-    fft::fft4step_regs<NP, false>(v, buf, t, tws);
+    fft::fft4step_regs<NP, false>(vr, buf, t, tws);
     constexpr int KN = (P + TPF - 1) / TPF;
     double2 za[KN], zb[KN];
 #pragma unroll
