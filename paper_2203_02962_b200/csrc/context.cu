@@ -1104,8 +1104,6 @@ void newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* a
     reduce_to_host(c, 1, &bz);
     const double bnorm = std::sqrt(std::max(0.0, bz));
     if (step == 0) bnorm0 = bnorm;
-    const double strain_scale = quad_norm(c, c->d_u, c->d_e);
-    const bool b_is_zero = bnorm == 0.0 || quad_norm(c, c->d_z, nullptr) <= 1e-12 * strain_scale;
     const bool residual_ok = bnorm <= cfg->eta_newton * bnorm0;
     const bool increment_ok = have_inc && inc_rel <= cfg->eta_newton;
     if (step > 0 && (increment_ok || residual_ok)) {
@@ -1118,6 +1116,10 @@ void newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* a
       rep->converged = 0;
       break;
     }
+    // zero-RHS test (only needed when the step is taken: the two strain norms
+    // are not computed for the final convergence check)
+    const double strain_scale = quad_norm(c, c->d_u, c->d_e);
+    const bool b_is_zero = bnorm == 0.0 || quad_norm(c, c->d_z, nullptr) <= 1e-12 * strain_scale;
     t0 = Clock::now();
     PcgResult pr;
     if (b_is_zero) {
