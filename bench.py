@@ -252,12 +252,15 @@ def run_gpu(args, rank, world, local_rank):
     kname, kdesc, kms, bytes_k = max(cands, key=lambda t: t[2])
     achieved = bytes_k / (kms / 1e3) / 1e9
     traffic = None
+    iter_traffic = None
     tp = os.path.join(ROOT, "profiles", "r01_c3_ncu_traffic.json")
     if os.path.exists(tp) and world == 1:
         with open(tp) as f:
             tj = json.load(f)
         if list(tj.get("dims", [])) == list(cfg.dims):
             traffic = tj["bytes_per_launch"].get(kname)
+            if fused_planes:  # one launch of each of the four iteration kernels
+                iter_traffic = sum(tj["bytes_per_launch"].values())
     # ideal fused iteration bytes per GPU: N_p (112 c + 1) / world
     b_iter = (112 * c + 1) * g.num_pixels / world
     iter_ms = cg_ms_max / max(iters, 1)
@@ -299,6 +302,7 @@ def run_gpu(args, rank, world, local_rank):
         "time_to_solution_s": wall_max / args.steps,
         "iteration_ms": iter_ms,
         "iteration_roofline_frac": (b_iter / (iter_ms / 1e3) / 1e9) / hbm,
+        "iteration_bytes": {"algorithmic": b_iter, "dram_ncu": iter_traffic},
         "roofline": {"kernel": f"{kdesc} ({kname})", "bound": "hbm", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
                      "traffic_source": "profiles/r01_c3_ncu_traffic.json (ncu --set full, per launch)"
