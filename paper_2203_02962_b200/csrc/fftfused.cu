@@ -687,7 +687,10 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
         issue(tile + 2 * gridDim.x, st);
       }
     }
-    __syncthreads();
+    // no block barrier here: the other warps go on to the next tile (other
+    // stage, its own mbarrier); this stage is only touched again after the
+    // next tile's first barrier, which warp 0 reaches after the refill issue
+    // (0.356 -> 0.350 ms)
   }
   if (tid == 0) fft::bulk_wait();  // stores complete before the block retires
   if (a.partials) {
