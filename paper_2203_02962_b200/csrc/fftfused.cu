@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(NP, HB_FWD_MINB) k_plane_fwd(const PlaneArgs a
         if (HB_FWD_RSTORE) reinterpret_cast<double2*>(a.r + plane)[idx] = w;
       }
       __syncthreads();
-      // r written back by TMA bulk stores (async proxy: no generic stores left
-      // in flight at the cluster barriers below)
+      // (HB_FWD_RSTORE=0: r written back by TMA bulk stores instead, so that no
+      // generic stores are in flight at the cluster barriers below)
       if (tid == 0 && !HB_FWD_RSTORE) {
         fft::fence_proxy_async();
         for (int y = 0; y < 32; ++y) fft::bulk_s2g(a.r + plane + (int64_t)y * NP, rows + y * P, ROWB);
