@@ -107,3 +107,24 @@ def test_cpp_shim_compiles_and_links(tmp_path):
                     os.path.join(ROOT, "examples", "solve_j2.cpp"), "-o", str(out2), "-L", lib_dir, "-lhomfe_gpu",
                     f"-Wl,-rpath,{lib_dir}"], check=True)
     assert out2.exists()
+
+
+def test_no_cpu_fallback_without_device_or_library(tmp_path):
+    """The product path fails loudly: without the library the package does not
+    import, and without a CUDA device every compute call raises DeviceError
+    (no silent CPU path)."""
+    import subprocess
+    import sys
+    env = dict(os.environ, HOMFE_LIB=str(tmp_path / "missing.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2203_02962_b200"], cwd=ROOT, env=env,
+                       capture_output=True, text=True)
+    out = r.stderr + r.stdout
+    assert r.returncode != 0 and ("libhomfe_gpu" in out or "missing.so" in out), out[-500:]
+    import torch
+    if torch.cuda.is_available():
+        return
+    import numpy as np
+    import paper_2203_02962_b200 as hb
+    g = hb.Grid((8, 8), [1.0, 1.0], "two-triangles")
+    with pytest.raises(hb.DeviceError):
+        hb.apply_operator(g, np.stack([np.eye(2)] * g.num_quads), np.zeros((1, g.num_nodes)))
