@@ -44,6 +44,20 @@ def _compile(src, verbose, obj_dir=None, defines=()):
     return obj, r.stderr
 
 
+def _nccl_link():
+    """Link the NCCL that PyTorch bundles when it is installed (same soname
+    libnccl.so.2 as the system one): whichever of torch and this library loads
+    first, the process then holds one NCCL that satisfies both (torch needs
+    symbols the older system NCCL lacks)."""
+    import glob
+    for base in sys.path:
+        hits = glob.glob(os.path.join(base, "nvidia", "nccl", "lib", "libnccl.so.2"))
+        if hits:
+            d = os.path.dirname(hits[0])
+            return ["-L" + d, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{d}"]
+    return ["-lnccl"]
+
+
 def build(verbose=False, force=False, lib=None, defines=()):
     """Compile and link. `lib`/`defines` build a tuning variant elsewhere."""
     lib = lib or LIB
@@ -61,7 +75,7 @@ def build(verbose=False, force=False, lib=None, defines=()):
             if log:
                 print(f"--- ptxas {s}\n{log}", file=sys.stderr)
     if _stale(lib, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcufft", "-lnccl",
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcufft", *_nccl_link(),
                "-Xlinker", f"-rpath,{CUDA}/lib64"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
