@@ -109,6 +109,12 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def workload_config(args, cfg):
+    """The `config` object both arms print (the driver compares them)."""
+    return {"workload": WORKLOADS[args.config], "dims": list(cfg.dims), "dof": int(cfg.dof),
+            "stencil": cfg.stencil, "eta_cg": cfg.eta_cg}
+
+
 def setup_problem(cfg):
     import paper_2203_02962_b200 as hb
     t0 = time.time()
@@ -235,6 +241,38 @@ def run_gpu(args, rank, world, local_rank):
         solver.ctx._material_key = None
     e2e_value = dof * e2e_iters / e2e_wall
 
+    slab_check = None
+    if slab:
+        # self-check of the decomposed solve (outside every timed region): the
+        # slabs of u from the last e2e solve are gathered and compared on rank
+        # 0 with a single-device solve of the same input
+        u_loc = torch.from_numpy(np.array(u_host, copy=True)).cuda()
+        if world > 1:
+            parts = torch.empty(world * u_loc.numel(), dtype=torch.float64, device="cuda")
+            torch.distributed.all_gather_into_tensor(parts, u_loc)
+        else:
+            parts = u_loc
+        k_slab = int(rep.total_cg)
+        if rank == 0:
+            c = cfg.components
+            u_slab = parts.view(world, c, -1).transpose(0, 1).reshape(c, -1).cpu().numpy()
+            del parts, u_loc
+            one = hb.Solver(g, mats, phases, eta_newton=cfg.eta_newton, eta_cg=cfg.eta_cg,
+                            reference=cfg.reference, reference_matrix=cfg.reference_matrix())
+            ref1 = one.solve(e)
+            k1 = int(ref1["report"]["cg_total"])
+            u1 = ref1["u"]
+            slab_check = {"against": "single-device solve of the same input on rank 0",
+                          "pcg_iterations": {"slab": k_slab, "single": k1},
+                          "rel_u": float(np.linalg.norm(u_slab - u1) / np.linalg.norm(u1)),
+                          "rel_sigma": float(np.linalg.norm(avg - ref1["average_stress"]) /
+                                             np.linalg.norm(ref1["average_stress"])),
+                          "u_checksum": {"slab": float(np.abs(u_slab).sum()), "single": float(np.abs(u1).sum())}}
+            slab_check["ok"] = bool(abs(k_slab - k1) <= 1 and slab_check["rel_sigma"] <= 1e-8)
+            del one
+        if world > 1:
+            torch.distributed.barrier()
+
     hbm, peak_kind = peaks()
     c = cfg.components
     npx = n_local if slab else g.num_pixels
@@ -292,13 +330,14 @@ def run_gpu(args, rank, world, local_rank):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic: seeded RSA inclusions / GRF per SURVEY 8(d) (no dataset in the reference)",
-        "config": {"workload": WORKLOADS[args.config], "dims": list(cfg.dims), "dof": dof,
-                   "pcg_iterations_per_step": iters // args.steps, "newton_steps": rep.n_steps,
-                   "parallelism": (f"slab decomposition over {world} GPUs ({transport}, "
-                                   f"{'fused FFT passes' if fused_planes else 'slab spectra: cuFFT + transposes'})")
-                   if slab else "1 GPU",
-                   "l2": f"inputs exceed L2: {cfg.components * g.num_pixels * 8 / 1e6:.0f} MB per vector vs 126 MB"
-                   if cfg.components * g.num_pixels * 8 > 126e6 else "L2-resident working set (no flush)"},
+        "config": workload_config(args, cfg),
+        "solve": {"pcg_iterations_per_step": iters // args.steps, "newton_steps": rep.n_steps,
+                  "parallelism": (f"slab decomposition over {world} GPUs ({transport}, "
+                                  f"{'fused FFT passes' if fused_planes else 'slab spectra: cuFFT + transposes'})")
+                  if slab else "1 GPU",
+                  "l2": f"inputs exceed L2: {cfg.components * g.num_pixels * 8 / 1e6:.0f} MB per vector vs 126 MB"
+                  if cfg.components * g.num_pixels * 8 > 126e6 else "L2-resident working set (no flush)",
+                  "step": "one linear solve to eta_cg (Newton linear branch + PCG), inputs resident in HBM"},
         "time_to_solution_s": wall_max / args.steps,
         "iteration_ms": iter_ms,
         "iteration_roofline_frac": (b_iter / (iter_ms / 1e3) / 1e9) / hbm,
@@ -317,80 +356,126 @@ def run_gpu(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(world * (u_host.nbytes + avg.nbytes)), "steps": e2e_steps},
         "clocks": clocks,
         **({"interconnect": nvlink} if nvlink else {}),
+        **({"slab_check": slab_check} if slab_check else {}),
         "gpu_launches": int(launches),
         "input_generation_s": t_inputs,
     }
     return out
 
 
-def cpu_baseline(args, sample_n=64, iters=6, threads=1):
-    """The oracle (faithful single-thread restatement of the reference) on a
-    bounded sample of the same workload: same recipe at sample_n^3, PCG
-    iterations timed with steady_clock-equivalent perf_counter, assembly
-    excluded. threads > 1: the oracle's threaded timing variant (same
-    algorithm, work split over host cores; the reference is single-threaded)."""
+def cpu_workload(args):
+    """The configuration's inputs for the CPU arms WITHOUT the product library:
+    inputs.py is loaded by path (no package import, so libhomfe_gpu.so is
+    never mapped) with the oracle's or_uniform as its RNG (the same
+    std::mt19937_64 stream, so the phase map is byte-identical to the GPU
+    arm's)."""
+    import importlib.util
     from oracle import oracle
+    name = "homfe_inputs_cpu"
+    if name not in sys.modules:
+        spec = importlib.util.spec_from_file_location(name, os.path.join(ROOT, "paper_2203_02962_b200", "inputs.py"))
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules[name] = mod
+        spec.loader.exec_module(mod)
+        mod.set_uniform_source(oracle.uniform_source())
+    mod = sys.modules[name]
+    cfg = mod.config(args.config, n=args.n, contrast=args.contrast)
+    return cfg, cfg.phases(), cfg.tangents()
+
+
+def oracle_pcg_sample(cfg, ph, tans, warm, timed, threads, pre_cache={}):
+    """The reference algorithm (oracle: impulse-probed blocks, PCG of
+    solver.cpp:50-97, phase-indexed tangent) on the configuration itself from
+    its Newton right-hand side; returns the steady_clock seconds of each of
+    the `timed` iterations after `warm` untimed ones. Assembly excluded (it is
+    setup, once per solve, in the reference too)."""
+    from oracle import oracle
+    from oracle.cfgutil import newton_rhs
     oracle.set_threads(threads)
-    from paper_2203_02962_b200 import inputs
-    cfg = inputs.config(args.config, n=sample_n) if args.config in ("c3", "c4") else inputs.config(args.config)
-    if args.config == "c5":
-        cfg = inputs.config("c5", n=256, contrast=args.contrast)
-    if args.config == "c2":
-        cfg = inputs.config("c2")
-    phases = cfg.phases()
-    tangents = cfg.tangents()
-    og = oracle.Grid(cfg.dims, [1.0] * cfg.dim, cfg.stencil)
     c = cfg.components
-    m = tangents.shape[1]
-    cref = cfg.reference_matrix()
-    if cref is None:
-        cref = (np.bincount(phases, minlength=len(tangents))[:, None, None] * tangents).sum(0) / phases.size
-    pre = oracle.Preconditioner(og, cref, c)
-    s = oracle.uniform(1, og.num_quads * m).reshape(og.num_quads, m)
-    b = -oracle.divergence(og, c, s)
-    t0 = time.perf_counter()
-    oracle.pcg(og, c, tangents, phases, pre, b, 0.0, iters)
-    dt = time.perf_counter() - t0
+    key = (tuple(cfg.dims), cfg.stencil, c)
+    if key not in pre_cache:
+        pre_cache.clear()
+        og = oracle.Grid(cfg.dims, [1.0] * cfg.dim, cfg.stencil)
+        if cfg.reference == "explicit":
+            cref = tans[cfg.reference_phase]
+        else:
+            f = np.bincount(ph, minlength=len(tans)).astype(float) / ph.size
+            cref = np.einsum("p,pij->ij", f, tans)
+        t0 = time.perf_counter()
+        pre = oracle.Preconditioner(og, cref, c)
+        b = newton_rhs(cfg.dims, [1.0] * cfg.dim, c, tans, ph, cfg.load)
+        pre_cache[key] = (og, pre, b, time.perf_counter() - t0)
+    og, pre, b, t_setup = pre_cache[key]
+    _, t = oracle.pcg_timed(og, c, tans, ph, pre, b, warm + timed)
     oracle.set_threads(1)
-    how = ("single thread as the reference (homog.cpp:41-43)" if threads == 1 else
-           f"{threads} host threads (two-colour plane sweep of the fused operator, FFT lines, "
-           f"frequencies and vector entries split over the cores; the reference itself is single-threaded)")
-    return {"value": cfg.dof * iters / dt, "unit": "DOF*it/s", "cores": threads, "kind": "port",
-            "sample": f"{args.config} recipe at {'x'.join(map(str, cfg.dims))} ({cfg.dof} DOF), {iters} PCG "
-                      f"iterations of the oracle (per-quad loop order, own FFT), assembly excluded, {how}",
-            "seconds": dt}
+    return t[warm:], t_setup
+
+
+def host_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def cpu_baseline(args, cpu_inputs=None):
+    """cpu_baseline of the GPU arm's line: the reference algorithm (oracle)
+    on the box's host cores, on a bounded sample of the same workload: the
+    configuration itself, 2 PCG iterations after 1 warm-up."""
+    cfg, ph, tans = cpu_inputs or cpu_workload(args)
+    threads = host_threads()
+    t, t_setup = oracle_pcg_sample(cfg, ph, tans, 1, 2, threads)
+    return {"value": cfg.dof * len(t) / float(t.sum()), "unit": "DOF*it/s", "cores": threads, "kind": "port",
+            "sample": f"{args.config} at {'x'.join(map(str, cfg.dims))} ({cfg.dof} DOF), the configuration itself: "
+                      f"{len(t)} PCG iterations (after 1 warm-up) of the oracle restatement of the reference "
+                      f"(probed blocks, per-quad loop order, own FFT) from the Newton RHS on {threads} host threads; "
+                      f"assembly ({t_setup:.1f} s) excluded",
+            "seconds": float(t.sum())}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU path (oracle port; the reference
-    itself cannot be built here: Eigen3/FFTW3/vendor missing)."""
+    """--impl reference: the reference's CPU path on the box's host cores.
+    The reference itself cannot be built here (Eigen3, FFTW3 and vendor/
+    are absent), so the oracle restatement of its algorithm runs: threaded
+    timing variant on every core this process may use, on the configuration
+    itself (same config object as the GPU arm); one step = one PCG iteration
+    of that configuration (a full solve is 155 iterations of ~4 s). The
+    single-core figure (the reference is single-threaded by design,
+    homog.cpp:41-43) is measured beside it on one pinned core."""
     if rank != 0:
         return None
-    # every host core this process may run on (the reference is single-
-    # threaded by design; the oracle's threaded variant times its algorithm
-    # on all of them)
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    sample_n = 128 if threads > 16 else 64
-    samples = []
-    for _ in range(args.warmup):
-        cpu_baseline(args, sample_n=sample_n, iters=2, threads=threads)
-    t_total = 0.0
-    dof_it = 0.0
-    for _ in range(args.steps):
-        r = cpu_baseline(args, sample_n=sample_n, iters=3, threads=threads)
-        t_total += r["seconds"]
-        dof_it += r["value"] * r["seconds"]
-        samples.append(r)
-    value = dof_it / t_total
+    cfg, ph, tans = cpu_workload(args)
+    threads = host_threads()
+    t, t_setup = oracle_pcg_sample(cfg, ph, tans, args.warmup, args.steps, threads)
+    value = cfg.dof * len(t) / float(t.sum())
+    # single core, pinned (taskset -c <first allowed core> equivalent)
+    single = None
+    if not args.no_single_core:
+        aff = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else None
+        try:
+            if aff:
+                os.sched_setaffinity(0, {aff[0]})
+            t1, _ = oracle_pcg_sample(cfg, ph, tans, 0, 1, 1)
+        finally:
+            if aff:
+                os.sched_setaffinity(0, set(aff))
+        single = {"value": cfg.dof / float(t1[0]), "unit": "DOF*it/s", "cores": 1,
+                  "sample": "1 PCG iteration of the same configuration, serial oracle (reference loop order), "
+                            "pinned to one core", "seconds": float(t1[0])}
+    sample = (f"{args.config} at {'x'.join(map(str, cfg.dims))} ({cfg.dof} DOF), the configuration itself: "
+              f"{args.steps} timed PCG iterations after {args.warmup} warm-up, oracle restatement of the reference "
+              f"(probed blocks, phase-indexed tangent, own FFT) from the Newton RHS, {threads} host threads "
+              f"(two-colour plane sweep of the fused operator, FFT lines, frequencies and vector entries split "
+              f"over the cores); assembly {t_setup:.1f} s excluded")
     return {"metric": "DOF·PCG-iterations/s", "value": value, "unit": "DOF*it/s", "impl": "reference",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (SURVEY 8(d))",
-            "config": {"workload": WORKLOADS[args.config]},
-            "cpu_baseline": {"value": value, "unit": "DOF*it/s", "cores": threads, "kind": "port",
-                             "sample": samples[-1]["sample"]},
+            "ms_per_step": float(t.sum()) / len(t) * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic: seeded RSA inclusions / GRF per SURVEY 8(d)",
+            "config": workload_config(args, cfg),
+            "cpu_baseline": {"value": value, "unit": "DOF*it/s", "cores": threads, "kind": "port", "sample": sample},
+            "single_core": single,
             "e2e": {"value": value, "unit": "DOF*it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "note": "reference not buildable in this image (Eigen3, FFTW3, vendor/ absent); CPU oracle port timed"}
+            "step": "one PCG iteration of the configuration (K apply, update, M^-1 with two FFT sweeps, dots)",
+            "note": "reference not buildable in this image (Eigen3, FFTW3, vendor/ absent); its algorithm is "
+                    "timed through the oracle restatement, with no product library loaded in this process"}
 
 
 def _emit(out):
@@ -416,10 +501,22 @@ def main():
     ap.add_argument("--contrast", type=float, default=None)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-single-core", action="store_true", help="--impl reference: skip the 1-core figure")
     ap.add_argument("--slab", action="store_true", help="use the slab (multi-GPU) context even at N=1")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        r = subprocess.run(cmd, stdout=_JSON_FD)
+        sys.exit(r.returncode)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

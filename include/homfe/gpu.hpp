@@ -92,7 +92,11 @@ class GridLayout {
   StencilKind kind() const { return kind_; }
   int dim() const { return cell_.dim(); }
   Index num_pixels() const { return cell_.pixel_count(); }
-  Index num_nodes() const { return num_pixels(); }
+  // grid.hpp:96-110: node types per pixel (FourTrianglesTwoNode adds the
+  // pixel-centre node), nodes = Nn * N_p
+  int nodes_per_pixel() const { return kind_ == StencilKind::FourTrianglesTwoNode ? 2 : 1; }
+  Index num_nodes() const { return num_pixels() * nodes_per_pixel(); }
+  Index num_quads() const { return num_pixels() * quads_per_pixel(); }
   // grid.cpp:114-229: 1 (BilinearQuad here: 4), 2, 4, 8 Gauss points per pixel
   int quads_per_pixel() const {
     switch (kind_) {

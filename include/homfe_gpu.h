@@ -40,7 +40,7 @@ extern "C" {
 /* StencilKind, in the order of proj/include/homfe/grid.hpp:30-35. */
 #define HOMFE_BILINEAR_QUAD 0
 #define HOMFE_TWO_TRIANGLES 1
-#define HOMFE_FOUR_TRIANGLES_TWO_NODE 2 /* not supported on the GPU path */
+#define HOMFE_FOUR_TRIANGLES_TWO_NODE 2 /* probed complex blocks (probe.cu) */
 #define HOMFE_TRILINEAR_HEX 3
 
 /* ReferencePolicy::Kind (proj/include/homfe/solver.hpp:82-101). */
@@ -129,7 +129,14 @@ int homfe_gpu_set_material(homfe_ctx* ctx, int32_t n_phases, const double* tange
 int homfe_gpu_set_material_device(homfe_ctx* ctx, int32_t n_phases, const double* tangents,
                                   const uint8_t* d_phase);
 
-/* newton_solve (solver.hpp:163-166) for linear materials: macroscopic load
+/* The context plays the caller's PrecondManager (solver.hpp:105-129): the
+   assembled reference, the volume-averaged tangent at the last assembly and
+   the drift rule persist across solves (load steps share one manager,
+   solver.cpp:306-318). homfe_gpu_precond_reset starts a new manager. */
+int homfe_gpu_precond_reset(homfe_ctx* ctx);
+
+/* newton_solve (solver.hpp:163-166) for linear materials (J2 catalogs and
+   two-node stencils run the general branch from a zero state): macroscopic load
    e (m), config, optional warm start u (c * num_nodes); outputs the periodic
    fluctuation u, the homogenized stress <sigma> (m) and the report. */
 int homfe_gpu_solve(homfe_ctx* ctx, const double* e, const homfe_solve_cfg* cfg,
@@ -205,6 +212,20 @@ int homfe_gpu_pcg(homfe_ctx* ctx, const double* b, double eta, int32_t it_max, d
    table nbr[p * n_offsets + o] (grid.cpp:267-288, operators.cpp:65-84),
    computed on the device. */
 int homfe_gpu_index_maps(homfe_ctx* ctx, int64_t* strides3, int64_t* nbr, int32_t* n_offsets);
+
+/* Which kernels the context runs (no reference counterpart; lets parity
+   tests assert that they exercise the path the benchmark times). Bits:
+   fused three-pass FFT preconditioner (fftfused.cu), modal hex K (hexfast.cu),
+   conditional-WHILE PCG graph, slab spectra (slabfft.cu), slab context,
+   peer-pull transport, 2-D warp-strip K (quad2d.cu). */
+#define HOMFE_PATH_FUSED_FFT 1
+#define HOMFE_PATH_HEX_MODAL 2
+#define HOMFE_PATH_WHILE_GRAPH 4
+#define HOMFE_PATH_SLAB_SPECTRA 8
+#define HOMFE_PATH_SLAB 16
+#define HOMFE_PATH_PEER_PULL 32
+#define HOMFE_PATH_ELEM2D 64
+int homfe_gpu_path_info(const homfe_ctx* ctx, int32_t* flags);
 
 /* Per-stage CUDA-event timing of one PCG iteration on the current buffers
    (call after a solve): ms[0..7] = K apply, x/r update, forward FFT, spectral

@@ -685,10 +685,20 @@ void jacobi_sym(std::vector<double> a, int n, std::vector<double>& lam, std::vec
       for (int j = 0; j < n; ++j) if (i != j) off += A(i, j) * A(i, j);
     }
     if (off <= 1e-34 * diag || off == 0.0) break;
+    int rotations = 0;
     for (int p = 0; p < n - 1; ++p)
       for (int q = p + 1; q < n; ++q) {
         const double apq = A(p, q);
         if (apq == 0.0) continue;
+        // below rounding of the diagonal: annihilate without a rotation
+        // (otherwise rounding can hold `off` just above the sweep test
+        // above and the loop runs all 100 sweeps)
+        if (std::abs(apq) <= 1e-18 * std::sqrt(std::abs(A(p, p) * A(q, q)))) {
+          A(p, q) = 0.0;
+          A(q, p) = 0.0;
+          continue;
+        }
+        ++rotations;
         const double theta = (A(q, q) - A(p, p)) / (2.0 * apq);
         const double t = (theta >= 0 ? 1.0 : -1.0) / (std::abs(theta) + std::sqrt(theta * theta + 1.0));
         const double cs = 1.0 / std::sqrt(t * t + 1.0), sn = t * cs;
@@ -708,6 +718,7 @@ void jacobi_sym(std::vector<double> a, int n, std::vector<double>& lam, std::vec
           v[q * n + k] = sn * vkp + cs * vkq;
         }
       }
+    if (rotations == 0) break;
   }
   lam.resize(n);
   for (int i = 0; i < n; ++i) lam[i] = A(i, i);
@@ -801,6 +812,172 @@ or_precond* assemble(const Layout& l, const double* c_ref, int c, bool weighted)
   return out;
 }
 
+// Exact symbol of the reference operator (TEST INFRASTRUCTURE, not a
+// restatement of a reference function). The reference obtains K_ref_hat(xi)
+// by probing: K_ref applied to an impulse, then an FFT of the response
+// (precond.cpp:44-85). Both steps round in fp64; at low frequencies the block
+// is O(theta^2) while the response entries are O(1), so its relative rounding
+// is ~eps/theta^2. Here the same quantity is evaluated in long double
+// (64-bit mantissa) from the stencil tables of grid.cpp (restated with long
+// double Gauss points) and the Mandel rows of operators.cpp:16-53:
+//   S_delta = sum_q w_q sum_{a,b : o_a - o_b = delta} B_a^T C_ref B_b,
+//   K_hat(xi)[row][col] = sum_delta S_delta[row][col] exp(-i xi . delta),
+// with xi_a = 2 pi f_a / N_a (f the non-negative FFT index, fft.cpp:71-79),
+// evaluated separably (last axis first). The result is exact to fp64
+// rounding at every frequency, so a PCG with it isolates the GPU's own
+// rounding from the reference's probing floor.
+using LD = long double;
+struct LEntry { int off; LD dphi[3]; };
+struct LQuad { LD w; std::vector<LEntry> e; };
+
+std::vector<LQuad> exact_quads(const Layout& l, bool weighted) {
+  std::vector<LQuad> qs;
+  LD h[3] = {1, 1, 1}, vp = 1;
+  for (int a = 0; a < l.d; ++a) { h[a] = (LD)l.L[a] / (LD)l.N[a]; vp *= h[a]; }
+  const LD gq = 0.5L / sqrtl(3.0L);
+  const LD gp[2] = {0.5L - gq, 0.5L + gq};
+  if (l.kind == OR_TWO_TRIANGLES) {
+    qs.push_back({vp / 2, {{0, {-1 / h[0], -1 / h[1], 0}}, {1, {1 / h[0], 0, 0}}, {2, {0, 1 / h[1], 0}}}});
+    qs.push_back({vp / 2, {{3, {1 / h[0], 1 / h[1], 0}}, {2, {-1 / h[0], 0, 0}}, {1, {0, -1 / h[1], 0}}}});
+  } else if (l.kind == OR_BILINEAR_QUAD) {
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) {
+        LQuad q{vp / 4, {}};
+        const LD xi[2] = {1 - gp[i], gp[i]}, dxi[2] = {-1 / h[0], 1 / h[0]};
+        const LD et[2] = {1 - gp[j], gp[j]}, det[2] = {-1 / h[1], 1 / h[1]};
+        for (int a = 0; a < 2; ++a)
+          for (int b = 0; b < 2; ++b) q.e.push_back({a + 2 * b, {dxi[a] * et[b], xi[a] * det[b], 0}});
+        qs.push_back(q);
+      }
+  } else if (l.kind == OR_TRILINEAR_HEX) {
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j)
+        for (int k = 0; k < 2; ++k) {
+          LQuad q{vp / 8, {}};
+          const LD xi[2] = {1 - gp[i], gp[i]}, dxi[2] = {-1 / h[0], 1 / h[0]};
+          const LD et[2] = {1 - gp[j], gp[j]}, det[2] = {-1 / h[1], 1 / h[1]};
+          const LD ze[2] = {1 - gp[k], gp[k]}, dze[2] = {-1 / h[2], 1 / h[2]};
+          for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b)
+              for (int c = 0; c < 2; ++c)
+                q.e.push_back({(a * 2 + b) * 2 + c,
+                               {dxi[a] * et[b] * ze[c], xi[a] * det[b] * ze[c], xi[a] * et[b] * dze[c]}});
+          qs.push_back(q);
+        }
+  } else {
+    throw ValidationError("exact symbol: one-node stencils only");
+  }
+  if (!weighted)
+    for (auto& q : qs) q.w = 1;
+  return qs;
+}
+
+// Mandel gradient rows of one node as an m x c matrix (operators.cpp:16-32).
+void exact_rows(int d, int c, const LD* dp, LD* B) {
+  const int m = grad_components(d, c);
+  for (int i = 0; i < m * c; ++i) B[i] = 0;
+  const LD s = sqrtl(2.0L) / 2;
+  if (c == 1) {
+    for (int a = 0; a < d; ++a) B[a] = dp[a];
+  } else if (d == 2) {
+    B[0 * 2 + 0] = dp[0];
+    B[1 * 2 + 1] = dp[1];
+    B[2 * 2 + 0] = s * dp[1];
+    B[2 * 2 + 1] = s * dp[0];
+  } else {
+    B[0 * 3 + 0] = dp[0];
+    B[1 * 3 + 1] = dp[1];
+    B[2 * 3 + 2] = dp[2];
+    B[3 * 3 + 1] = s * dp[2];
+    B[3 * 3 + 2] = s * dp[1];
+    B[4 * 3 + 0] = s * dp[2];
+    B[4 * 3 + 2] = s * dp[0];
+    B[5 * 3 + 0] = s * dp[1];
+    B[5 * 3 + 1] = s * dp[0];
+  }
+}
+
+or_precond* assemble_exact(const Layout& l, const double* c_ref, int c, bool weighted) {
+  if (c != 1 && c != l.d) throw ValidationError("assemble_reference: bad component count");
+  if (l.Nn != 1) throw ValidationError("exact symbol: one-node stencils only");
+  const int m = grad_components(l.d, c);
+  check_spd(c_ref, m, "reference tangent");
+  const int D = l.d;
+  int nd = 1;
+  for (int a = 0; a < D; ++a) nd *= 3;
+  // S[delta][row][col], delta id = sum_a (delta_a + 1) 3^(D-1-a)
+  std::vector<LD> S(nd * c * c, 0);
+  std::vector<LD> Ba(m * c), Bb(m * c), CB(m * c);
+  for (const auto& q : exact_quads(l, weighted))
+    for (const auto& ea : q.e)
+      for (const auto& eb : q.e) {
+        exact_rows(D, c, ea.dphi, Ba.data());
+        exact_rows(D, c, eb.dphi, Bb.data());
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < c; ++j) {
+            LD acc = 0;
+            for (int k = 0; k < m; ++k) acc += (LD)c_ref[k * m + i] * Bb[k * c + j];  // col-major C
+            CB[i * c + j] = acc;
+          }
+        int id = 0;
+        for (int a = 0; a < D; ++a) id = id * 3 + (int)(l.offsets[ea.off][a] - l.offsets[eb.off][a]) + 1;
+        for (int r = 0; r < c; ++r)
+          for (int cc = 0; cc < c; ++cc) {
+            LD acc = 0;
+            for (int k = 0; k < m; ++k) acc += Ba[k * c + r] * CB[k * c + cc];
+            S[(id * c + r) * c + cc] += q.w * acc;
+          }
+      }
+  auto* out = new or_precond();
+  out->c = c;
+  out->Nn = 1;
+  out->bdim = c;
+  out->weighted = weighted;
+  std::vector<Index> dims(l.N, l.N + D);
+  out->fft = std::make_shared<FftGrid>(dims);
+  out->nf = out->fft->spec_size;
+  out->data.assign(out->nf * c * c, 0.0);
+  const LD two_pi = 6.283185307179586476925286766559L;
+  auto phase = [&](int a, Index f, int delta) {  // exp(-i 2 pi f delta / N_a)
+    const LD t = -two_pi * (LD)((f * delta) % l.N[a]) / (LD)l.N[a];
+    return std::complex<LD>(cosl(t), sinl(t));
+  };
+  // last axis first: T[outer delta id][f_last][row][col]
+  const Index sl = out->fft->spec.back();
+  const int no = nd / 3;
+  std::vector<std::complex<LD>> T(no * sl * c * c);
+  for (int o = 0; o < no; ++o)
+    for (Index f = 0; f < sl; ++f)
+      for (int e = 0; e < c * c; ++e) {
+        std::complex<LD> acc = 0;
+        for (int dl = -1; dl <= 1; ++dl) acc += S[(o * 3 + dl + 1) * c * c + e] * phase(D - 1, f, dl);
+        T[(o * sl + f) * c * c + e] = acc;
+      }
+  const Index rows = out->nf / sl;
+  par_range(rows, [&](Index lo, Index hi, int) {
+    std::vector<std::complex<LD>> ph(no);
+    for (Index rw = lo; rw < hi; ++rw) {
+      Index fo[2] = {0, 0};
+      if (D == 3) { fo[0] = rw / out->fft->spec[1]; fo[1] = rw % out->fft->spec[1]; }
+      else fo[0] = rw;
+      for (int o = 0; o < no; ++o) {
+        if (D == 3) ph[o] = phase(0, fo[0], o / 3 - 1) * phase(1, fo[1], o % 3 - 1);
+        else ph[o] = phase(0, fo[0], o - 1);
+      }
+      for (Index f = 0; f < sl; ++f) {
+        cplx* blk = out->block(rw * sl + f);
+        for (int r = 0; r < c; ++r)
+          for (int cc = 0; cc < c; ++cc) {
+            std::complex<LD> acc = 0;
+            for (int o = 0; o < no; ++o) acc += ph[o] * T[(o * sl + f) * c * c + r * c + cc];
+            blk[cc * c + r] = cplx((double)acc.real(), (double)acc.imag());
+          }
+      }
+    }
+  });
+  return out;
+}
+
 // Zero frequency: (B0 + V V^T)^-1 - V V^T; others: V diag(1/lambda) V^H with
 // the 1e-12 singularity test (precond.cpp:87-124).
 void invert(or_precond* b) {
@@ -818,17 +995,20 @@ void invert(or_precond* b) {
     inverse_gj(tmp.data(), n, b0);
     for (int i = 0; i < n * n; ++i) b0[i] -= vvt[i];
   }
+  // Blocks are independent: with or_set_threads > 1 they are split over the
+  // host threads (each block's arithmetic is unchanged); the first singular
+  // block in frequency order is reported, as in the serial loop.
+  std::vector<Index> bad(std::max(g_threads, 1), -1);
+  par_range(b->nf - 1, [&](Index lo0, Index hi0, int worker) {
   std::vector<double> lam, v;
-  for (Index k = 1; k < b->nf; ++k) {
+  for (Index k = lo0 + 1; k < hi0 + 1; ++k) {
     cplx* blk = b->block(k);
     jacobi_sym(embed(blk, n), 2 * n, lam, v);
     double lmax = 0.0, lmin = std::numeric_limits<double>::infinity();
     for (double x : lam) { lmax = std::max(lmax, std::abs(x)); lmin = std::min(lmin, x); }
     if (lmin <= 1e-12 * lmax) {
-      const auto f = b->fft->frequency(k);
-      throw NumericalError("invert_blocks: singular non-zero-frequency block at (" +
-                           std::to_string(f[0]) + "," + std::to_string(f[1]) + "," +
-                           std::to_string(f[2]) + ")");
+      bad[worker] = k;
+      return;
     }
     // Real inverse of the embedding, then read back Re / Im blocks.
     const int N2 = 2 * n;
@@ -842,6 +1022,14 @@ void invert(or_precond* b) {
         blk[j * n + i] = cplx(re, im);
       }
   }
+  });
+  for (Index k : bad)
+    if (k >= 0) {
+      const auto f = b->fft->frequency(k);
+      throw NumericalError("invert_blocks: singular non-zero-frequency block at (" +
+                           std::to_string(f[0]) + "," + std::to_string(f[1]) + "," +
+                           std::to_string(f[2]) + ")");
+    }
   b->inverted = true;
 }
 
@@ -935,8 +1123,9 @@ using Op = std::function<void(const double*, double*)>;
 
 // solver.cpp:50-97.
 PcgOut pcg(const Op& apply_a, const Op& apply_minv, const double* b, Index n, int c,
-           Index nodes, double eta, int it_max, double* x) {
+           Index nodes, double eta, int it_max, double* x, double* iter_seconds = nullptr) {
   PcgOut out;
+  auto t_it = std::chrono::steady_clock::now();
   std::fill(x, x + n, 0.0);
   std::vector<double> r(b, b + n), z(n), p(n), ap(n);
   apply_minv(r.data(), z.data());
@@ -970,6 +1159,11 @@ PcgOut pcg(const Op& apply_a, const Op& apply_minv, const double* b, Index n, in
       for (Index i = lo; i < hi; ++i) p[i] = z[i] + beta * p[i];
     });
     rz = rzn;
+    if (iter_seconds) {  // timing only (bench.py): steady_clock as solver.cpp:14-18
+      const auto now = std::chrono::steady_clock::now();
+      iter_seconds[k - 1] = std::chrono::duration<double>(now - t_it).count();
+      t_it = now;
+    }
   }
   remove_means(x, c, nodes);
   return out;
@@ -1091,6 +1285,21 @@ int or_precond_assemble(const or_grid* g, const double* c_ref, int32_t c, int32_
   });
 }
 
+int or_precond_exact(const or_grid* g, const double* c_ref, int32_t c, int32_t weighted, int32_t do_invert,
+                     or_precond** out) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    or_precond* p = assemble_exact(l, c_ref, c, weighted != 0);
+    try {
+      if (do_invert) invert(p);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *out = p;
+  });
+}
+
 int or_precond_from_symbol(const or_grid* g, int32_t c, const double* blocks_rm, int32_t weighted,
                            or_precond** out) {
   return guarded([&] {
@@ -1147,6 +1356,17 @@ int or_pcg(const or_grid* g, int32_t c, int32_t n_phases, const double* cmat,
     if (iterations) *iterations = o.iterations;
     if (converged) *converged = o.converged ? 1 : 0;
     if (history) std::copy(o.history.begin(), o.history.end(), history);
+  });
+}
+
+int or_pcg_timed(const or_grid* g, int32_t c, int32_t n_phases, const double* cmat, const uint8_t* phase,
+                 const or_precond* p, const double* b, int32_t it_max, double* x, double* iter_seconds) {
+  return guarded([&] {
+    const Layout l = make_layout(g);
+    const Index nodes = l.num_nodes(), n = c * nodes;
+    Op A = [&](const double* v, double* out) { apply_phase(l, c, n_phases, cmat, phase, v, true, out); };
+    Op M = [&](const double* v, double* out) { precond_apply(l, p, v, out); };
+    pcg(A, M, b, n, c, nodes, 0.0, it_max, x, iter_seconds);
   });
 }
 
@@ -1436,9 +1656,45 @@ int or_j2_evaluate(int32_t d, double bulk, double shear, double yield_stress, do
   });
 }
 
+
+// PrecondManager (solver.hpp:105-129): shared by the load steps of a program
+// (solver.cpp:306-318).
+struct or_manager {
+  std::unique_ptr<or_precond> minv;
+  std::vector<double> c_ref_used, mean_at_assembly;
+  int assemblies = 0;
+};
+
+namespace {
+int newton_models(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
+                  const uint8_t* phase, const double* g0_in, const double* e, const or_solve_cfg* cfg,
+                  const double* warm_u, double* u_out, double* g_out, double* avg_out, or_report* rep,
+                  or_manager* mgr);
+}  // namespace
+
+or_manager* or_manager_create(void) { return new or_manager(); }
+void or_manager_destroy(or_manager* m) { delete m; }
+int or_manager_assemblies(const or_manager* m) { return m ? m->assemblies : 0; }
+
 int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
                            const uint8_t* phase, const double* g0_in, const double* e, const or_solve_cfg* cfg,
                            const double* warm_u, double* u_out, double* g_out, double* avg_out, or_report* rep) {
+  return newton_models(g, thermal, n_phases, models, phase, g0_in, e, cfg, warm_u, u_out, g_out, avg_out, rep,
+                       nullptr);
+}
+
+int or_newton_solve_managed(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
+                            const uint8_t* phase, const double* g0_in, const double* e, const or_solve_cfg* cfg,
+                            const double* warm_u, double* u_out, double* g_out, double* avg_out, or_report* rep,
+                            or_manager* mgr) {
+  return newton_models(g, thermal, n_phases, models, phase, g0_in, e, cfg, warm_u, u_out, g_out, avg_out, rep, mgr);
+}
+
+namespace {
+int newton_models(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
+                  const uint8_t* phase, const double* g0_in, const double* e, const or_solve_cfg* cfg,
+                  const double* warm_u, double* u_out, double* g_out, double* avg_out, or_report* rep,
+                  or_manager* mgr_in) {
   return guarded([&] {
     const auto t_total = Clock::now();
     const Layout l = make_layout(g);
@@ -1518,9 +1774,13 @@ int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, 
       for (double v : a) s2 += v * v;
       return std::sqrt(s2);
     };
-    // PrecondManager state (solver.cpp:120-142)
-    std::unique_ptr<or_precond> minv;
-    std::vector<double> c_ref_used, mean_at_assembly, mean;
+    // PrecondManager state (solver.cpp:120-142): the caller's, or one for this solve
+    or_manager local_mgr;
+    or_manager& mgr = mgr_in ? *mgr_in : local_mgr;
+    std::unique_ptr<or_precond>& minv = mgr.minv;
+    std::vector<double>& c_ref_used = mgr.c_ref_used;
+    std::vector<double>& mean_at_assembly = mgr.mean_at_assembly;
+    std::vector<double> mean;
 
     double bnorm0 = 0.0, inc_rel = std::numeric_limits<double>::infinity();
     bool have_inc = false;
@@ -1562,6 +1822,7 @@ int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, 
           mean_at_assembly = mean;
           reassembled = true;
           rep->assemblies += 1;
+          mgr.assemblies += 1;
         }
       }
       rep->seconds_assembly += since(t0);
@@ -1639,6 +1900,7 @@ int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, 
     if (!rep->converged) throw NonConvergence(rep->cause == 1 ? "cg-stall" : "newton-cap");
   });
 }
+}  // namespace
 
 
 // ------------------------------------------------- strain-based scheme (f4)

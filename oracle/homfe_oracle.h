@@ -96,6 +96,11 @@ int or_fft_inverse(int32_t rank, const int64_t* dims, const double* in_c, double
 typedef struct or_precond or_precond;
 int or_precond_assemble(const or_grid* g, const double* c_ref, int32_t c,
                         int32_t weighted, int32_t invert, or_precond** out);
+/* Same blocks from the exact symbol of the reference operator, evaluated in
+   long double (one-node stencils): no impulse-probing rounding. Test
+   infrastructure for the noise-floor protocol of SURVEY 8(c) item 5. */
+int or_precond_exact(const or_grid* g, const double* c_ref, int32_t c, int32_t weighted, int32_t invert,
+                     or_precond** out);
 /* Preconditioner from a given symbol (nf x bdim x bdim complex, row-major per
    block), inverted like invert_blocks: used to separate the reference's own
    impulse-probing rounding from implementation differences in parity tests. */
@@ -112,6 +117,13 @@ int or_pcg(const or_grid* g, int32_t c, int32_t n_phases, const double* cmat,
            const uint8_t* phase, const or_precond* p, const double* b, double eta,
            int32_t it_max, double* x, int32_t* iterations, double* history,
            int32_t* converged);
+
+/* Timing variant (bench.py CPU arms): fixed it_max iterations (eta = 0),
+   iter_seconds[k-1] = steady_clock duration of iteration k (K apply, update,
+   M^-1, dot, direction update). */
+int or_pcg_timed(const or_grid* g, int32_t c, int32_t n_phases, const double* cmat,
+                 const uint8_t* phase, const or_precond* p, const double* b, int32_t it_max,
+                 double* x, double* iter_seconds);
 
 /* Linear Newton solve (solver.cpp:171-296) for a phase-indexed linear catalog.
    thermal=1: c=1, m=d; else c=d, m=mandel_dim(d). */
@@ -143,6 +155,18 @@ int or_newton_solve_models(const or_grid* g, int32_t thermal, int32_t n_phases, 
                            const uint8_t* phase, const double* g0, const double* e, const or_solve_cfg* cfg,
                            const double* warm_u, double* u_out, double* g_out, double* avg_stress_out,
                            or_report* report);
+
+/* PrecondManager (solver.hpp:105-129) shared across load steps: the same
+   Newton solve with the caller's manager (assembly, C_ref and the tangent
+   mean at the last assembly persist, solver.cpp:306-318). */
+typedef struct or_manager or_manager;
+or_manager* or_manager_create(void);
+void or_manager_destroy(or_manager* m);
+int or_manager_assemblies(const or_manager* m);
+int or_newton_solve_managed(const or_grid* g, int32_t thermal, int32_t n_phases, const or_material* models,
+                            const uint8_t* phase, const double* g0, const double* e, const or_solve_cfg* cfg,
+                            const double* warm_u, double* u_out, double* g_out, double* avg_stress_out,
+                            or_report* report, or_manager* manager);
 
 /* Strain-based scheme (projection.cpp): gamma_apply with the
    unweighted reference blocks (projection.cpp:22-41), and the SB Newton

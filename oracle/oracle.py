@@ -227,9 +227,16 @@ def fft_inverse(X, shape):
 class Preconditioner:
     """Impulse-probed, FFT-diagonalised, pseudo-inverted reference operator."""
 
-    def __init__(self, g, c_ref, c, weighted=True, invert=True, symbol=None):
+    def __init__(self, g, c_ref, c, weighted=True, invert=True, symbol=None, exact=False):
+        """exact=True: blocks from the long-double exact symbol
+        (or_precond_exact) instead of the reference's impulse probing."""
         h = C.c_void_p()
-        if symbol is not None:
+        if exact:
+            m = g.m(c)
+            cr = _cmat(c_ref, m)
+            _check(lib().or_precond_exact(g.ref, _ptr(cr), C.c_int32(c), C.c_int32(int(weighted)),
+                                          C.c_int32(int(invert)), C.byref(h)))
+        elif symbol is not None:
             sym = np.ascontiguousarray(symbol, dtype=np.complex128)
             _check(lib().or_precond_from_symbol(g.ref, C.c_int32(c), _ptr(sym.view(np.float64)),
                                                 C.c_int32(int(weighted)), C.byref(h)))
@@ -276,6 +283,28 @@ def pcg(g, c, cmats, phase, precond, b, eta, it_max):
                         precond._h, _ptr(b), C.c_double(eta), C.c_int32(it_max), _ptr(x),
                         C.byref(it), _ptr(hist), C.byref(conv)))
     return dict(x=x, iterations=it.value, history=hist[: it.value + 1], converged=bool(conv.value))
+
+
+def pcg_timed(g, c, cmats, phase, precond, b, iterations):
+    """Fixed-iteration PCG returning (x, per-iteration seconds) (timing only)."""
+    m = g.m(c)
+    cm = _cmat(cmats, m)
+    ph = np.ascontiguousarray(phase, dtype=np.uint8).ravel()
+    b = _f64(b).ravel()
+    x = np.zeros_like(b)
+    t = np.zeros(iterations)
+    _check(lib().or_pcg_timed(g.ref, C.c_int32(c), C.c_int32(cm.size // (m * m)), _ptr(cm), _ptr(ph, C.c_uint8),
+                              precond._h, _ptr(b), C.c_int32(iterations), _ptr(x), _ptr(t)))
+    return x, t
+
+
+def uniform_source():
+    """The oracle's or_uniform as a C function pointer with argtypes (same
+    stream as the product's homfe_random_uniform)."""
+    fn = lib().or_uniform
+    fn.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, C.POINTER(C.c_double)]
+    fn.restype = C.c_int
+    return fn
 
 
 POLICIES = {"identity": 0, "identity-scaled": 0, "volume-mean": 1, "explicit": 2}
@@ -350,10 +379,32 @@ def j2_evaluate(d, bulk, shear, yield_stress, hardening, eps, g):
     return sig, tan.reshape(m, m).T.copy(), gn
 
 
+class PrecondManager:
+    """PrecondManager (solver.hpp:105-129) shared by the steps of a load
+    program (solver.cpp:306-318)."""
+
+    def __init__(self):
+        lib().or_manager_create.restype = C.c_void_p
+        self._h = C.c_void_p(lib().or_manager_create())
+
+    def __del__(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().or_manager_destroy.argtypes = [C.c_void_p]
+            lib().or_manager_destroy.restype = None
+            lib().or_manager_destroy(self._h)
+            self._h = None
+
+    @property
+    def assemblies(self):
+        lib().or_manager_assemblies.argtypes = [C.c_void_p]
+        return lib().or_manager_assemblies(self._h)
+
+
 def newton_solve_models(g, thermal, models, phase, e, g0=None, eta_newton=1e-5, eta_cg=1e-5, max_newton=25,
                         max_cg=20000, reassembly_threshold=0.1, criterion="strain", reference="volume-mean",
-                        reference_scale=1.0, reference_matrix=None, warm_u=None):
-    """Newton solve for a general (linear + J2) catalog with internal state."""
+                        reference_scale=1.0, reference_matrix=None, warm_u=None, manager=None):
+    """Newton solve for a general (linear + J2) catalog with internal state;
+    `manager`: a PrecondManager kept across calls (None: one per solve)."""
     d = g.dim
     c = 1 if thermal else d
     m = g.m(c)
@@ -379,9 +430,12 @@ def newton_solve_models(g, thermal, models, phase, e, g0=None, eta_newton=1e-5, 
     avg = np.zeros(m)
     rep = _Report()
     wu = _f64(warm_u).ravel() if warm_u is not None else None
-    code = lib().or_newton_solve_models(g.ref, C.c_int32(int(thermal)), C.c_int32(len(models)), arr,
-                                        _ptr(ph, C.c_uint8), _ptr(g0a), _ptr(e), C.byref(cfg), _ptr(wu), _ptr(u),
-                                        _ptr(gout) if width else None, _ptr(avg), C.byref(rep))
+    args = (g.ref, C.c_int32(int(thermal)), C.c_int32(len(models)), arr, _ptr(ph, C.c_uint8), _ptr(g0a), _ptr(e),
+            C.byref(cfg), _ptr(wu), _ptr(u), _ptr(gout) if width else None, _ptr(avg), C.byref(rep))
+    if manager is None:
+        code = lib().or_newton_solve_models(*args)
+    else:
+        code = lib().or_newton_solve_managed(*args, manager._h)
     if code not in (0, 3):
         _check(code)
     steps = [dict(cg_iterations=rep.steps[i].cg_iterations, residual_initial=rep.steps[i].residual_initial,

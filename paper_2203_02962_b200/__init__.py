@@ -233,6 +233,12 @@ class _Context:
             lib.homfe_gpu_destroy(h)
             self.h = None
 
+    def path(self):
+        """Names of the kernels this context runs (homfe_gpu_path_info)."""
+        f = C.c_int32()
+        _check(lib.homfe_gpu_path_info(self.h, C.byref(f)))
+        return {k for k, bit in _native.PATH_FLAGS.items() if f.value & bit}
+
     def set_material(self, cmats, phases):
         cm = _f64(np.asarray(cmats).reshape(-1, self.m, self.m).transpose(0, 2, 1))
         ph = np.ascontiguousarray(phases, dtype=np.uint8).ravel()
@@ -535,6 +541,8 @@ class Solver:
         else:
             self.ctx.set_material(np.stack([m.tangent for m in materials]), ph)
         self.width = 7 if self.nonlinear else 0
+        # a Solver is one PrecondManager (solver.hpp:105-129) over its solves
+        _check(lib.homfe_gpu_precond_reset(self.ctx.h))
         self.cfg = _native.SolveCfg()
         self.cfg.eta_newton, self.cfg.eta_cg = eta_newton, eta_cg
         self.cfg.max_newton, self.cfg.max_cg = max_newton, max_cg

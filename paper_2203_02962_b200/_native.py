@@ -87,6 +87,8 @@ def _load():
         "homfe_gpu_gamma_apply": (C.c_int, [vp, P(d), P(d)]),
         "homfe_gpu_sb_solve": (C.c_int, [vp, P(d), P(SolveCfg), P(d), P(d), P(d), P(d), P(d), P(d), P(Report)]),
         "homfe_gpu_eigenvalue_bounds": (C.c_int, [vp, P(d), i32, P(d), P(d), P(d), P(d)]),
+        "homfe_gpu_path_info": (C.c_int, [vp, P(i32)]),
+        "homfe_gpu_precond_reset": (C.c_int, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -105,4 +107,8 @@ EXPORTED = ("homfe_gpu_last_error", "homfe_isotropic_stiffness", "homfe_gpu_crea
             "homfe_random_uniform", "homfe_random_normal", "homfe_gpu_kernel_times",
             "homfe_nccl_unique_id", "homfe_gpu_create_dist", "homfe_gpu_slab_transport", "homfe_gpu_set_material_models",
             "homfe_gpu_internal_width", "homfe_gpu_solve_state", "homfe_gpu_stress_field",
-            "homfe_gpu_gamma_apply", "homfe_gpu_sb_solve", "homfe_gpu_eigenvalue_bounds")
+            "homfe_gpu_gamma_apply", "homfe_gpu_sb_solve", "homfe_gpu_eigenvalue_bounds", "homfe_gpu_path_info",
+            "homfe_gpu_precond_reset")
+
+PATH_FLAGS = {"fused_fft": 1, "hex_modal": 2, "while_graph": 4, "slab_spectra": 8, "slab": 16, "peer_pull": 32,
+              "elem2d": 64}

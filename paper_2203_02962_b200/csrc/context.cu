@@ -84,6 +84,24 @@ T* dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 
+// Scratch device buffers of one call, freed on every exit path (exceptions
+// included).
+struct Scratch {
+  std::vector<void*> bufs;
+  Scratch() = default;
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  ~Scratch() {
+    for (void* p : bufs) cudaFree(p);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    T* p = dalloc<T>(n > 0 ? n : 1);
+    bufs.push_back(p);
+    return p;
+  }
+};
+
 }  // namespace
 
 struct SimGroup {
@@ -150,6 +168,12 @@ struct homfe_ctx {
   SpecParams spp{};
   bool have_ref = false;
   std::vector<double> c_ref;
+  // PrecondManager state (solver.hpp:105-129): the context is the caller's
+  // manager; it persists across solves (load steps) until
+  // homfe_gpu_precond_reset (a new PrecondManager)
+  bool pm_valid = false;
+  std::vector<double> pm_mean;      // volume-averaged tangent at the last assembly
+  std::vector<double> pm_cref;      // reference used by the last assembly
   // scalars
   PcgState* d_st = nullptr;
   PcgState* h_st = nullptr;         // pinned
@@ -1048,6 +1072,46 @@ std::vector<double> resolve_reference(homfe_ctx* c, const homfe_solve_cfg* cfg) 
   return cr;
 }
 
+double frob(const std::vector<double>& a) {
+  double s2 = 0.0;
+  for (double v : a) s2 += v * v;
+  return std::sqrt(s2);
+}
+
+// PrecondManager::ensure (solver.cpp:120-142) with the volume-averaged
+// tangent `mean` of the current state: reassemble on first use, or when the
+// mean drifted beyond the threshold AND the resolved reference changed.
+// Returns whether it reassembled (one assembly counted).
+bool precond_ensure(homfe_ctx* c, const homfe_solve_cfg* cfg, const std::vector<double>& mean, homfe_report* rep) {
+  const int m = c->g.m;
+  bool need = !c->pm_valid;
+  if (!need) {
+    std::vector<double> diff(m * m);
+    for (int i = 0; i < m * m; ++i) diff[i] = mean[i] - c->pm_mean[i];
+    need = frob(diff) > cfg->reassembly_threshold * frob(c->pm_mean);
+  }
+  if (need) {
+    std::vector<double> cref;
+    if (cfg->reference_policy == HOMFE_REF_VOLUME_MEAN) {
+      cref = mean;
+    } else {
+      cref = resolve_reference(c, cfg);
+    }
+    if (!c->pm_valid || cref != c->pm_cref) {
+      set_reference(c, cref.data());
+      c->pm_cref = cref;
+      c->pm_mean = mean;
+      c->pm_valid = true;
+      rep->assemblies += 1;
+      return true;
+    }
+  }
+  // the manager keeps its blocks: restore them on the device if a parity hook
+  // (homfe_gpu_set_reference) replaced the context's reference since
+  if (!c->have_ref || c->c_ref != c->pm_cref) set_reference(c, c->pm_cref.data());
+  return false;
+}
+
 void validate_cfg(const homfe_solve_cfg* cfg) {
   if (!cfg) throw ValidationError("solver: null config");
   if (!(cfg->eta_newton > 0.0 && cfg->eta_newton < 1.0) || !(cfg->eta_cg > 0.0 && cfg->eta_cg < 1.0))
@@ -1078,15 +1142,12 @@ void newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* a
     element_load(c->sp, c->g.d, c->g.c, &c->catalog[(size_t)ph * m * m], e, &fe[(size_t)ph * ne]);
   HB_CUDA(cudaMemcpyAsync(c->d_fe, fe.data(), fe.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
 
-  // PrecondManager::ensure: one assembly for a linear tangent.
+  // PrecondManager::ensure: a linear tangent's volume mean is the phase-count
+  // average; it never drifts within a solve, so only step 0 can reassemble.
   auto t0 = Clock::now();
-  const std::vector<double> cref = resolve_reference(c, cfg);
-  bool reassembled = false;
-  if (!c->have_ref || cref != c->c_ref) {
-    set_reference(c, cref.data());
-    reassembled = true;
-  }
-  rep->assemblies = 1;
+  homfe_solve_cfg vm = *cfg;
+  vm.reference_policy = HOMFE_REF_VOLUME_MEAN;
+  const bool reassembled = precond_ensure(c, cfg, resolve_reference(c, &vm), rep);
   rep->seconds_assembly += since(t0);
 
   double bnorm0 = 0.0, inc_rel = INFINITY;
@@ -1215,11 +1276,6 @@ std::vector<double> nl_sweep(homfe_ctx* c) {
   return mean;
 }
 
-double frob(const std::vector<double>& a) {
-  double s2 = 0.0;
-  for (double v : a) s2 += v * v;
-  return std::sqrt(s2);
-}
 
 // newton_solve (solver.cpp:171-296) for a catalog with J2 phases: a
 // constitutive sweep per Newton step, PrecondManager::ensure with the
@@ -1240,7 +1296,6 @@ bool newton_nl(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double
     destroy_graphs(c);  // captured operator changes
     c->graphs_nl = true;
   }
-  std::vector<double> mean_at_assembly;
   double bnorm0 = 0.0, inc_rel = INFINITY;
   bool have_inc = false, converged_state = false;
   const int64_t n = c->nvec();
@@ -1253,33 +1308,7 @@ bool newton_nl(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double
     rep->seconds_constitutive += since(t0);
     // PrecondManager::ensure
     t0 = Clock::now();
-    bool reassembled = false;
-    bool need = !c->have_ref || mean_at_assembly.empty();
-    if (!need) {
-      std::vector<double> diff(m * m);
-      for (int i = 0; i < m * m; ++i) diff[i] = mean[i] - mean_at_assembly[i];
-      need = frob(diff) > cfg->reassembly_threshold * frob(mean_at_assembly);
-    }
-    if (need) {
-      std::vector<double> cref(m * m, 0.0);
-      if (cfg->reference_policy == HOMFE_REF_IDENTITY_SCALED) {
-        if (!(cfg->reference_scale > 0.0)) throw ValidationError("reference: identity scale must be > 0");
-        for (int i = 0; i < m; ++i) cref[i * m + i] = cfg->reference_scale;
-      } else if (cfg->reference_policy == HOMFE_REF_VOLUME_MEAN) {
-        cref = mean;
-      } else if (cfg->reference_policy == HOMFE_REF_EXPLICIT) {
-        if (!cfg->reference_matrix) throw ValidationError("reference: explicit matrix has wrong size");
-        std::copy(cfg->reference_matrix, cfg->reference_matrix + m * m, cref.begin());
-      } else {
-        throw ValidationError("reference: invalid policy");
-      }
-      if (!c->have_ref || mean_at_assembly.empty() || cref != c->c_ref) {
-        set_reference(c, cref.data());
-        mean_at_assembly = mean;
-        reassembled = true;
-        rep->assemblies += 1;
-      }
-    }
+    const bool reassembled = precond_ensure(c, cfg, mean, rep);
     rep->seconds_assembly += since(t0);
     // z = M^-1 b and b.z
     c->nl_op = false;
@@ -1362,6 +1391,19 @@ bool newton_nl(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double
   return converged_state;
 }
 
+
+// newton_solve dispatch: the linear branch (phase-indexed tangents), or the
+// general one (J2 catalogs; two-node stencils, whose operator runs on the
+// quadrature-point path) from a zero committed state.
+void solve_dispatch(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, double* avg_out, homfe_report* r) {
+  if (c->nonlinear || c->g.nn > 1) {
+    ensure_nl_buffers(c);
+    HB_CUDA(cudaMemsetAsync(c->d_g0, 0, (size_t)c->g.np * c->sp.nq * 7 * sizeof(double), c->stream));
+    newton_nl(c, e, cfg, avg_out, r);
+  } else {
+    newton(c, e, cfg, avg_out, r);
+  }
+}
 
 void ensure_sb_buffers(homfe_ctx* c) {
   if (c->d_strain) return;
@@ -2006,6 +2048,15 @@ int homfe_gpu_set_material_device(homfe_ctx* c, int32_t n_phases, const double* 
   });
 }
 
+int homfe_gpu_precond_reset(homfe_ctx* c) {
+  return guarded([&] {
+    if (!c) throw ValidationError("precond_reset: null context");
+    c->pm_valid = false;
+    c->pm_mean.clear();
+    c->pm_cref.clear();
+  });
+}
+
 int homfe_gpu_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* warm_u,
                     double* u_out, double* avg_out, homfe_report* rep) {
   return guarded([&] {
@@ -2015,12 +2066,7 @@ int homfe_gpu_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, c
     else HB_CUDA(cudaMemsetAsync(c->d_u, 0, n * sizeof(double), c->stream));
     homfe_report local;
     homfe_report* r = rep ? rep : &local;
-    if (c->nonlinear || c->g.nn > 1) {
-      HB_CUDA(cudaMemsetAsync(c->d_g0, 0, (size_t)c->g.np * c->sp.nq * 7 * sizeof(double), c->stream));
-      newton_nl(c, e, cfg, avg_out, r);
-    } else {
-      newton(c, e, cfg, avg_out, r);
-    }
+    solve_dispatch(c, e, cfg, avg_out, r);
     if (u_out) HB_CUDA(cudaMemcpyAsync(u_out, c->d_u, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     if (!r->converged) throw NonConverged(r->cause == 1 ? "cg-stall" : "newton-cap");
@@ -2200,13 +2246,12 @@ int homfe_gpu_eigenvalue_bounds(homfe_ctx* c, const double* tangent, int32_t pix
       }
     const int64_t nq = c->g.np * c->sp.nq, nn = c->nodes();
     const int cc = c->g.c;
-    double* d_t = nullptr;
-    double *d_lo = nullptr, *d_hi = nullptr, *d_lo2 = nullptr, *d_hi2 = nullptr;
-    HB_CUDA(cudaMallocAsync(&d_t, (size_t)nq * m * m * sizeof(double), c->stream));
-    HB_CUDA(cudaMallocAsync(&d_lo, (size_t)nn * cc * sizeof(double), c->stream));
-    HB_CUDA(cudaMallocAsync(&d_hi, (size_t)nn * cc * sizeof(double), c->stream));
-    HB_CUDA(cudaMallocAsync(&d_lo2, (size_t)nn * cc * sizeof(double), c->stream));
-    HB_CUDA(cudaMallocAsync(&d_hi2, (size_t)nn * cc * sizeof(double), c->stream));
+    Scratch scratch;
+    double* d_t = scratch.alloc<double>((size_t)nq * m * m);
+    double* d_lo = scratch.alloc<double>((size_t)nn * cc);
+    double* d_hi = scratch.alloc<double>((size_t)nn * cc);
+    double* d_lo2 = scratch.alloc<double>((size_t)nn * cc);
+    double* d_hi2 = scratch.alloc<double>((size_t)nn * cc);
     HB_CUDA(cudaMemcpyAsync(d_t, tangent, (size_t)nq * m * m * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     const int st = bounds_device(c->g, c->sp, d_t, pixel_constant, Li.data(), cc, d_lo, d_hi, c->stream);
     if (st == 2) throw ValidationError("eigenvalue_bounds: tangent must be positive definite per point");
@@ -2214,14 +2259,12 @@ int homfe_gpu_eigenvalue_bounds(homfe_ctx* c, const double* tangent, int32_t pix
     size_t tmp_bytes = 0;
     const int nk = (int)(nn * cc);
     HB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, d_lo, d_lo2, nk, 0, 64, c->stream));
-    void* d_tmp = nullptr;
-    HB_CUDA(cudaMallocAsync(&d_tmp, tmp_bytes, c->stream));
+    void* d_tmp = scratch.alloc<unsigned char>(tmp_bytes);
     HB_CUDA(cub::DeviceRadixSort::SortKeys(d_tmp, tmp_bytes, d_lo, d_lo2, nk, 0, 64, c->stream));
     HB_CUDA(cub::DeviceRadixSort::SortKeys(d_tmp, tmp_bytes, d_hi, d_hi2, nk, 0, 64, c->stream));
     HB_CUDA(cudaMemcpyAsync(lower, d_lo2, (size_t)nk * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     HB_CUDA(cudaMemcpyAsync(upper, d_hi2, (size_t)nk * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
-    for (void* ptr : {(void*)d_t, (void*)d_lo, (void*)d_hi, (void*)d_lo2, (void*)d_hi2, d_tmp}) cudaFree(ptr);
     if (!(lower[0] > 0.0)) throw ValidationError("condition_estimate: bounds must be positive");
     if (cond) *cond = upper[nk - 1] / lower[0];
   });
@@ -2257,7 +2300,7 @@ int homfe_gpu_solve_device(homfe_ctx* c, const double* e, const homfe_solve_cfg*
     else HB_CUDA(cudaMemsetAsync(c->d_u, 0, n * sizeof(double), c->stream));
     homfe_report local;
     homfe_report* r = rep ? rep : &local;
-    newton(c, e, cfg, avg_out, r);
+    solve_dispatch(c, e, cfg, avg_out, r);
     if (d_u_out) HB_CUDA(cudaMemcpyAsync(d_u_out, c->d_u, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     sync(c);
     if (!r->converged) throw NonConverged(r->cause == 1 ? "cg-stall" : "newton-cap");
@@ -2311,11 +2354,11 @@ int homfe_gpu_reference_blocks(homfe_ctx* c, double* blocks) {
       return;
     }
     const size_t cnt = (size_t)c->nf * c->g.c * c->g.c;
-    double2* d = dalloc<double2>(cnt);
+    Scratch scratch;
+    double2* d = scratch.alloc<double2>(cnt);
     launch_symbol_dump(c->spp, d, c->stream);
     HB_CUDA(cudaMemcpyAsync(blocks, d, cnt * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
-    cudaFree(d);
   });
 }
 
@@ -2462,6 +2505,16 @@ int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
     ms[7] = ms[0] + ms[1] + ms[2] + ms[3] + ms[4] + ms[5] + ms[6];
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+  });
+}
+
+int homfe_gpu_path_info(const homfe_ctx* c, int32_t* flags) {
+  return guarded([&] {
+    if (!c || !flags) throw ValidationError("path_info: null argument");
+    *flags = (c->fused ? HOMFE_PATH_FUSED_FFT : 0) | (c->hex_fast ? HOMFE_PATH_HEX_MODAL : 0) |
+             (c->use_while ? HOMFE_PATH_WHILE_GRAPH : 0) | (c->slab_fft ? HOMFE_PATH_SLAB_SPECTRA : 0) |
+             (c->dist ? HOMFE_PATH_SLAB : 0) | (c->peer ? HOMFE_PATH_PEER_PULL : 0) |
+             (elem2d_eligible(c->g) && !c->no_fast2d ? HOMFE_PATH_ELEM2D : 0);
   });
 }
 

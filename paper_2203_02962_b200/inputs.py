@@ -24,22 +24,56 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._native import lib
-
 BASE_SEED = 2203020
+
+# The uniform stream (std::mt19937_64 + (gen() >> 11) 2^-53) comes from a C
+# function `fn(seed, n, lo, hi, double* out)`: the product library's
+# homfe_random_uniform by default. The CPU baseline arm of bench.py loads this
+# module by path (no package import) and points it at the oracle's identical
+# or_uniform, so that process never maps libhomfe_gpu.so.
+_uniform_fn = None
+
+
+def set_uniform_source(fn):
+    global _uniform_fn
+    _uniform_fn = fn
 
 
 def uniform(seed, n, lo=0.0, hi=1.0):
+    global _uniform_fn
+    if _uniform_fn is None:
+        from ._native import lib
+        _uniform_fn = lib.homfe_random_uniform
     out = np.zeros(int(n))
-    lib.homfe_random_uniform(C.c_uint64(seed), int(n), float(lo), float(hi),
-                             out.ctypes.data_as(C.POINTER(C.c_double)))
+    _uniform_fn(C.c_uint64(seed), C.c_int64(int(n)), C.c_double(lo), C.c_double(hi),
+                out.ctypes.data_as(C.POINTER(C.c_double)))
     return out
 
 
 def normal(seed, n):
-    out = np.zeros(int(n))
-    lib.homfe_random_normal(C.c_uint64(seed), int(n), out.ctypes.data_as(C.POINTER(C.c_double)))
-    return out
+    """Standard normals by Box-Muller on consecutive uniform pairs of the same
+    stream (out[2i] = r cos, out[2i+1] = r sin)."""
+    n = int(n)
+    u = uniform(seed, 2 * ((n + 1) // 2))
+    r = np.sqrt(-2.0 * np.log1p(-u[0::2]))
+    t = 2.0 * math.pi * u[1::2]
+    out = np.empty(2 * r.size)
+    out[0::2] = r * np.cos(t)
+    out[1::2] = r * np.sin(t)
+    return out[:n]
+
+
+def isotropic_stiffness(bulk, shear, dim):
+    """3K P_vol + 2G P_dev in Mandel notation (mandel.cpp:114-134; plane
+    strain in 2-D: the in-plane block of the 3-D tensor)."""
+    vol = np.zeros((6, 6))
+    vol[:3, :3] = 1.0
+    pv = vol / 3.0
+    pd = np.eye(6) - pv
+    m3 = (3.0 * bulk) * pv + (2.0 * shear) * pd
+    if dim == 3:
+        return m3
+    return m3[np.ix_([0, 1, 5], [0, 1, 5])].copy()
 
 
 def youngs_to_bulk_shear(E, nu):
@@ -155,7 +189,6 @@ class Config:
         return self.components * self.num_pixels
 
     def tangents(self):
-        from . import isotropic_stiffness
         out = []
         for mat in self.materials:
             if mat[0] == "kappa":

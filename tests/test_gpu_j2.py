@@ -147,3 +147,38 @@ def test_linear_stress_field_matches_oracle(hb, oracle_mod):
     cm = np.stack([c0, c1])[np.repeat(ph, og.quads_per_pixel)]
     sig = np.einsum("qij,qj->qi", cm, eps)
     assert np.abs(out["stress"] - sig).max() <= 1e-12 * np.abs(sig).max()
+
+
+def test_j2_load_program_shares_precond_manager(hb, oracle_mod):
+    """run_load_program shares ONE PrecondManager over its steps
+    (solver.cpp:306-318): with the volume-mean policy the reference is
+    reassembled only when the averaged tangent drifts beyond the threshold
+    (solver.cpp:120-142), so later steps may reuse an older C_ref. Per-step
+    CG counts, reassembly flags and assembly counts match the oracle run with
+    one shared manager."""
+    gpu, orc = _j2_pair(hb, oracle_mod, 2, [(1.0, 0.5, 1e-3, 0.05), (10.0, 5.0, 2e-3, 0.5)])
+    ph = np.zeros(16 * 16, np.uint8)
+    ph.reshape(16, 16)[4:12, 4:12] = 1
+    loads = [np.array([1e-3, 0.0, 0.5e-3]) * s for s in (1.0, 2.0, 3.0, 4.0)]
+    kw = dict(eta_newton=1e-9, eta_cg=1e-10, reference="volume-mean", reassembly_threshold=0.05)
+    grid = hb.Grid((16, 16), (1.0, 1.0), "two-triangles")
+    res = hb.run_load_program(grid, gpu, ph, loads, **kw)
+    og = oracle_mod.Grid((16, 16), (1.0, 1.0), "two-triangles")
+    mgr = oracle_mod.PrecondManager()
+    g = warm = None
+    flags_g, flags_o = [], []
+    for step, e in enumerate(loads):
+        ref = oracle_mod.newton_solve_models(og, False, orc, ph, e, g0=g, warm_u=warm, manager=mgr, **kw)
+        got = res[step]
+        assert got["converged"] and ref["converged"]
+        assert got["report"]["newton_steps"] == len(ref["steps"]), step
+        for sg, so in zip(got["report"]["steps"], ref["steps"]):
+            assert abs(sg["cg_iterations"] - so["cg_iterations"]) <= 1, step
+            flags_g.append(sg["precond_reassembled"])
+            flags_o.append(so["precond_reassembled"])
+        assert got["report"]["assemblies"] == ref["assemblies"], step
+        assert _rel(got["average_stress"], ref["average_stress"]) < 1e-8
+        g, warm = ref["internal"], ref["u"]
+    assert flags_g == flags_o
+    # the drift rule did skip reassemblies on later Newton steps
+    assert sum(flags_o) < len(flags_o) and mgr.assemblies == sum(flags_o)
