@@ -208,6 +208,17 @@ int homfe_gpu_volume_average(homfe_ctx* ctx, const double* s, double* out);
    homfe_gpu_set_reference; history holds it_max + 1 doubles. */
 int homfe_gpu_pcg(homfe_ctx* ctx, const double* b, double eta, int32_t it_max, double* x,
                   int32_t* iterations, double* history, int32_t* converged);
+/* pcg_solve with an IterateObserver (solver.hpp:57-78, solver.cpp:87):
+   `observer(user, k, x_k)` receives a host copy of the iterate after every
+   iteration k >= 1 (x before the final mean removal, as in the reference).
+   Runs the iterations one graph launch at a time (inspection, not speed). */
+typedef void (*homfe_iterate_observer)(void* user, int32_t iteration, const double* x);
+int homfe_gpu_pcg_observed(homfe_ctx* ctx, const double* b, double eta, int32_t it_max, double* x,
+                           int32_t* iterations, double* history, int32_t* converged,
+                           homfe_iterate_observer observer, void* user);
+/* weighted_dot (fields.hpp:86-88): sum_q w_q a(q).b(q) of two m-component
+   quad fields (m of the context). */
+int homfe_gpu_weighted_dot(homfe_ctx* ctx, const double* a, const double* b, double* out);
 /* Index maps for bit-exact comparison: strides (3) and the periodic neighbour
    table nbr[p * n_offsets + o] (grid.cpp:267-288, operators.cpp:65-84),
    computed on the device. */

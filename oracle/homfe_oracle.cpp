@@ -818,8 +818,8 @@ or_precond* assemble(const Layout& l, const double* c_ref, int c, bool weighted)
 // (precond.cpp:44-85). Both steps round in fp64; at low frequencies the block
 // is O(theta^2) while the response entries are O(1), so its relative rounding
 // is ~eps/theta^2. Here the same quantity is evaluated in long double
-// (64-bit mantissa) from the stencil tables of grid.cpp (restated with long
-// double Gauss points) and the Mandel rows of operators.cpp:16-53:
+// (64-bit mantissa) from the operator's own fp64 stencil tables (grid.cpp)
+// and the Mandel rows of operators.cpp:16-53:
 //   S_delta = sum_q w_q sum_{a,b : o_a - o_b = delta} B_a^T C_ref B_b,
 //   K_hat(xi)[row][col] = sum_delta S_delta[row][col] exp(-i xi . delta),
 // with xi_a = 2 pi f_a / N_a (f the non-negative FFT index, fft.cpp:71-79),
@@ -830,45 +830,19 @@ using LD = long double;
 struct LEntry { int off; LD dphi[3]; };
 struct LQuad { LD w; std::vector<LEntry> e; };
 
+// The stencil tables of the reference operator exactly as it applies them
+// (the fp64 dphi and weights of make_layout, grid.cpp:114-229), promoted to
+// long double: the symbol below is the exact symbol of THAT discrete
+// operator, so the only difference to the probed blocks is the probing's own
+// rounding (operator sweep + FFT).
 std::vector<LQuad> exact_quads(const Layout& l, bool weighted) {
+  if (l.Nn != 1) throw ValidationError("exact symbol: one-node stencils only");
   std::vector<LQuad> qs;
-  LD h[3] = {1, 1, 1}, vp = 1;
-  for (int a = 0; a < l.d; ++a) { h[a] = (LD)l.L[a] / (LD)l.N[a]; vp *= h[a]; }
-  const LD gq = 0.5L / sqrtl(3.0L);
-  const LD gp[2] = {0.5L - gq, 0.5L + gq};
-  if (l.kind == OR_TWO_TRIANGLES) {
-    qs.push_back({vp / 2, {{0, {-1 / h[0], -1 / h[1], 0}}, {1, {1 / h[0], 0, 0}}, {2, {0, 1 / h[1], 0}}}});
-    qs.push_back({vp / 2, {{3, {1 / h[0], 1 / h[1], 0}}, {2, {-1 / h[0], 0, 0}}, {1, {0, -1 / h[1], 0}}}});
-  } else if (l.kind == OR_BILINEAR_QUAD) {
-    for (int i = 0; i < 2; ++i)
-      for (int j = 0; j < 2; ++j) {
-        LQuad q{vp / 4, {}};
-        const LD xi[2] = {1 - gp[i], gp[i]}, dxi[2] = {-1 / h[0], 1 / h[0]};
-        const LD et[2] = {1 - gp[j], gp[j]}, det[2] = {-1 / h[1], 1 / h[1]};
-        for (int a = 0; a < 2; ++a)
-          for (int b = 0; b < 2; ++b) q.e.push_back({a + 2 * b, {dxi[a] * et[b], xi[a] * det[b], 0}});
-        qs.push_back(q);
-      }
-  } else if (l.kind == OR_TRILINEAR_HEX) {
-    for (int i = 0; i < 2; ++i)
-      for (int j = 0; j < 2; ++j)
-        for (int k = 0; k < 2; ++k) {
-          LQuad q{vp / 8, {}};
-          const LD xi[2] = {1 - gp[i], gp[i]}, dxi[2] = {-1 / h[0], 1 / h[0]};
-          const LD et[2] = {1 - gp[j], gp[j]}, det[2] = {-1 / h[1], 1 / h[1]};
-          const LD ze[2] = {1 - gp[k], gp[k]}, dze[2] = {-1 / h[2], 1 / h[2]};
-          for (int a = 0; a < 2; ++a)
-            for (int b = 0; b < 2; ++b)
-              for (int c = 0; c < 2; ++c)
-                q.e.push_back({(a * 2 + b) * 2 + c,
-                               {dxi[a] * et[b] * ze[c], xi[a] * det[b] * ze[c], xi[a] * et[b] * dze[c]}});
-          qs.push_back(q);
-        }
-  } else {
-    throw ValidationError("exact symbol: one-node stencils only");
+  for (const auto& q : l.quads) {
+    LQuad lq{weighted ? (LD)q.w : (LD)1, {}};
+    for (const auto& e : q.entries) lq.e.push_back({e.off, {(LD)e.dphi[0], (LD)e.dphi[1], (LD)e.dphi[2]}});
+    qs.push_back(lq);
   }
-  if (!weighted)
-    for (auto& q : qs) q.w = 1;
   return qs;
 }
 

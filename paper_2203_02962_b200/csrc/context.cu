@@ -870,7 +870,11 @@ struct PcgResult {
 };
 
 // pcg_solve with r = b already in d_r; x lands in d_x (mean-free).
-PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history) {
+// obs (nullable): IterateObserver of pcg_solve (solver.cpp:87), called with
+// a host copy of x_k after every iteration; forces the host-driven loop of
+// one-iteration graphs (a debugging / inspection mode, not the fast path).
+PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history,
+                  homfe_iterate_observer obs = nullptr, void* obs_user = nullptr) {
   if (it_max + 1 > c->hist_cap) {
     destroy_graphs(c);  // graphs capture the history pointer
     if (c->d_hist) cudaFree(c->d_hist);
@@ -886,7 +890,7 @@ PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history) {
       }
     }
   }
-  if (c->use_while) {
+  if (c->use_while && !obs) {
     HB_CUDA(cudaGraphLaunch(c->pcg_exec, c->stream));
   } else {
     capture_init(c, c->stream);
@@ -902,14 +906,20 @@ PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history) {
     sync(c);
     int launched = 0;
     int batch = 1;
+    std::vector<double> hx(obs ? c->nvec() : 0);
     while (!c->h_st->done && launched < it_max) {
+      const int it_before = c->h_st->it;
       for (int i = 0; i < batch && launched < it_max; ++i, ++launched) {
         if (c->body_exec) HB_CUDA(cudaGraphLaunch(c->body_exec, c->stream));
         else body_sequence(c, c->stream, false, 0);
       }
       HB_CUDA(cudaMemcpyAsync(c->h_st, c->d_st, sizeof(PcgState), cudaMemcpyDeviceToHost, c->stream));
+      if (obs) HB_CUDA(cudaMemcpyAsync(hx.data(), c->d_x, hx.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                       c->stream));
       sync(c);
-      batch = std::min(batch * 2, 16);
+      if (c->h_st->status == 4) break;
+      if (obs && c->h_st->it > it_before) obs(obs_user, c->h_st->it, hx.data());
+      batch = obs ? 1 : std::min(batch * 2, 16);
     }
     capture_tail(c, c->stream);
   }
@@ -2402,6 +2412,25 @@ int homfe_gpu_divergence(homfe_ctx* c, const double* s, int32_t weighted, double
   });
 }
 
+int homfe_gpu_weighted_dot(homfe_ctx* c, const double* a, const double* b, double* out) {
+  if (c && c->dist) {
+    g_err = "not available in slab mode (use a single-device context)";
+    return HOMFE_VALIDATION;
+  }
+  return guarded([&] {
+    if (!a || !b || !out) throw ValidationError("weighted_dot: null argument");
+    HB_CUDA(cudaSetDevice(c->device));
+    const size_t n = (size_t)c->g.np * c->sp.nq * c->g.m;
+    Scratch scratch;
+    double* da = scratch.alloc<double>(n);
+    double* db = a == b ? da : scratch.alloc<double>(n);
+    HB_CUDA(cudaMemcpyAsync(da, a, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    if (db != da) HB_CUDA(cudaMemcpyAsync(db, b, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    launch_quad_wdot(c->g, c->sp, da, db, c->d_partials, c->stream);
+    reduce_to_host(c, 1, out);
+  });
+}
+
 int homfe_gpu_volume_average(homfe_ctx* c, const double* s, double* out) {
   if (c && c->dist) {
     g_err = "not available in slab mode (use a single-device context)";
@@ -2429,6 +2458,25 @@ int homfe_gpu_pcg(homfe_ctx* c, const double* b, double eta, int32_t it_max, dou
     const int64_t n = c->nvec();
     HB_CUDA(cudaMemcpyAsync(c->d_r, b, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     const PcgResult r = run_pcg(c, eta, it_max, history);
+    HB_CUDA(cudaMemcpyAsync(x, c->d_x, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (iterations) *iterations = r.iterations;
+    if (converged) *converged = r.converged ? 1 : 0;
+  });
+}
+
+int homfe_gpu_pcg_observed(homfe_ctx* c, const double* b, double eta, int32_t it_max, double* x,
+                           int32_t* iterations, double* history, int32_t* converged, homfe_iterate_observer obs,
+                           void* user) {
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    require_material(c);
+    require_reference(c);
+    if (it_max < 0) throw ValidationError("pcg: it_max must be >= 0");
+    if (c->dist) throw ValidationError("pcg_observed: single-GPU contexts only");
+    const int64_t n = c->nvec();
+    HB_CUDA(cudaMemcpyAsync(c->d_r, b, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    const PcgResult r = run_pcg(c, eta, it_max, history, obs, user);
     HB_CUDA(cudaMemcpyAsync(x, c->d_x, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     sync(c);
     if (iterations) *iterations = r.iterations;

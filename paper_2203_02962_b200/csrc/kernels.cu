@@ -331,6 +331,23 @@ __global__ void __launch_bounds__(kBlock) k_quad_wsum(const Grid g, const __grid
   block_sum_store<M>(acc, partials + (size_t)blockIdx.x * M);
 }
 
+// sum_q w_q a(q).b(q) over M-component quad fields (fields.cpp:19-35), one
+// per-block partial (fixed grid: deterministic).
+template <int M>
+__global__ void __launch_bounds__(kBlock) k_quad_wdot(const Grid g, const __grid_constant__ StencilParams sp,
+                                                      const double* __restrict__ a, const double* __restrict__ b,
+                                                      double* partials) {
+  double acc[1] = {0.0};
+  const int64_t nQ = g.np * sp.nq;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nQ; q += (int64_t)gridDim.x * blockDim.x) {
+    double d = 0.0;
+#pragma unroll
+    for (int k = 0; k < M; ++k) d = fma(a[q * M + k], b[q * M + k], d);
+    acc[0] = fma(sp.w[q % sp.nq], d, acc[0]);
+  }
+  block_sum_store<1>(acc, partials + blockIdx.x);
+}
+
 __global__ void k_index_maps(const Grid g, const __grid_constant__ StencilParams sp, int64_t* nbr) {
   const int64_t np = g.np;
   const int64_t s0 = g.d == 3 ? (int64_t)g.n1 * g.n2 : g.n1;
@@ -600,6 +617,17 @@ void launch_quad_wsum(const Grid& g, const StencilParams& sp, const double* sf, 
     case 3: k_quad_wsum<3><<<kRedBlocks, kBlock, 0, s>>>(g, sp, sf, partials); break;
     case 6: k_quad_wsum<6><<<kRedBlocks, kBlock, 0, s>>>(g, sp, sf, partials); break;
     default: throw ValidationError("volume_average: unsupported component count");
+  }
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_quad_wdot(const Grid& g, const StencilParams& sp, const double* a, const double* b, double* partials,
+                      cudaStream_t s) {
+  switch (g.m) {
+    case 2: k_quad_wdot<2><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, b, partials); break;
+    case 3: k_quad_wdot<3><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, b, partials); break;
+    case 6: k_quad_wdot<6><<<kRedBlocks, kBlock, 0, s>>>(g, sp, a, b, partials); break;
+    default: throw ValidationError("weighted_dot: unsupported component count");
   }
   HB_CUDA(cudaGetLastError());
 }

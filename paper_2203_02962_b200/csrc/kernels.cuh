@@ -99,6 +99,8 @@ struct QuadArgs {
 void launch_quad(const Grid& g, const StencilParams& sp, int mode, const QuadArgs& a, cudaStream_t s);
 void launch_divergence(const Grid& g, const StencilParams& sp, const double* sfield, bool weighted,
                        double* out, cudaStream_t s);
+void launch_quad_wdot(const Grid& g, const StencilParams& sp, const double* a, const double* b, double* partials,
+                      cudaStream_t s);
 void launch_quad_wsum(const Grid& g, const StencilParams& sp, const double* sfield, double* partials,
                       cudaStream_t s);
 void launch_index_maps(const Grid& g, const StencilParams& sp, int64_t* nbr, cudaStream_t s);
