@@ -156,7 +156,7 @@ def run_gpu(args, rank, world, local_rank):
         transport = {"peer_pull": "peer pull over NVLink + barrier all-reduces",
                      "all_to_all": "NCCL halo + all-to-all", "single": "one rank"}[sc.transport]
         z0, nz = hdist.slab_range(g.dims[0], rank, world)
-        plane = g.dims[1] * g.dims[2]
+        plane = int(np.prod(g.dims[1:]))
         ph_local = np.ascontiguousarray(phases[z0 * plane:(z0 + nz) * plane])
         sc.set_material(tangents, ph_local)
         scfg = _native.SolveCfg()
@@ -309,7 +309,7 @@ def run_gpu(args, rank, world, local_rank):
         # transposes ((G-1)/G of the rank's c N_f / G complex values each)
         nh = g.dims[-1] // 2 + 1
         nf = int(np.prod(g.dims[:-1])) * nh
-        halo = 2 * c * g.dims[1] * g.dims[2] * 8 if world > 1 else 0
+        halo = 2 * c * int(np.prod(g.dims[1:])) * 8 if world > 1 else 0
         a2a = 2 * c * 16 * (nf / world) * (world - 1) / world
         nbytes = halo + a2a
         nv_peak = 900.0  # GB/s per direction, NVLink 5 (B200 datasheet)

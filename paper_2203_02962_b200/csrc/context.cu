@@ -459,6 +459,7 @@ void slab_solve(homfe_ctx* c, const PcgState* st, double* partials, cudaStream_t
   p.nf = (int64_t)c->sd.n0 * c->sd.n1l * c->sd.nh;
   p.n1r = c->sd.n1l;
   p.k1off = c->sd.me * c->sd.n1l;
+  if (c->g.d == 2) p.nh = c->sd.n1l;  // frequencies (i0, k1off + k1l), columns >= nhv are padding
   launch_spectral(p, c->d_W, st, partials, s);
   c->launches += 1;
 }
@@ -1712,10 +1713,11 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
   const int G = dist ? world : 1;
   if (dist) {
     if (rank < 0 || rank >= world) throw ValidationError("slab: rank out of range");
-    if (d != 3 || desc->stencil != HOMFE_TRILINEAR_HEX)
-      throw ValidationError("slab mode: 3-d trilinear-hex grids only");
-    if (desc->dims[0] % world != 0 || desc->dims[1] % world != 0)
-      throw ValidationError("slab mode: dims[0] and dims[1] must be divisible by the number of ranks");
+    if (desc->stencil == HOMFE_FOUR_TRIANGLES_TWO_NODE)
+      throw ValidationError("slab mode: one-node stencils only");
+    if (desc->dims[0] % world != 0 || (d == 3 && desc->dims[1] % world != 0))
+      throw ValidationError(d == 3 ? "slab mode: dims[0] and dims[1] must be divisible by the number of ranks"
+                                   : "slab mode: dims[0] must be divisible by the number of ranks");
     if (!nccl_id) throw ValidationError("slab mode: missing NCCL unique id");
   }
   auto* ctx = new homfe_ctx();
@@ -1822,6 +1824,7 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     p.k1off = 0;
     p.n2 = g.n2;
     p.nh = nh;
+    p.nhv = nh;
     p.nf = ctx->nf;
     p.w = ctx->sp.w[0];
     p.inv_np = 1.0 / (double)g.npg;
@@ -1843,7 +1846,37 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
     if (const char* env = std::getenv("HOMFE_FAST2D")) ctx->no_fast2d = env[0] == '0';
     const char* fenv = std::getenv("HOMFE_FUSED_FFT");
     const bool fused_ok = fused_fft_eligible(g) && g.n1 % G == 0;
-    if (dist && !fused_ok) {
+    if (dist && d == 2) {
+      // 2-D row slabs (c5): 1-D r2c along axis 1 of the local rows, the
+      // half-spectrum columns split over the ranks (nhl = ceil(nh / G) each,
+      // the last chunk zero-padded), 1-D c2c along axis 0 on the rank's
+      // columns. The 3-D slab layouts with a unit last axis: S
+      // [c][i0l][k1 < G nhl][1], W [c][i0][k1l][1] (slabfft.cu, unchanged).
+      SlabDims& sd = ctx->sd;
+      const int nhl = (nh + G - 1) / G;
+      sd = SlabDims{c, g.n0g, g.n0, G * nhl, nhl, 1, g.rank, G};
+      int nr[1] = {g.n1}, nsp[1] = {G * nhl};
+      HB_CUFFT(cufftPlanMany(&ctx->p2f, 1, nr, nr, 1, g.n1, nsp, 1, G * nhl, CUFFT_D2Z, c * g.n0));
+      HB_CUFFT(cufftPlanMany(&ctx->p2i, 1, nr, nsp, 1, G * nhl, nr, 1, g.n1, CUFFT_Z2D, c * g.n0));
+      int n1d[1] = {g.n0g};
+      const int rs = nhl;  // axis-0 stride of W
+      HB_CUFFT(cufftPlanMany(&ctx->p1, 1, n1d, n1d, rs, 1, n1d, rs, 1, CUFFT_Z2Z, rs));
+      const int64_t tot = sd.chunk() * G;
+      ctx->d_S = dalloc<double2>(tot);
+      ctx->d_W = dalloc<double2>(tot);
+      HB_CUDA(cudaMemset(ctx->d_S, 0, tot * sizeof(double2)));  // padding columns stay zero
+      HB_CUDA(cudaMemset(ctx->d_W, 0, tot * sizeof(double2)));
+      if (p2p_wanted(G)) setup_peers(ctx, ctx->d_W, ctx->d_S);
+      if (G == 1) {
+        ctx->peer_a[0] = ctx->d_W;
+        ctx->peer_b[0] = ctx->d_S;
+      }
+      if (!ctx->peer && G > 1) {
+        ctx->d_send = dalloc<double2>(tot);
+        ctx->d_recv = dalloc<double2>(tot);
+      }
+      ctx->slab_fft = true;
+    } else if (dist && !fused_ok) {
       // slab spectra for any plane size: cuFFT per rank + transposes (slabfft.cu)
       SlabDims& sd = ctx->sd;
       sd = SlabDims{c, g.n0g, g.n0, g.n1, g.n1 / G, g.n2 / 2 + 1, g.rank, G};

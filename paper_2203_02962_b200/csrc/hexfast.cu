@@ -431,7 +431,7 @@ __device__ __forceinline__ void z_issue(const HexArgs& a, const int* its, int u,
   }
 }
 
-template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT = false>
+template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT = false, bool MATS = true>
 __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1 : (C == 3 ? HB_HEXZ_MINB3 : 2))
     k_hex_z(const HexArgs a, const ZRun run) {
   if (a.st && a.st->done) return;
@@ -466,11 +466,11 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
     for (int d = 0; d < D; ++d) fft::mbar_init(&full[d], 1);
     fft::fence_mbar_init();
   }
-  const bool mat_in_smem = a.n_phases * MS <= 2048;
-  if (mat_in_smem)
+  // MATS: the per-phase table lives in shared memory (the common case; a
+  // statically shared pointer keeps its loads LDS instead of generic LD)
+  if (MATS)
     for (int i = tid; i < a.n_phases * MS; i += nx) mat_s[i] = a.mat[i];
   __syncthreads();
-  const double* matp = mat_in_smem ? mat_s : a.mat;
   const int n_its = n_its_s;
   const int nunits = n_its * (KZ + 2);
   if (tid == 0)
@@ -489,16 +489,18 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
     for (int m = 0; m < 4; ++m) zc[k][m] = 0.0;
   }
   int u = 0;
+  int slot = 0, par = 0, pw = 0;  // ring slot u % D, its phase (u / D) & 1, producer warp u % nw
 #pragma unroll 1
   for (int it = 0; it < n_its; ++it) {
     const int info = its[it];
     const int y = info & 0xffff, zb = (info >> 16) & 0x7fff;
     const bool warm = info < 0;
+    // output node (x, y) of plane zb*KZ, component 0; + zi*plane + k*np
+    double* orow = a.out + ((int64_t)zb * KZ * a.n1 + y) * nx + x;
 #pragma unroll 1
     for (int j = 0; j < KZ + 2; ++j, ++u) {
-      const int slot = u % D;
       unsigned char* sl = ring + slot * sb;
-      fft::mbar_wait(&full[slot], (u / D) & 1);
+      fft::mbar_wait(&full[slot], par);
       const double* rows = reinterpret_cast<const double*>(sl);
       double Up[C][4], ucur[C];
 #pragma unroll
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
         for (int k = 0; k < C; ++k)
 #pragma unroll
           for (int m = 0; m < 4; ++m) A[k][m] = zc[k][m];
-        const double* mat = matp + ph * MS;
+        const double* mat = (MATS ? mat_s : a.mat) + ph * MS;
         if constexpr (QT && C == 3) {
 #pragma unroll
           for (int k = 0; k < C; ++k)
@@ -603,10 +605,14 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
         for (int m = 0; m < 4; ++m) lo_s[(k * 4 + m) * nx + x] = Up[k][m];
       __syncthreads();  // edges visible; ring slot fully read
       // producer role rotates over the warps (spreads the issue cost)
-      if (tid == ((u % nw) << 5) && u + D < nunits) z_issue<C, KZ>(a, its, u + D, sl, &full[slot]);
+      if (tid == (pw << 5) && u + D < nunits) z_issue<C, KZ>(a, its, u + D, sl, &full[slot]);
+      pw = pw + 1 == nw ? 0 : pw + 1;
+      if (++slot == D) {
+        slot = 0;
+        par ^= 1;
+      }
       if (j >= 2) {
         const int zi = j - 2;
-        const int z = zb * KZ + zi;
         const double* eg = edge + ((u & 1) * nw + (warp == 0 ? nw - 1 : warp - 1)) * C * 2;
 #pragma unroll
         for (int k = 0; k < C; ++k) {
@@ -619,7 +625,7 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
           double* yb = ybuf + (zi * C + k) * nx + x;
           if (!warm) {
             const double val = a.scale * (rowy + *yb);
-            a.out[k * np + (int64_t)z * plane + (int64_t)y * nx + x] = val;
+            orow[k * np + zi * plane] = val;
             dotacc = fma(uprev[k], val, dotacc);
           }
           *yb = rowy1;
@@ -847,8 +853,18 @@ bool hex_fast_tables(const Grid& g, int n_phases, const double* cmats, std::vect
   return all_iso;
 }
 
+template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT = false, bool MATS = true>
+static void launch_hex_z_nx_m(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s);
+
 template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT = false>
 static void launch_hex_z_nx(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
+  constexpr int MS = QT ? 3 : mat_stride<C, ISO>();
+  if (n_phases * MS <= 2048) launch_hex_z_nx_m<C, ISO, KZ, FE, NXT, QT, true>(g, a, n_phases, s);
+  else launch_hex_z_nx_m<C, ISO, KZ, FE, NXT, QT, false>(g, a, n_phases, s);
+}
+
+template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT, bool MATS>
+static void launch_hex_z_nx_m(const Grid& g, const HexArgs& a, int n_phases, cudaStream_t s) {
   constexpr int MS = QT ? 3 : mat_stride<C, ISO>();
   const int nx = g.n2, nw = nx / 32;
   const int rows_total = g.n1 * (g.n0 / KZ);
@@ -857,7 +873,7 @@ static void launch_hex_z_nx(const Grid& g, const HexArgs& a, int n_phases, cudaS
     const int cap = 2 * per + 4;
     size_t b = (size_t)kZDepth * zslot_bytes<C>(nx) + sizeof(double) * ((size_t)KZ * C * nx + 4 * C * nx + 2 * nw * C * 2) +
                sizeof(uint64_t) * kZDepth + sizeof(int) * ((cap + 1) & ~1);
-    if (n_phases * MS <= 2048) b += sizeof(double) * (size_t)n_phases * MS;
+    if (MATS) b += sizeof(double) * (size_t)n_phases * MS;
     return b;
   };
   static int sms = 0;
@@ -867,20 +883,20 @@ static void launch_hex_z_nx(const Grid& g, const HexArgs& a, int n_phases, cudaS
     HB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   }
   size_t smem = smem_for(2 * sms);
-  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT, QT, MATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hex_z<C, ISO, KZ, FE, NXT, QT>, nx, smem));
+  HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hex_z<C, ISO, KZ, FE, NXT, QT, MATS>, nx, smem));
   if (per_sm < 1) per_sm = 1;
   int grid = per_sm * sms;
   if (grid > rows_total) grid = rows_total;
   if (grid > kRedBlocks) grid = kRedBlocks;
   smem = smem_for(grid);
-  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT, QT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HB_CUDA(cudaFuncSetAttribute(k_hex_z<C, ISO, KZ, FE, NXT, QT, MATS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ZRun run;
   run.rows_total = rows_total;
   run.grid = grid;
   run.list_cap = 2 * ((rows_total + grid - 1) / grid) + 4;
-  k_hex_z<C, ISO, KZ, FE, NXT, QT><<<grid, nx, smem, s>>>(a, run);
+  k_hex_z<C, ISO, KZ, FE, NXT, QT, MATS><<<grid, nx, smem, s>>>(a, run);
 }
 
 template <int C, bool ISO, int KZ, bool FE>

@@ -93,9 +93,10 @@ __global__ void __launch_bounds__(kBlock) k_apply_elem(const Grid g, const ElemA
         a0 = e & 1; a1 = (e >> 1) & 1;
       }
       const int64_t eidx = flat(w0[1 - a0], w1[1 - a1], w2[1 - a2]);
-      // slab mode: the element below plane 0 lives on the previous rank
-      const bool elo = D == 3 && g.dist && c0 - a0 < 0;
-      const int ph = elo ? a.ph_lo[(int64_t)w1[1 - a1] * g.n2 + w2[1 - a2]] : a.phase[eidx];
+      // slab mode: the element below plane (2-D: row) 0 lives on the previous rank
+      const bool elo = g.dist && c0 - a0 < 0;
+      const int ph = elo ? a.ph_lo[D == 3 ? (int64_t)w1[1 - a1] * g.n2 + w2[1 - a2] : (int64_t)w1[1 - a1]]
+                         : a.phase[eidx];
       const double* row = ke + (size_t)ph * NE * NE + (size_t)(e * C) * NE;
 #pragma unroll
       for (int j = 0; j < NL; ++j) {
@@ -109,12 +110,12 @@ __global__ void __launch_bounds__(kBlock) k_apply_elem(const Grid g, const ElemA
         // slab mode: node planes -1 / n0 come from the halo planes (exchanged, or a peer's field)
         const double* ub = a.u;
         int64_t cs = np, ni = nidx;
-        if (D == 3 && g.dist) {
+        if (g.dist) {
           const int z = c0 - a0 + b0;
           if (z < 0 || z >= g.n0) {
             ub = z < 0 ? a.halo_lo : a.halo_hi;
             cs = a.halo_cs ? a.halo_cs : (int64_t)g.n1 * g.n2;
-            ni = (int64_t)w1[1 - a1 + b1] * g.n2 + w2[1 - a2 + b2];
+            ni = D == 3 ? (int64_t)w1[1 - a1 + b1] * g.n2 + w2[1 - a2 + b2] : (int64_t)w1[1 - a1 + b1];
           }
         }
 #pragma unroll

@@ -136,7 +136,9 @@ struct SpecParams {
   int iso;              // C_ref isotropic: K_hat = (lam + mu) M + mu tr(M) I (c = d) / kappa tr(M)
   double lam, mu;       // isotropic reference moduli (mu = kappa for c = 1)
   const double4* tab[3];  // per axis: (sin, cos, sin(t/2), cos(t/2))
-  int n1r, k1off;         // 3-D: axis-1 rows held (n1, or a slab rank's n1/W) and the first one's k1
+  int n1r, k1off;         // 3-D: axis-1 rows held (n1, or a slab rank's n1/W) and the first one's k1;
+                          // 2-D slab: k1off = first half-spectrum column held (nh = columns held)
+  int nhv;                // valid last-axis spectrum length N_last/2 + 1 (2-D slab chunks are padded)
   // division-free Gram factors (set_gram_factors): cd[a] = 8 w / h_a^2,
   // co[a][b] = 4 w / (h_a h_b)
   double cd[3], co[3][3];

@@ -61,7 +61,9 @@ __global__ void __launch_bounds__(kBlock) k_spectral(const __grid_constant__ Spe
     double2 z[C];
     int f[3];
     freq_index<D>(p, k, f);
-    if (f[0] == 0 && f[1] == 0 && f[2] == 0) {  // zero frequency (a slab rank may not hold it)
+    if ((f[0] == 0 && f[1] == 0 && f[2] == 0) ||  // zero frequency (a slab rank may not hold it)
+        f[D - 1] >= p.nhv) {                       // padding column of a 2-D slab chunk
+
 #pragma unroll
       for (int i = 0; i < C; ++i) z[i] = make_double2(0.0, 0.0);
     } else {

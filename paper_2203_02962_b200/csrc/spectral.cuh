@@ -18,9 +18,9 @@ __device__ __forceinline__ void freq_index(const SpecParams& p, int64_t k, int (
       const unsigned t0 = t / n1r;
       f[1] = p.k1off + (int)(t - t0 * n1r);
       f[0] = (int)t0;
-    } else {
+    } else {  // 2-D: k1off = the first column held (a slab rank's column chunk; 0 on one device)
       const unsigned t = kk / nh;
-      f[1] = (int)(kk - t * nh);
+      f[1] = p.k1off + (int)(kk - t * nh);
       f[0] = (int)t;
       f[2] = 0;
     }
@@ -32,7 +32,7 @@ __device__ __forceinline__ void freq_index(const SpecParams& p, int64_t k, int (
     f[1] = p.k1off + (int)(t % p.n1r);
     f[0] = (int)(t / p.n1r);
   } else {
-    f[1] = (int)(k % p.nh);
+    f[1] = p.k1off + (int)(k % p.nh);
     f[0] = (int)(k / p.nh);
     f[2] = 0;
   }

@@ -1,13 +1,16 @@
 """Slab-decomposed solves over several GPUs of one node.
 
 One process per GPU (torchrun / torch.distributed for the rendezvous only).
-Rank r of G owns planes [r n0/G, (r+1) n0/G) of axis 0. The library's slab
+Rank r of G owns planes (2-D: rows) [r n0/G, (r+1) n0/G) of axis 0. The library's slab
 context (homfe_gpu_create_dist) does the data-path exchanges itself with NCCL
 over NVLink / NVSwitch:
 
-  * K p: one halo plane from each neighbour (ring), before every stencil;
-  * M^-1: pass 1 (per plane) -> all-to-all of k1 rows -> pass 2 (per axis-0
-    pencil, spectral solve) -> all-to-all back -> pass 3 (per plane);
+  * K p: one halo plane (row) from each neighbour (ring), before every stencil;
+  * M^-1 (3-D): pass 1 (per plane) -> all-to-all of k1 rows -> pass 2 (per
+    axis-0 pencil, spectral solve) -> all-to-all back -> pass 3 (per plane);
+  * M^-1 (2-D, c5): 1-D r2c along axis 1 of the owned rows -> all-to-all of
+    half-spectrum column chunks (ceil(nh / G) each, the last padded) -> 1-D
+    c2c along axis 0 + spectral solve on the owned columns -> back;
   * p.Ap, r.z, means and norms: all-reductions of per-rank fixed-order sums.
 
 The exchange patterns and the transposed layouts are restated in numpy in
@@ -73,6 +76,31 @@ class slab_layout:
         return (me - q) * chunk
 
 
+class slab_layout_2d:
+    """2-D row slabs (csrc/context.cu, d == 2 slab spectra): the half
+    spectrum's nh = n1/2 + 1 columns are split into G chunks of
+    nhl = ceil(nh / G) (the last one zero-padded); S[c][i0l][k1 < G nhl] on the
+    row owner, W[c][i0][k1l] on the column owner (k1 = owner * nhl + k1l)."""
+
+    def __init__(self, c, n0, n1, world):
+        self.c, self.n0, self.n1, self.world = c, n0, n1, world
+        self.nzl = n0 // world
+        self.nh = n1 // 2 + 1
+        self.nhl = (self.nh + world - 1) // world
+
+    def owner(self, k1):
+        return k1 // self.nhl
+
+    def s_index(self, comp, i0l, k1):
+        return (comp * self.nzl + i0l) * (self.world * self.nhl) + k1
+
+    def w_index(self, comp, i0, k1l):
+        return (comp * self.n0 + i0) * self.nhl + k1l
+
+    def valid(self, k1):
+        return k1 < self.nh
+
+
 def nccl_unique_id():
     buf = (C.c_uint8 * 128)()
     _check(lib.homfe_nccl_unique_id(C.cast(buf, C.c_void_p)))
@@ -91,11 +119,12 @@ class SlabContext:
 
     def __init__(self, grid: Grid, components, rank, world, nccl_id: bytes, device=0):
         desc = _native.GridDesc()
+        from . import STENCILS
         desc.dim = grid.dim
-        desc.stencil = 3
+        desc.stencil = STENCILS[grid.stencil]
         for a in range(3):
-            desc.dims[a] = grid.dims[a]
-            desc.lengths[a] = grid.lengths[a]
+            desc.dims[a] = grid.dims[a] if a < grid.dim else 1
+            desc.lengths[a] = grid.lengths[a] if a < grid.dim else 1.0
         desc.components = components
         desc.device = device
         idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
@@ -105,7 +134,7 @@ class SlabContext:
         self.grid, self.c, self.rank, self.world = grid, components, rank, world
         self.m = grid.dim if components == 1 else mandel_dim(grid.dim)
         self.z0, self.nz = slab_range(grid.dims[0], rank, world)
-        self.n_local = self.nz * grid.dims[1] * grid.dims[2]
+        self.n_local = self.nz * int(np.prod(grid.dims[1:]))
 
     @property
     def transport(self):

@@ -158,3 +158,99 @@ def test_slab_ranges_and_halos_match_reference_wrap(oracle_mod):
             prev_last = (((z0 - 1) % n0) * 4) * 4
             assert nbr[prev_last, 4] // 16 == z0 and lo == (z0 - 1) % n0
         assert covered == list(range(n0))
+
+
+def _worker_2d(rank, world, port, out):
+    """2-D row slabs (c5): halo rows and the half-spectrum column-chunk
+    transposes of the slab spectra (csrc/context.cu d == 2, slabfft.cu with a
+    unit last axis), restated with dist.slab_layout_2d: row r2c on the owner,
+    padded column chunks exchanged, axis-0 transform on the column owner ==
+    numpy rfft2 of the global field on those columns; and back."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2203_02962_b200.dist import halo_planes, slab_layout_2d, slab_range
+    rng = np.random.default_rng(11)
+    c, n0, n1 = 1, 12, 10
+    glob = rng.standard_normal((c, n0, n1))
+    z0, nz = slab_range(n0, rank, world)
+    local = glob[:, z0:z0 + nz]
+    # halo rows
+    prev, nxt = (rank - 1) % world, (rank + 1) % world
+    hlo = torch.zeros(c * n1, dtype=torch.float64)
+    hhi = torch.zeros(c * n1, dtype=torch.float64)
+    first = torch.from_numpy(np.ascontiguousarray(local[:, 0]).ravel())
+    last = torch.from_numpy(np.ascontiguousarray(local[:, -1]).ravel())
+    if world == 1:
+        hhi.copy_(first)
+        hlo.copy_(last)
+    else:
+        reqs = [dist.isend(first, prev), dist.isend(last, nxt), dist.irecv(hhi, nxt), dist.irecv(hlo, prev)]
+        for r in reqs:
+            r.wait()
+    lo_g, hi_g = halo_planes(n0, rank, world)
+    ok_halo = np.array_equal(hlo.numpy().reshape(c, n1), glob[:, lo_g]) and \
+        np.array_equal(hhi.numpy().reshape(c, n1), glob[:, hi_g])
+    # forward: row r2c into padded S, pack per destination, exchange
+    L = slab_layout_2d(c, n0, n1, world)
+    S = np.zeros(c * nz * world * L.nhl, dtype=np.complex128)
+    rows = np.fft.rfft(local, axis=2)  # (c, nz, nh)
+    for comp in range(c):
+        for i0l in range(nz):
+            for k1 in range(L.nh):
+                S[L.s_index(comp, i0l, k1)] = rows[comp, i0l, k1]
+    chunk = c * nz * L.nhl
+    send = []
+    for q in range(world):
+        buf = np.zeros(chunk, dtype=np.complex128)
+        for comp in range(c):
+            for i0l in range(nz):
+                for k1l in range(L.nhl):
+                    buf[(comp * nz + i0l) * L.nhl + k1l] = S[L.s_index(comp, i0l, q * L.nhl + k1l)]
+        send.append(buf)
+    recv = _exchange(send, world)
+    W = np.zeros(c * n0 * L.nhl, dtype=np.complex128)
+    for q in range(world):
+        for comp in range(c):
+            for i0l in range(nz):
+                for k1l in range(L.nhl):
+                    W[L.w_index(comp, q * nz + i0l, k1l)] = recv[q][(comp * nz + i0l) * L.nhl + k1l]
+    Wf = np.fft.fft(W.reshape(c, n0, L.nhl), axis=1)
+    full = np.fft.rfft2(glob, axes=(1, 2))
+    ok_fwd = True
+    for k1l in range(L.nhl):
+        k1 = rank * L.nhl + k1l
+        if L.valid(k1):
+            ok_fwd &= np.allclose(Wf[:, :, k1l], full[:, :, k1], rtol=0, atol=1e-12)
+        else:
+            ok_fwd &= np.array_equal(Wf[:, :, k1l], np.zeros((c, n0)))  # padding stays zero
+    # inverse: axis-0 inverse on the columns, exchange back, row c2r
+    Wi = np.fft.ifft(Wf, axis=1).reshape(-1)
+    send = []
+    for q in range(world):
+        buf = np.zeros(chunk, dtype=np.complex128)
+        for comp in range(c):
+            for i0l in range(nz):
+                for k1l in range(L.nhl):
+                    buf[(comp * nz + i0l) * L.nhl + k1l] = Wi[L.w_index(comp, q * nz + i0l, k1l)]
+        send.append(buf)
+    recv = _exchange(send, world)
+    S2 = np.zeros((c, nz, world * L.nhl), dtype=np.complex128)
+    for q in range(world):
+        for comp in range(c):
+            for i0l in range(nz):
+                S2[comp, i0l, q * L.nhl:(q + 1) * L.nhl] = recv[q][(comp * nz) * L.nhl + i0l * L.nhl:
+                                                                    (comp * nz) * L.nhl + (i0l + 1) * L.nhl]
+    back = np.fft.irfft(S2[:, :, :L.nh], n=n1, axis=2)
+    ok_inv = np.allclose(back, local, rtol=0, atol=1e-12)
+    out[rank] = (bool(ok_halo), bool(ok_fwd), bool(ok_inv))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_slab_2d_exchanges_gloo(world):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_2d, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        assert out[r] == (True, True, True), (r, out[r])

@@ -125,3 +125,79 @@ def test_slab_multi_rank_in_process_matches_single_device(hb, world, dims, c, tr
         assert _rel(out["average_stress"], ref["average_stress"]) < 1e-12
     # 1e-10 (north_star): the slab spectra use 2-D + 1-D cuFFT plans instead of one 3-D plan
     assert _rel(uu, ref["u"]) < 1e-10
+
+
+@pytest.mark.parametrize("world,n,c,transport", [
+    (1, 256, 1, "single"), (2, 256, 1, "peer_pull"), (4, 512, 1, "all_to_all"), (8, 1024, 1, "peer_pull"),
+    (8, 1024, 1, "all_to_all"), (2, 128, 2, "peer_pull"), (4, 256, 2, "all_to_all")])
+def test_slab_2d_rows_match_single_device(hb, world, n, c, transport, monkeypatch):
+    """2-D row slabs (c5 on 1 and 8 GPUs, BASELINE configs[4]): halo rows for
+    K, 1-D r2c along axis 1 of the owned rows, all-to-all of half-spectrum
+    column chunks (padded to G ceil(nh / G)), 1-D c2c along axis 0 and the
+    spectral solve on the owned columns. W ranks in-process on one GPU
+    against the single-device context (2-D cuFFT, warp-strip K)."""
+    import threading
+    from paper_2203_02962_b200 import dist, inputs
+    monkeypatch.setenv("HOMFE_P2P", "1" if transport == "peer_pull" else "0")
+    dims = (n, n)
+    ph, _ = inputs.rsa_balls(dims, radius=12.0 * n / 256, seed=BASE_2D_SEED, fraction=0.30)
+    if c == 1:
+        cm = np.stack([np.eye(2), 1e3 * np.eye(2)])
+        e = [1.0, 0.0]
+        kw = dict(eta_cg=1e-8, reference="volume-mean")
+    else:
+        cm = np.stack([hb.isotropic_stiffness(0.8333, 0.3846, 2), hb.isotropic_stiffness(555.5, 416.7, 2)])
+        e = [0.0, 0.0, np.sqrt(2.0) * 0.01]
+        kw = dict(eta_cg=1e-8, reference="explicit", reference_matrix=cm[0])
+    g = hb.Grid(dims, [1.0, 1.0], "two-triangles")
+    mats = [hb.Material(t, c == 1, 2) for t in cm]
+    single = hb.Solver(g, mats, ph, **kw)
+    ref = single.solve(e)
+    rng = np.random.default_rng(3)
+    u = rng.uniform(-1, 1, (c, g.num_nodes))
+    ku_ref = hb.apply_operator(g, cm[np.repeat(ph, 2)], u)
+    r = u - u.mean(axis=1, keepdims=True)
+    cref = cm[0] if c > 1 else (np.bincount(ph, minlength=2)[:, None, None] * cm).sum(0) / ph.size
+    z_ref = hb.apply_preconditioner(g, hb.assemble_preconditioner(g, cref, c), r)
+    row = n
+    gid = 5000 + world * 10 + c + (0 if transport != "all_to_all" else 500) + n
+    res = [None] * world
+    errors = []
+
+    def rank_main(rank):
+        try:
+            ident = dist.sim_group_id(gid) if world > 1 else dist.nccl_unique_id()
+            sc = dist.SlabContext(g, c, rank, world, ident)
+            assert sc.transport == transport, sc.transport
+            sl = slice(sc.z0 * row, (sc.z0 + sc.nz) * row)
+            sc.set_material(cm, ph[sl])
+            ku = sc.apply_K(u[:, sl])
+            sc.set_reference(cref)
+            z = sc.apply_minv(r[:, sl])
+            out = sc.solve(e, single.cfg)
+            res[rank] = (sl, ku, z, out)
+        except Exception as ex:  # noqa: BLE001
+            errors.append(repr(ex))
+
+    threads = [threading.Thread(target=rank_main, args=(k,)) for k in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not errors, errors
+    ku = np.zeros_like(u)
+    z = np.zeros_like(u)
+    uu = np.zeros_like(u)
+    for sl, kl, zl, out in res:
+        ku[:, sl], z[:, sl], uu[:, sl] = kl, zl, out["u"]
+    # the slab K is the generic node-centric kernel, the single device's the warp-strip one
+    assert _rel(ku, ku_ref) < 1e-13, _rel(ku, ku_ref)
+    assert _rel(z, z_ref) < 1e-13, _rel(z, z_ref)
+    for sl, kl, zl, out in res:
+        assert out["converged"]
+        assert abs(out["report"]["steps"][0]["cg_iterations"] - ref["report"]["steps"][0]["cg_iterations"]) <= 1
+        assert _rel(out["average_stress"], ref["average_stress"]) < 1e-10
+    assert _rel(uu, ref["u"]) < 1e-8
+
+
+BASE_2D_SEED = 2203025
