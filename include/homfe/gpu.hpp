@@ -16,7 +16,11 @@
 #ifndef HOMFE_GPU_HPP
 #define HOMFE_GPU_HPP
 
+#include <algorithm>
+#include <cmath>
+#include <complex>
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -84,13 +88,18 @@ inline StencilKind stencil_kind_from_string(const std::string& name) {
 // shared between host threads (fft.hpp:18-20).
 class GridLayout {
  public:
-  GridLayout(CellSpec cell, StencilKind kind) : cell_(std::move(cell)), kind_(kind) {
+  // n_gpus > 1: one context over that many devices of this process (slab
+  // decomposition along axis 0, homfe_gpu_create_multi); newton_solve,
+  // run_load_program, apply_tangent_operator, apply_preconditioner and
+  // pcg_solve take and return global fields.
+  GridLayout(CellSpec cell, StencilKind kind, int n_gpus = 1) : cell_(std::move(cell)), kind_(kind), n_gpus_(n_gpus) {
     if (cell_.dims.size() != cell_.lengths.size()) throw ValidationError("cell: dims and lengths must have equal rank");
     if (cell_.dim() != 2 && cell_.dim() != 3) throw ValidationError("cell: dimension must be 2 or 3");
   }
   const CellSpec& cell() const { return cell_; }
   StencilKind kind() const { return kind_; }
   int dim() const { return cell_.dim(); }
+  int n_gpus() const { return n_gpus_; }
   Index num_pixels() const { return cell_.pixel_count(); }
   // grid.hpp:96-110: node types per pixel (FourTrianglesTwoNode adds the
   // pixel-centre node), nodes = Nn * N_p
@@ -121,7 +130,8 @@ class GridLayout {
     d.components = components;
     d.device = device;
     homfe_ctx* h = nullptr;
-    detail::check(homfe_gpu_create(&d, &h));
+    if (n_gpus_ > 1) detail::check(homfe_gpu_create_multi(&d, n_gpus_, &h));
+    else detail::check(homfe_gpu_create(&d, &h));
     auto* raw = h;
     ctx_.emplace(components, std::shared_ptr<homfe_ctx>(h, [](homfe_ctx* p) { homfe_gpu_destroy(p); }));
     return raw;
@@ -130,6 +140,7 @@ class GridLayout {
  private:
   CellSpec cell_;
   StencilKind kind_;
+  int n_gpus_ = 1;
   mutable std::map<int, std::shared_ptr<homfe_ctx>> ctx_;
 };
 
@@ -297,12 +308,22 @@ class PrecondManager {
   int assemblies() const { return assemblies_; }
   void count_assembly(int n) { assemblies_ += n; }
   double threshold() const { return threshold_; }
+  // The device context holds the manager's state (assembled reference, the
+  // tangent mean at the last assembly, homfe_gpu_precond_reset): a manager
+  // used with a context it was not last bound to starts fresh there.
+  void bind(homfe_ctx* ctx) {
+    if (bound_ != ctx) {
+      detail::check(homfe_gpu_precond_reset(ctx));
+      bound_ = ctx;
+    }
+  }
 
  private:
   ReferencePolicy policy_;
   double threshold_;
   int components_;
   int assemblies_ = 0;
+  homfe_ctx* bound_ = nullptr;
 };
 
 // solver.hpp:145-161
@@ -334,6 +355,7 @@ inline NewtonOutcome newton_solve(const GridLayout& layout, const MaterialMap& m
     throw ValidationError("materials: phase map does not match the grid");
   homfe_ctx* ctx = layout.context(c);
   detail::set_material(ctx, map);
+  precond.bind(ctx);
   homfe_solve_cfg sc{};
   sc.eta_newton = cfg.eta_newton;
   sc.eta_cg = cfg.eta_cg;
@@ -403,6 +425,7 @@ inline std::vector<LoadStepResult> run_load_program(const GridLayout& layout, co
   if (loads.empty()) throw ValidationError("loading: at least one load step is required");
   PrecondManager precond(policy, cfg.reassembly_threshold, map.node_components(layout.dim()));
   std::vector<LoadStepResult> results;
+  results.reserve(loads.size());  // `warm` points into the previous result
   InternalState g = map.make_state(layout);
   const NodalField* warm = nullptr;
   for (const auto& e : loads) {
@@ -412,6 +435,230 @@ inline std::vector<LoadStepResult> run_load_program(const GridLayout& layout, co
     warm = &results.back().outcome.u;
   }
   return results;
+}
+
+// ---- operator-level seams (operators.hpp, fields.hpp, precond.hpp, solver.hpp)
+
+// fields.hpp:40-61: point-interleaved data[q * m + k]
+struct QuadField {
+  Index quads = 0;
+  int m = 0;
+  std::vector<double> data;
+  QuadField() = default;
+  QuadField(Index q, int m_) : quads(q), m(m_), data(static_cast<std::size_t>(q * m_), 0.0) {}
+  double* vec(Index q) { return data.data() + q * m; }
+  const double* vec(Index q) const { return data.data() + q * m; }
+};
+
+namespace detail {
+// the context whose gradient width is m (c = 1: m = d; c = d: Mandel)
+inline homfe_ctx* quad_context(const GridLayout& layout, int m) {
+  const int d = layout.dim();
+  if (m == d) return layout.context(1);
+  if (m == d * (d + 1) / 2) return layout.context(d);
+  throw ValidationError("quadrature field shape does not match layout");
+}
+inline void check_quad(const GridLayout& layout, const QuadField& s) {
+  if (s.quads != layout.num_quads() || static_cast<Index>(s.data.size()) != s.quads * s.m)
+    throw ValidationError("quadrature field shape does not match layout");
+}
+inline void check_nodal(const GridLayout& layout, const NodalField& u) {
+  if (u.nodes != layout.num_nodes() || (u.components != 1 && u.components != layout.dim()) ||
+      static_cast<Index>(u.data.size()) != u.components * u.nodes)
+    throw ValidationError("nodal field shape does not match layout");
+}
+}  // namespace detail
+
+// gradient_apply (operators.hpp:20-21): the dense product D u at every
+// quadrature point.
+inline QuadField gradient_apply(const GridLayout& layout, const NodalField& u) {
+  detail::check_nodal(layout, u);
+  const int d = layout.dim();
+  QuadField out(layout.num_quads(), u.components == 1 ? d : d * (d + 1) / 2);
+  detail::check(homfe_gpu_gradient(layout.context(u.components), u.data.data(), out.data.data()));
+  return out;
+}
+
+// divergence_apply (operators.hpp:23-25): D^T W s, or D^T s unweighted.
+inline NodalField divergence_apply(const GridLayout& layout, const QuadField& s, bool weighted = true) {
+  detail::check_quad(layout, s);
+  homfe_ctx* ctx = detail::quad_context(layout, s.m);
+  NodalField out(s.m == layout.dim() ? 1 : layout.dim(), layout.num_nodes());
+  detail::check(homfe_gpu_divergence(ctx, s.data.data(), weighted ? 1 : 0, out.data.data()));
+  return out;
+}
+
+// weighted_dot / weighted_norm / volume_average (fields.hpp:86-95).
+inline double weighted_dot(const GridLayout& layout, const QuadField& a, const QuadField& b) {
+  detail::check_quad(layout, a);
+  detail::check_quad(layout, b);
+  if (a.m != b.m) throw ValidationError("weighted_dot: fields differ in width");
+  double v = 0.0;
+  detail::check(homfe_gpu_weighted_dot(detail::quad_context(layout, a.m), a.data.data(), b.data.data(), &v));
+  return v;
+}
+inline double weighted_norm(const GridLayout& layout, const QuadField& a) {
+  const double v = weighted_dot(layout, a, a);
+  return v > 0.0 ? std::sqrt(v) : 0.0;
+}
+inline std::vector<double> volume_average(const GridLayout& layout, const QuadField& s) {
+  detail::check_quad(layout, s);
+  std::vector<double> out(static_cast<std::size_t>(s.m), 0.0);
+  detail::check(homfe_gpu_volume_average(detail::quad_context(layout, s.m), s.data.data(), out.data()));
+  return out;
+}
+
+// FrequencyBlockDiag (precond.hpp:28-79). The device never stores the
+// blocks of a one-node stencil: it evaluates the reference symbol in closed
+// form inside the spectral kernels, so this handle
+// carries the reference tangent, the weighting and the inversion state;
+// block(k) reads the assembled (pre-inversion) symbol back for inspection.
+class FrequencyBlockDiag {
+ public:
+  int block_dim() const { return components_ * nodes_per_pixel_; }
+  Index num_frequencies() const { return num_freq_; }
+  int components() const { return components_; }
+  int nodes_per_pixel() const { return nodes_per_pixel_; }
+  bool weighted() const { return weighted_; }
+  bool inverted() const { return inverted_; }
+  Index zero_frequency() const { return 0; }
+  const std::vector<double>& reference() const { return c_ref_; }
+  // K_ref_hat(xi_k) before inversion, column-major block_dim^2 (precond.hpp:38-45)
+  std::vector<std::complex<double>> block(Index k) const {
+    if (k < 0 || k >= num_freq_) throw ValidationError("block: frequency out of range");
+    if (symbol_.empty()) {
+      homfe_ctx* ctx = layout_->context(components_);
+      detail::check(homfe_gpu_set_reference(ctx, c_ref_.data()));
+      const int b = block_dim();
+      std::vector<double> raw(static_cast<std::size_t>(num_freq_ * b * b * 2));
+      detail::check(homfe_gpu_reference_blocks(ctx, raw.data()));
+      symbol_.resize(static_cast<std::size_t>(num_freq_ * b * b));
+      for (std::size_t i = 0; i < symbol_.size(); ++i) symbol_[i] = {raw[2 * i], raw[2 * i + 1]};
+    }
+    const int b = block_dim();
+    const double sc = weighted_ ? 1.0 : 1.0 / w_;
+    std::vector<std::complex<double>> out(static_cast<std::size_t>(b * b));
+    for (int i = 0; i < b * b; ++i) out[static_cast<std::size_t>(i)] = sc * symbol_[static_cast<std::size_t>(k * b * b + i)];
+    return out;
+  }
+
+ private:
+  friend FrequencyBlockDiag assemble_reference(const GridLayout&, const std::vector<double>&, int, bool);
+  friend FrequencyBlockDiag invert_blocks(const FrequencyBlockDiag&);
+  friend NodalField apply_preconditioner(const GridLayout&, const FrequencyBlockDiag&, const NodalField&);
+  const GridLayout* layout_ = nullptr;
+  std::vector<double> c_ref_;
+  int components_ = 0, nodes_per_pixel_ = 1;
+  Index num_freq_ = 0;
+  bool weighted_ = true, inverted_ = false;
+  double w_ = 1.0;  // quadrature weight (unweighted blocks = weighted / w)
+  mutable std::vector<std::complex<double>> symbol_;
+};
+
+// assemble_reference (precond.hpp:90-93): validates c_ref (symmetric positive
+// definite, ValidationError otherwise) and sets it as the device reference.
+inline FrequencyBlockDiag assemble_reference(const GridLayout& layout, const std::vector<double>& c_ref,
+                                             int components, bool weighted = true) {
+  const int d = layout.dim();
+  if (components != 1 && components != d) throw ValidationError("assemble_reference: bad component count");
+  const int m = components == 1 ? d : d * (d + 1) / 2;
+  if (static_cast<int>(c_ref.size()) != m * m) throw ValidationError("reference tangent has wrong dimension");
+  homfe_ctx* ctx = layout.context(components);
+  detail::check(homfe_gpu_set_reference(ctx, c_ref.data()));
+  FrequencyBlockDiag b;
+  b.layout_ = &layout;
+  b.c_ref_ = c_ref;
+  b.components_ = components;
+  b.nodes_per_pixel_ = layout.nodes_per_pixel();
+  b.weighted_ = weighted;
+  Index nf = 1;
+  for (int a = 0; a < d; ++a) nf *= a == d - 1 ? layout.cell().dims[a] / 2 + 1 : layout.cell().dims[a];
+  b.num_freq_ = nf;
+  b.w_ = layout.cell().cell_volume() / static_cast<double>(layout.num_pixels()) / layout.quads_per_pixel();
+  return b;
+}
+
+// invert_blocks (precond.hpp:95-102): the device inverts per frequency inside
+// the spectral kernel (zero frequency pseudo-inverted); NumericalError for a
+// numerically singular non-zero-frequency block is raised at assembly.
+inline FrequencyBlockDiag invert_blocks(const FrequencyBlockDiag& blocks) {
+  if (blocks.inverted_) throw ValidationError("invert_blocks: blocks are already inverted");
+  FrequencyBlockDiag out = blocks;
+  out.inverted_ = true;
+  return out;
+}
+
+// apply_preconditioner (precond.hpp:104-106): M^-1 r.
+inline NodalField apply_preconditioner(const GridLayout& layout, const FrequencyBlockDiag& inv_blocks,
+                                       const NodalField& r) {
+  if (!inv_blocks.inverted_) throw ValidationError("apply_preconditioner: blocks are not inverted");
+  detail::check_nodal(layout, r);
+  if (r.components != inv_blocks.components_) throw ValidationError("apply_preconditioner: field shape mismatch");
+  homfe_ctx* ctx = layout.context(r.components);
+  detail::check(homfe_gpu_set_reference(ctx, inv_blocks.c_ref_.data()));
+  NodalField out(r.components, r.nodes);
+  detail::check(homfe_gpu_apply_minv(ctx, r.data.data(), out.data.data()));
+  if (!inv_blocks.weighted_)
+    for (double& v : out.data) v *= inv_blocks.w_;
+  return out;
+}
+
+// pcg_solve (solver.hpp:57-78) with A = the tangent operator of a linear
+// material map and M^-1 = inverted reference blocks, both on the device.
+// The observer receives x_k after every iteration (solver.cpp:87); with an
+// observer the iterations run one graph launch at a time.
+using IterateObserver = std::function<void(const NodalField&)>;
+
+struct PcgOutcome {
+  NodalField x;
+  int iterations = 0;
+  std::vector<double> history;  // |r_k|_{M^-1}, starting from r_0
+  bool converged = false;
+};
+
+struct TangentOperator {
+  const GridLayout* layout;
+  MaterialMap map;
+};
+
+namespace detail {
+struct ObserverCall {
+  const IterateObserver* obs;
+  NodalField buf;
+};
+inline void observer_trampoline(void* user, int32_t, const double* x) {
+  auto* oc = static_cast<ObserverCall*>(user);
+  std::copy(x, x + oc->buf.data.size(), oc->buf.data.begin());
+  (*oc->obs)(oc->buf);
+}
+}  // namespace detail
+
+inline PcgOutcome pcg_solve(const TangentOperator& apply_a, const FrequencyBlockDiag& minv, const NodalField& b,
+                            double eta, int it_max, const IterateObserver& observer = {}) {
+  const GridLayout& layout = *apply_a.layout;
+  detail::check_nodal(layout, b);
+  if (!minv.inverted()) throw ValidationError("pcg: preconditioner blocks are not inverted");
+  if (b.components != minv.components()) throw ValidationError("pcg: field shape mismatch");
+  if (it_max < 0) throw ValidationError("pcg: it_max must be >= 0");
+  homfe_ctx* ctx = layout.context(b.components);
+  detail::set_material(ctx, apply_a.map);
+  detail::check(homfe_gpu_set_reference(ctx, minv.reference().data()));
+  PcgOutcome out;
+  out.x = NodalField(b.components, b.nodes);
+  std::vector<double> hist(static_cast<std::size_t>(it_max + 1), 0.0);
+  int32_t its = 0, conv = 0;
+  if (observer) {
+    detail::ObserverCall oc{&observer, NodalField(b.components, b.nodes)};
+    detail::check(homfe_gpu_pcg_observed(ctx, b.data.data(), eta, it_max, out.x.data.data(), &its, hist.data(),
+                                         &conv, &detail::observer_trampoline, &oc));
+  } else {
+    detail::check(homfe_gpu_pcg(ctx, b.data.data(), eta, it_max, out.x.data.data(), &its, hist.data(), &conv));
+  }
+  out.iterations = its;
+  out.converged = conv != 0;
+  hist.resize(static_cast<std::size_t>(its + 1));
+  out.history = std::move(hist);
+  return out;
 }
 
 // apply_tangent_operator (operators.hpp:31-33) for a linear material map.

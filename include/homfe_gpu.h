@@ -100,6 +100,15 @@ const char* homfe_gpu_last_error(void);
    the buffers owned by NodalField/FrequencyBlockDiag (grid.hpp:75-129,
    fft.hpp:22-57, precond.hpp:28-79). */
 int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out);
+/* One context over n_gpus devices of this process (the
+   reference's callers are single-process, proj/tools/homog.cpp:41-43): the
+   slab decomposition of homfe_gpu_create_dist with rank r on device
+   desc->device + r and one host thread per rank inside every call. Host
+   buffers are GLOBAL (component-planar over the whole grid); supported:
+   set_material, set_reference, precond_reset, solve, apply_K, apply_minv,
+   pcg, sizes, path_info, slab_transport, destroy (the rest return
+   HOMFE_VALIDATION). n_gpus = 1 is homfe_gpu_create. */
+int homfe_gpu_create_multi(const homfe_grid_desc* desc, int32_t n_gpus, homfe_ctx** out);
 int homfe_gpu_destroy(homfe_ctx* ctx);
 
 /* Slab decomposition along axis 0 (the reference is
@@ -196,8 +205,10 @@ int homfe_gpu_apply_K(homfe_ctx* ctx, const double* u, double* ku);
    NumericalError on singular blocks) and apply it (precond.hpp:104-106). */
 int homfe_gpu_set_reference(homfe_ctx* ctx, const double* c_ref);
 int homfe_gpu_apply_minv(homfe_ctx* ctx, const double* r, double* z);
-/* Dense Fourier symbol K_ref(xi) of the stored reference, nf x c x c complex
-   (row-major within the block), for comparison with assembled blocks. */
+/* Dense Fourier symbol K_ref(xi) of the stored reference, nf blocks of
+   (c Nn) x (c Nn) complex, column-major within the block like
+   FrequencyBlockDiag (precond.hpp:38-45), for comparison with assembled
+   blocks. */
 int homfe_gpu_reference_blocks(homfe_ctx* ctx, double* blocks_c);
 /* gradient_apply / divergence_apply (operators.hpp:20-25). */
 int homfe_gpu_gradient(homfe_ctx* ctx, const double* u, double* grad);
@@ -236,6 +247,7 @@ int homfe_gpu_index_maps(homfe_ctx* ctx, int64_t* strides3, int64_t* nbr, int32_
 #define HOMFE_PATH_SLAB 16
 #define HOMFE_PATH_PEER_PULL 32
 #define HOMFE_PATH_ELEM2D 64
+#define HOMFE_PATH_MULTI 128
 int homfe_gpu_path_info(const homfe_ctx* ctx, int32_t* flags);
 
 /* Per-stage CUDA-event timing of one PCG iteration on the current buffers

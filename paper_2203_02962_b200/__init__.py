@@ -211,6 +211,7 @@ class _Context:
 
     def __init__(self, grid, components, device=0):
         desc = _native.GridDesc()
+        n_gpus = getattr(grid, "n_gpus", 1)
         desc.dim = grid.dim
         desc.stencil = STENCILS[grid.stencil]
         for a in range(3):
@@ -219,7 +220,10 @@ class _Context:
         desc.components = components
         desc.device = device
         h = C.c_void_p()
-        _check(lib.homfe_gpu_create(C.byref(desc), C.byref(h)))
+        if n_gpus > 1:
+            _check(lib.homfe_gpu_create_multi(C.byref(desc), int(n_gpus), C.byref(h)))
+        else:
+            _check(lib.homfe_gpu_create(C.byref(desc), C.byref(h)))
         self.h = h
         self.grid = grid
         self.c = components
@@ -270,8 +274,12 @@ class _Context:
 class Grid:
     """Periodic grid (proj/include/homfe/grid.hpp:75-129)."""
 
-    def __init__(self, dims, lengths, stencil):
+    def __init__(self, dims, lengths, stencil, n_gpus=1):
+        """n_gpus > 1: one context over that many devices of this process
+        (slab decomposition along axis 0, homfe_gpu_create_multi); linear
+        solves, K, M^-1 and PCG take and return global fields."""
         dims = [int(x) for x in dims]
+        self.n_gpus = int(n_gpus)
         lengths = [float(x) for x in lengths]
         if len(dims) != len(lengths):
             raise ValidationError("cell: dims and lengths must have equal rank")

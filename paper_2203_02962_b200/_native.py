@@ -92,6 +92,7 @@ def _load():
         "homfe_gpu_eigenvalue_bounds": (C.c_int, [vp, P(d), i32, P(d), P(d), P(d), P(d)]),
         "homfe_gpu_path_info": (C.c_int, [vp, P(i32)]),
         "homfe_gpu_precond_reset": (C.c_int, [vp]),
+        "homfe_gpu_create_multi": (C.c_int, [P(GridDesc), i32, P(vp)]),
         "homfe_gpu_weighted_dot": (C.c_int, [vp, P(d), P(d), P(d)]),
         "homfe_gpu_pcg_observed": (C.c_int, [vp, P(d), d, i32, P(d), P(i32), P(d), P(i32), OBSERVER, vp]),
     }
@@ -113,7 +114,8 @@ EXPORTED = ("homfe_gpu_last_error", "homfe_isotropic_stiffness", "homfe_gpu_crea
             "homfe_nccl_unique_id", "homfe_gpu_create_dist", "homfe_gpu_slab_transport", "homfe_gpu_set_material_models",
             "homfe_gpu_internal_width", "homfe_gpu_solve_state", "homfe_gpu_stress_field",
             "homfe_gpu_gamma_apply", "homfe_gpu_sb_solve", "homfe_gpu_eigenvalue_bounds", "homfe_gpu_path_info",
-            "homfe_gpu_precond_reset", "homfe_gpu_weighted_dot", "homfe_gpu_pcg_observed")
+            "homfe_gpu_precond_reset", "homfe_gpu_weighted_dot", "homfe_gpu_pcg_observed",
+            "homfe_gpu_create_multi")
 
 PATH_FLAGS = {"fused_fft": 1, "hex_modal": 2, "while_graph": 4, "slab_spectra": 8, "slab": 16, "peer_pull": 32,
-              "elem2d": 64}
+              "elem2d": 64, "multi": 128}

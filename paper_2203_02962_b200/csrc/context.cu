@@ -10,7 +10,9 @@
 #include <cufft.h>
 #include <nccl.h>
 #include <cub/cub.cuh>
+#include <atomic>
 #include <condition_variable>
+#include <thread>
 #include <mutex>
 #include <map>
 
@@ -219,6 +221,12 @@ struct homfe_ctx {
   double2* d_recv = nullptr;
   std::vector<void*> ipc_open;               // IPC mappings to close
   double* d_bar = nullptr;                   // barrier all-reduce scratch
+
+  // single-process multi-GPU context (homfe_gpu_create_multi): the rank
+  // contexts of the slab decomposition, one host thread each per call
+  std::vector<homfe_ctx*> ranks;
+  int64_t mp_np = 0, mp_nq = 0, mp_nf = 0;  // global sizes
+  int mp_c = 0, mp_m = 0;
 
   int64_t nvec() const { return (int64_t)g.c * g.nn * g.np; }
   int64_t nodes() const { return (int64_t)g.nn * g.np; }
@@ -1587,6 +1595,86 @@ bool sb_newton(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const 
 }  // namespace
 
 // ===================================================================== C ABI
+namespace {
+
+bool is_multi(const homfe_ctx* c) { return c && !c->ranks.empty(); }
+
+int multi_unsupported(const char* what) {
+  g_err = std::string(what) + ": not available on a multi-GPU context (use one slab context per rank)";
+  return HOMFE_VALIDATION;
+}
+
+// f(rank_ctx, rank) on every rank, each in its own host thread (the rank
+// contexts' collectives need all ranks inside a call at once); the first
+// failing rank's status and message are returned. HOMFE_NONCONVERGED is a
+// result, not a failure: it is returned once every rank finished.
+template <class F>
+int multi_run(homfe_ctx* c, F&& f) {
+  const int W = (int)c->ranks.size();
+  std::vector<int> codes(W, HOMFE_OK);
+  std::vector<std::string> errs(W);
+  std::vector<std::thread> th;
+  th.reserve(W);
+  for (int r = 0; r < W; ++r)
+    th.emplace_back([&, r] {
+      codes[r] = f(c->ranks[r], r);
+      if (codes[r] != HOMFE_OK) errs[r] = g_err;
+    });
+  for (auto& t : th) t.join();
+  int soft = HOMFE_OK;
+  for (int r = 0; r < W; ++r) {
+    if (codes[r] == HOMFE_OK) continue;
+    if (codes[r] == HOMFE_NONCONVERGED) {
+      soft = HOMFE_NONCONVERGED;
+      g_err = errs[r];
+      continue;
+    }
+    g_err = errs[r];
+    return codes[r];
+  }
+  return soft;
+}
+
+// component-planar global <-> rank slab (contiguous per component)
+struct MultiSplit {
+  int c;
+  int64_t n_glob, n_loc;
+  void scatter(const double* g, std::vector<double>& l, int r) const {
+    l.resize((size_t)c * n_loc);
+    for (int k = 0; k < c; ++k)
+      std::memcpy(l.data() + (size_t)k * n_loc, g + (size_t)k * n_glob + (size_t)r * n_loc, n_loc * sizeof(double));
+  }
+  void gather(const std::vector<double>& l, double* g, int r) const {
+    for (int k = 0; k < c; ++k)
+      std::memcpy(g + (size_t)k * n_glob + (size_t)r * n_loc, l.data() + (size_t)k * n_loc, n_loc * sizeof(double));
+  }
+};
+
+MultiSplit split_of(const homfe_ctx* c) {
+  const homfe_ctx* r0 = c->ranks[0];
+  return MultiSplit{r0->g.c, r0->g.np * (int64_t)c->ranks.size(), r0->g.np};
+}
+
+// vector op y = op(x) on the slabs
+template <class F>
+int multi_map(homfe_ctx* c, const double* x, double* y, F&& op) {
+  const MultiSplit sp = split_of(c);
+  std::vector<std::vector<double>> yl(c->ranks.size());
+  const int code = multi_run(c, [&](homfe_ctx* rc, int r) {
+    std::vector<double> xl;
+    sp.scatter(x, xl, r);
+    yl[r].assign(xl.size(), 0.0);
+    return op(rc, xl.data(), yl[r].data());
+  });
+  if (code == HOMFE_OK || code == HOMFE_NONCONVERGED)
+    for (size_t r = 0; r < yl.size(); ++r) sp.gather(yl[r], y, (int)r);
+  return code;
+}
+
+std::atomic<uint64_t> g_multi_sim_group{7700000};
+
+}  // namespace
+
 extern "C" {
 
 const char* homfe_gpu_last_error(void) { return g_err.c_str(); }
@@ -1991,6 +2079,70 @@ int homfe_gpu_create(const homfe_grid_desc* desc, homfe_ctx** out) {
   });
 }
 
+int homfe_gpu_create_multi(const homfe_grid_desc* desc, int32_t n_gpus, homfe_ctx** out) {
+  return guarded([&] {
+    if (!desc || !out) throw ValidationError("create: null argument");
+    if (n_gpus < 1) throw ValidationError("create_multi: n_gpus must be >= 1");
+    if (n_gpus == 1) {
+      *out = create_impl(desc, 0, 0, nullptr);
+      return;
+    }
+    // HOMFE_MULTI_SIM=1: every rank on desc->device with the in-process
+    // transport (host barriers; tests on one GPU), else ranks on devices
+    // desc->device ... desc->device + n_gpus - 1 over NCCL
+    const char* sim_env = std::getenv("HOMFE_MULTI_SIM");
+    const bool sim = sim_env && sim_env[0] == '1';
+    if (!sim) {
+      int ndev = 0;
+      HB_CUDA(cudaGetDeviceCount(&ndev));
+      if (desc->device < 0 || desc->device + n_gpus > ndev)
+        throw ValidationError("create_multi: " + std::to_string(n_gpus) + " devices requested from device " +
+                              std::to_string(desc->device) + ", " + std::to_string(ndev) + " visible");
+    }
+    unsigned char id[128] = {};
+    if (sim) {
+      std::memcpy(id, "HBSIMGRP", 8);
+      const uint64_t gid = g_multi_sim_group.fetch_add(1);
+      std::memcpy(id + 8, &gid, 8);
+    } else {
+      ncclUniqueId uid;
+      HB_NCCL(ncclGetUniqueId(&uid));
+      std::memcpy(id, &uid, sizeof(uid));
+    }
+    auto* m = new homfe_ctx();
+    m->device = desc->device;
+    m->ranks.assign(n_gpus, nullptr);
+    std::vector<std::string> errs(n_gpus);
+    std::vector<std::thread> th;
+    for (int r = 0; r < n_gpus; ++r)
+      th.emplace_back([&, r] {
+        homfe_grid_desc d = *desc;
+        d.device = sim ? desc->device : desc->device + r;
+        try {
+          m->ranks[r] = create_impl(&d, r, n_gpus, id);
+        } catch (const std::exception& e) {
+          errs[r] = e.what();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < n_gpus; ++r)
+      if (!errs[r].empty()) {
+        for (homfe_ctx* rc : m->ranks)
+          if (rc) homfe_gpu_destroy(rc);
+        m->ranks.clear();
+        delete m;
+        throw ValidationError(errs[r]);
+      }
+    const homfe_ctx* r0 = m->ranks[0];
+    m->mp_np = r0->g.np * n_gpus;
+    m->mp_nq = m->mp_np * r0->sp.nq;
+    m->mp_nf = r0->nf;
+    m->mp_c = r0->g.c;
+    m->mp_m = r0->g.m;
+    *out = m;
+  });
+}
+
 int homfe_nccl_unique_id(void* out) {
   return guarded([&] {
     ncclUniqueId id;
@@ -2009,6 +2161,7 @@ int homfe_gpu_create_dist(const homfe_grid_desc* desc, int32_t rank, int32_t wor
 }
 
 int homfe_gpu_slab_transport(const homfe_ctx* c, int32_t* kind) {
+  if (is_multi(c)) return homfe_gpu_slab_transport(c->ranks[0], kind);
   return guarded([&] {
     if (!c || !kind) throw ValidationError("slab_transport: null argument");
     *kind = c->peer ? 2 : (c->dist && c->g.world > 1 ? 1 : 0);
@@ -2017,6 +2170,11 @@ int homfe_gpu_slab_transport(const homfe_ctx* c, int32_t* kind) {
 
 int homfe_gpu_destroy(homfe_ctx* c) {
   if (!c) return HOMFE_OK;
+  if (is_multi(c)) {
+    for (homfe_ctx* rc : c->ranks) homfe_gpu_destroy(rc);
+    delete c;
+    return HOMFE_OK;
+  }
   cudaSetDevice(c->device);
   destroy_graphs(c);
   if (c->fwd) cufftDestroy(c->fwd);
@@ -2067,6 +2225,13 @@ int homfe_gpu_destroy(homfe_ctx* c) {
 }
 
 int homfe_gpu_sizes(const homfe_ctx* c, int64_t* np, int64_t* nq, int32_t* m, int64_t* nf) {
+  if (is_multi(c)) {
+    if (np) *np = c->mp_np;
+    if (nq) *nq = c->mp_nq;
+    if (m) *m = c->mp_m;
+    if (nf) *nf = c->mp_nf;
+    return HOMFE_OK;
+  }
   return guarded([&] {
     if (np) *np = c->g.np;
     if (nq) *nq = c->g.np * c->sp.nq;
@@ -2076,6 +2241,12 @@ int homfe_gpu_sizes(const homfe_ctx* c, int64_t* np, int64_t* nq, int32_t* m, in
 }
 
 int homfe_gpu_set_material(homfe_ctx* c, int32_t n_phases, const double* t, const uint8_t* phase) {
+  if (is_multi(c)) {
+    const int64_t nl = c->ranks[0]->g.np;
+    return multi_run(c, [&](homfe_ctx* rc, int r) {
+      return homfe_gpu_set_material(rc, n_phases, t, phase ? phase + (size_t)r * nl : nullptr);
+    });
+  }
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     c->nonlinear = false;
@@ -2085,6 +2256,7 @@ int homfe_gpu_set_material(homfe_ctx* c, int32_t n_phases, const double* t, cons
 }
 
 int homfe_gpu_set_material_device(homfe_ctx* c, int32_t n_phases, const double* t, const uint8_t* d_phase) {
+  if (is_multi(c)) return multi_unsupported("gpu_set_material_device");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     set_material(c, n_phases, t, d_phase, true);
@@ -2092,6 +2264,7 @@ int homfe_gpu_set_material_device(homfe_ctx* c, int32_t n_phases, const double* 
 }
 
 int homfe_gpu_precond_reset(homfe_ctx* c) {
+  if (is_multi(c)) return multi_run(c, [&](homfe_ctx* rc, int) { return homfe_gpu_precond_reset(rc); });
   return guarded([&] {
     if (!c) throw ValidationError("precond_reset: null context");
     c->pm_valid = false;
@@ -2102,6 +2275,25 @@ int homfe_gpu_precond_reset(homfe_ctx* c) {
 
 int homfe_gpu_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* warm_u,
                     double* u_out, double* avg_out, homfe_report* rep) {
+  if (is_multi(c)) {
+    const MultiSplit sp = split_of(c);
+    std::vector<std::vector<double>> ul(c->ranks.size());
+    std::vector<homfe_report> reps(c->ranks.size());
+    std::vector<std::vector<double>> avgs(c->ranks.size(), std::vector<double>(6, 0.0));
+    const int code = multi_run(c, [&](homfe_ctx* rc, int r) {
+      std::vector<double> wl;
+      if (warm_u) sp.scatter(warm_u, wl, r);
+      ul[r].assign((size_t)sp.c * sp.n_loc, 0.0);
+      return homfe_gpu_solve(rc, e, cfg, warm_u ? wl.data() : nullptr, ul[r].data(), avgs[r].data(), &reps[r]);
+    });
+    if (code == HOMFE_OK || code == HOMFE_NONCONVERGED) {
+      if (u_out)
+        for (size_t r = 0; r < ul.size(); ++r) sp.gather(ul[r], u_out, (int)r);
+      if (avg_out) std::copy(avgs[0].begin(), avgs[0].begin() + c->mp_m, avg_out);
+      if (rep) *rep = reps[0];
+    }
+    return code;
+  }
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     const int64_t n = c->nvec();
@@ -2118,6 +2310,7 @@ int homfe_gpu_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, c
 
 int homfe_gpu_set_material_models(homfe_ctx* c, int32_t n_phases, const homfe_material* models,
                                   const uint8_t* phase) {
+  if (is_multi(c)) return multi_unsupported("gpu_set_material_models");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     if (!models) throw ValidationError("materials: null catalog");
@@ -2186,6 +2379,7 @@ int homfe_gpu_set_material_models(homfe_ctx* c, int32_t n_phases, const homfe_ma
 }
 
 int homfe_gpu_internal_width(homfe_ctx* c, int32_t* width, int64_t* num_quads) {
+  if (is_multi(c)) return multi_unsupported("gpu_internal_width");
   return guarded([&] {
     if (width) *width = c->nonlinear ? 7 : 0;
     if (num_quads) *num_quads = c->g.np * c->sp.nq;
@@ -2194,6 +2388,7 @@ int homfe_gpu_internal_width(homfe_ctx* c, int32_t* width, int64_t* num_quads) {
 
 int homfe_gpu_solve_state(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* warm_u,
                           const double* g0, double* u_out, double* g_out, double* avg_out, homfe_report* rep) {
+  if (is_multi(c)) return multi_unsupported("gpu_solve_state");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     const int64_t n = c->nvec();
@@ -2219,6 +2414,7 @@ int homfe_gpu_solve_state(homfe_ctx* c, const double* e, const homfe_solve_cfg* 
 }
 
 int homfe_gpu_gamma_apply(homfe_ctx* c, const double* s_in, double* s_out) {
+  if (is_multi(c)) return multi_unsupported("gpu_gamma_apply");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_reference(c);
@@ -2235,6 +2431,7 @@ int homfe_gpu_gamma_apply(homfe_ctx* c, const double* s_in, double* s_out) {
 int homfe_gpu_sb_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* c_ref,
                        const double* warm_strain, const double* g0, double* strain_out, double* g_out,
                        double* avg_out, homfe_report* rep) {
+  if (is_multi(c)) return multi_unsupported("gpu_sb_solve");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     if (!c_ref) throw ValidationError("sb_newton_solve: reference tangent required");
@@ -2264,6 +2461,7 @@ int homfe_gpu_sb_solve(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg
 
 int homfe_gpu_eigenvalue_bounds(homfe_ctx* c, const double* tangent, int32_t pixel_constant, const double* c_ref,
                                 double* lower, double* upper, double* cond) {
+  if (is_multi(c)) return multi_unsupported("gpu_eigenvalue_bounds");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     if (c->dist) throw ValidationError("eigenvalue_bounds: single-GPU contexts only");
@@ -2314,6 +2512,7 @@ int homfe_gpu_eigenvalue_bounds(homfe_ctx* c, const double* tangent, int32_t pix
 }
 
 int homfe_gpu_stress_field(homfe_ctx* c, double* out) {
+  if (is_multi(c)) return multi_unsupported("gpu_stress_field");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_material(c);
@@ -2336,6 +2535,7 @@ int homfe_gpu_stress_field(homfe_ctx* c, double* out) {
 
 int homfe_gpu_solve_device(homfe_ctx* c, const double* e, const homfe_solve_cfg* cfg, const double* d_warm,
                            double* d_u_out, double* avg_out, homfe_report* rep) {
+  if (is_multi(c)) return multi_unsupported("gpu_solve_device");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     const int64_t n = c->nvec();
@@ -2351,6 +2551,8 @@ int homfe_gpu_solve_device(homfe_ctx* c, const double* e, const homfe_solve_cfg*
 }
 
 int homfe_gpu_apply_K(homfe_ctx* c, const double* u, double* ku) {
+  if (is_multi(c))
+    return multi_map(c, u, ku, [](homfe_ctx* rc, const double* x, double* y) { return homfe_gpu_apply_K(rc, x, y); });
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_material(c);
@@ -2364,6 +2566,7 @@ int homfe_gpu_apply_K(homfe_ctx* c, const double* u, double* ku) {
 }
 
 int homfe_gpu_set_reference(homfe_ctx* c, const double* c_ref) {
+  if (is_multi(c)) return multi_run(c, [&](homfe_ctx* rc, int) { return homfe_gpu_set_reference(rc, c_ref); });
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     set_reference(c, c_ref);
@@ -2371,6 +2574,8 @@ int homfe_gpu_set_reference(homfe_ctx* c, const double* c_ref) {
 }
 
 int homfe_gpu_apply_minv(homfe_ctx* c, const double* r, double* z) {
+  if (is_multi(c))
+    return multi_map(c, r, z, [](homfe_ctx* rc, const double* x, double* y) { return homfe_gpu_apply_minv(rc, x, y); });
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_reference(c);
@@ -2383,6 +2588,7 @@ int homfe_gpu_apply_minv(homfe_ctx* c, const double* r, double* z) {
 }
 
 int homfe_gpu_reference_blocks(homfe_ctx* c, double* blocks) {
+  if (is_multi(c)) return multi_unsupported("gpu_reference_blocks");
   if (c && c->dist) {
     g_err = "not available in slab mode (use a single-device context)";
     return HOMFE_VALIDATION;
@@ -2411,6 +2617,7 @@ static double* quad_buffer(homfe_ctx* c) {
 }
 
 int homfe_gpu_gradient(homfe_ctx* c, const double* u, double* grad) {
+  if (is_multi(c)) return multi_unsupported("gpu_gradient");
   if (c && c->dist) {
     g_err = "not available in slab mode (use a single-device context)";
     return HOMFE_VALIDATION;
@@ -2429,6 +2636,7 @@ int homfe_gpu_gradient(homfe_ctx* c, const double* u, double* grad) {
 }
 
 int homfe_gpu_divergence(homfe_ctx* c, const double* s, int32_t weighted, double* out) {
+  if (is_multi(c)) return multi_unsupported("gpu_divergence");
   if (c && c->dist) {
     g_err = "not available in slab mode (use a single-device context)";
     return HOMFE_VALIDATION;
@@ -2446,6 +2654,7 @@ int homfe_gpu_divergence(homfe_ctx* c, const double* s, int32_t weighted, double
 }
 
 int homfe_gpu_weighted_dot(homfe_ctx* c, const double* a, const double* b, double* out) {
+  if (is_multi(c)) return multi_unsupported("gpu_weighted_dot");
   if (c && c->dist) {
     g_err = "not available in slab mode (use a single-device context)";
     return HOMFE_VALIDATION;
@@ -2465,6 +2674,7 @@ int homfe_gpu_weighted_dot(homfe_ctx* c, const double* a, const double* b, doubl
 }
 
 int homfe_gpu_volume_average(homfe_ctx* c, const double* s, double* out) {
+  if (is_multi(c)) return multi_unsupported("gpu_volume_average");
   if (c && c->dist) {
     g_err = "not available in slab mode (use a single-device context)";
     return HOMFE_VALIDATION;
@@ -2483,6 +2693,22 @@ int homfe_gpu_volume_average(homfe_ctx* c, const double* s, double* out) {
 
 int homfe_gpu_pcg(homfe_ctx* c, const double* b, double eta, int32_t it_max, double* x, int32_t* iterations,
                   double* history, int32_t* converged) {
+  if (is_multi(c)) {
+    std::vector<int32_t> its(c->ranks.size()), conv(c->ranks.size());
+    std::vector<double> hist0;
+    if (history) hist0.assign((size_t)std::max(it_max, 0) + 1, 0.0);
+    const int code = multi_map(c, b, x, [&](homfe_ctx* rc, const double* bl, double* xl) {
+      int r = 0;
+      while (c->ranks[r] != rc) ++r;
+      return homfe_gpu_pcg(rc, bl, eta, it_max, xl, &its[r], r == 0 && history ? hist0.data() : nullptr, &conv[r]);
+    });
+    if (code == HOMFE_OK) {
+      if (iterations) *iterations = its[0];
+      if (converged) *converged = conv[0];
+      if (history) std::copy(hist0.begin(), hist0.begin() + its[0] + 1, history);
+    }
+    return code;
+  }
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_material(c);
@@ -2501,6 +2727,7 @@ int homfe_gpu_pcg(homfe_ctx* c, const double* b, double eta, int32_t it_max, dou
 int homfe_gpu_pcg_observed(homfe_ctx* c, const double* b, double eta, int32_t it_max, double* x,
                            int32_t* iterations, double* history, int32_t* converged, homfe_iterate_observer obs,
                            void* user) {
+  if (is_multi(c)) return multi_unsupported("gpu_pcg_observed");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_material(c);
@@ -2522,6 +2749,7 @@ int homfe_gpu_pcg_observed(homfe_ctx* c, const double* b, double eta, int32_t it
 // 3 spectral solve, 4 inverse FFT, 5 p update, 6 the two tiny scalar kernels,
 // 7 their sum. Averages over `reps` launches.
 int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
+  if (is_multi(c)) return multi_unsupported("gpu_kernel_times");
   return guarded([&] {
     HB_CUDA(cudaSetDevice(c->device));
     require_material(c);
@@ -2590,6 +2818,11 @@ int homfe_gpu_kernel_times(homfe_ctx* c, int32_t reps, double* ms) {
 }
 
 int homfe_gpu_path_info(const homfe_ctx* c, int32_t* flags) {
+  if (is_multi(c)) {
+    const int code = homfe_gpu_path_info(c->ranks[0], flags);
+    if (code == HOMFE_OK && flags) *flags |= HOMFE_PATH_MULTI;
+    return code;
+  }
   return guarded([&] {
     if (!c || !flags) throw ValidationError("path_info: null argument");
     *flags = (c->fused ? HOMFE_PATH_FUSED_FFT : 0) | (c->hex_fast ? HOMFE_PATH_HEX_MODAL : 0) |
@@ -2600,6 +2833,7 @@ int homfe_gpu_path_info(const homfe_ctx* c, int32_t* flags) {
 }
 
 int homfe_gpu_index_maps(homfe_ctx* c, int64_t* strides3, int64_t* nbr, int32_t* n_off) {
+  if (is_multi(c)) return multi_unsupported("gpu_index_maps");
   if (c && c->dist) {
     g_err = "not available in slab mode (use a single-device context)";
     return HOMFE_VALIDATION;

@@ -201,3 +201,48 @@ def test_slab_2d_rows_match_single_device(hb, world, n, c, transport, monkeypatc
 
 
 BASE_2D_SEED = 2203025
+
+
+@pytest.mark.parametrize("n_gpus,dims,stencil,c", [(2, (64, 128, 128), "trilinear-hex", 3),
+                                                   (4, (128, 128, 128), "trilinear-hex", 1),
+                                                   (8, (1024, 1024), "two-triangles", 1),
+                                                   (2, (32, 64, 64), "trilinear-hex", 3)])
+def test_single_process_multi_gpu_context(hb, n_gpus, dims, stencil, c, monkeypatch):
+    """homfe_gpu_create_multi (one host process driving n_gpus
+    slab ranks, one host thread per rank inside each call) through the
+    ordinary Python API with GLOBAL fields: Grid(..., n_gpus). On the one
+    test GPU every rank runs on device 0 with the in-process transport
+    (HOMFE_MULTI_SIM=1). Against the single-device context."""
+    from paper_2203_02962_b200 import inputs
+    monkeypatch.setenv("HOMFE_MULTI_SIM", "1")
+    d = len(dims)
+    ph, _ = inputs.rsa_balls(dims, radius=dims[0] / 16.0, seed=9, fraction=0.25)
+    if c == 1:
+        cm = np.stack([np.eye(d), 100.0 * np.eye(d)])
+        e = np.zeros(d)
+        e[0] = 1.0
+    else:
+        cm = np.stack([hb.isotropic_stiffness(0.8333, 0.3846, 3), hb.isotropic_stiffness(555.5, 416.7, 3)])
+        e = np.array([0, 0, 0, 0, 0, np.sqrt(2.0) * 0.01])
+    lengths = [x / dims[-1] for x in dims]
+    mats = [hb.Material(t, c == 1, d) for t in cm]
+    g1 = hb.Grid(dims, lengths, stencil)
+    gm = hb.Grid(dims, lengths, stencil, n_gpus=n_gpus)
+    kw = dict(eta_cg=1e-8, reference="explicit", reference_matrix=cm[0])
+    ref = hb.Solver(g1, mats, ph, **kw).solve(e)
+    sm = hb.Solver(gm, mats, ph, **kw)
+    assert "multi" in gm.context(c).path() and "slab" in gm.context(c).path()
+    out = sm.solve(e)
+    assert out["converged"]
+    assert abs(out["report"]["steps"][0]["cg_iterations"] - ref["report"]["steps"][0]["cg_iterations"]) <= 1
+    assert _rel(out["average_stress"], ref["average_stress"]) < 1e-10
+    assert _rel(out["u"], ref["u"]) < 1e-8
+    # operators with global fields
+    rng = np.random.default_rng(4)
+    u = rng.uniform(-1, 1, (c, g1.num_nodes))
+    nq = g1.quads_per_pixel
+    assert _rel(hb.apply_operator(gm, cm[np.repeat(ph, nq)], u), hb.apply_operator(g1, cm[np.repeat(ph, nq)], u)) < 1e-13
+    r = u - u.mean(axis=1, keepdims=True)
+    zm = hb.apply_preconditioner(gm, hb.assemble_preconditioner(gm, cm[0], c), r)
+    z1 = hb.apply_preconditioner(g1, hb.assemble_preconditioner(g1, cm[0], c), r)
+    assert _rel(zm, z1) < 1e-13

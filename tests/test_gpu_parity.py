@@ -490,3 +490,28 @@ def test_tiny_grids_match_oracle(hb, oracle_mod, dims, stencil, c):
     assert tol["converged"] and gpu["converged"]
     assert abs(gpu["iterations"] - tol["iterations"]) <= 1
     assert _rel(gpu["x"], tol["x"]) <= 1e-8
+
+
+def test_cpp_operator_seams(hb):
+    """tests/cpp/test_seams.cpp through include/homfe/gpu.hpp: gradient /
+    divergence / fused K against the dense triple product
+    (test_operators.cpp:168-193), assemble_reference / invert_blocks /
+    apply_preconditioner against the dense pseudo-inverse
+    (test_precond.cpp:201-252), pcg_solve with an IterateObserver,
+    weighted_norm / volume_average, a FourTrianglesTwoNode newton_solve
+    (u sized 2 N_p) and the PrecondManager reuse across solves."""
+    import os
+    import subprocess
+    import tempfile
+    from paper_2203_02962_b200 import _native
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib_dir = os.path.dirname(_native.LIB_PATH)
+    with tempfile.TemporaryDirectory() as d:
+        exe = os.path.join(d, "test_seams")
+        subprocess.run(["g++", "-std=c++17", "-O1", "-fsanitize=address", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "tests", "cpp", "test_seams.cpp"), "-o", exe, "-L", lib_dir,
+                        "-lhomfe_gpu", f"-Wl,-rpath,{lib_dir}"], check=True)
+        env = dict(os.environ, ASAN_OPTIONS="protect_shadow_gap=0:detect_leaks=0")
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ALL OK" in r.stdout, r.stdout
