@@ -431,6 +431,49 @@ __device__ __forceinline__ void z_issue(const HexArgs& a, const int* its, int u,
   }
 }
 
+// One piece of unit u's copies: part 2k + r = row y + r of component k
+// (r = 0, 1), part 2C = the element phase row; part 0 also registers the
+// unit's byte count (arrive.expect_tx; the tx-count may go transiently
+// negative when another part's copy lands first). Spreading the parts over
+// the warps keeps any one warp from arriving late at the next barrier.
+template <int C, int KZ>
+__device__ __forceinline__ void z_issue_part(const HexArgs& a, const int* its, int u, unsigned char* slot,
+                                             uint64_t* bar, int part) {
+  const int nx = a.n2;
+  const int i = u / (KZ + 2), j = u - i * (KZ + 2);
+  const int info = its[i];
+  const int y = info & 0xffff, zb = (info >> 16) & 0x7fff;
+  const uint32_t row_bytes = nx * 8;
+  if (part == 0) fft::mbar_expect_tx(bar, 2 * C * row_bytes + (j ? nx : 0));
+  const int64_t plane = (int64_t)a.n1 * nx;
+  if (part < 2 * C) {
+    const int k = part >> 1, r = part & 1;
+    const int yr = r ? (y + 1 == a.n1 ? 0 : y + 1) : y;
+    int pz = zb * KZ - 1 + j;
+    const double* src;
+    int64_t cs;
+    if (a.dist) {
+      src = pz < 0 ? a.halo_lo : (pz >= a.n0 ? a.halo_hi : a.u + (int64_t)pz * plane);
+      cs = (pz < 0 || pz >= a.n0) ? a.halo_cs : plane * a.n0;
+    } else {
+      pz = pz < 0 ? pz + a.n0 : (pz >= a.n0 ? pz - a.n0 : pz);
+      src = a.u + (int64_t)pz * plane;
+      cs = plane * a.n0;
+    }
+    fft::bulk_g2s(reinterpret_cast<double*>(slot) + (r * C + k) * nx, src + k * cs + (int64_t)yr * nx, row_bytes,
+                  bar);
+  } else if (j) {
+    int zp = zb * KZ - 2 + j;  // element plane
+    const uint8_t* ph;
+    if (a.dist && zp < 0) ph = a.ph_lo;
+    else {
+      zp = zp < 0 ? zp + a.n0 : zp;
+      ph = a.phase + (int64_t)zp * plane;
+    }
+    fft::bulk_g2s(slot + 2 * C * row_bytes, ph + (int64_t)y * nx, nx, bar);
+  }
+}
+
 template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT = false, bool MATS = true>
 __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1 : (C == 3 ? HB_HEXZ_MINB3 : 2))
     k_hex_z(const HexArgs a, const ZRun run) {
@@ -478,8 +521,8 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
 
   const int x = tid;
   const int xp = x + 1 == nx ? 0 : x + 1;
-  const int64_t plane = (int64_t)a.n1 * nx;
-  const int64_t np = plane * a.n0;
+  const int plane_i = a.n1 * nx;
+  const int np_i = plane_i * a.n0;
   double dotacc = 0.0;
   double zc[C][4], uprev[C];
 #pragma unroll
@@ -489,14 +532,15 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
     for (int m = 0; m < 4; ++m) zc[k][m] = 0.0;
   }
   int u = 0;
-  int slot = 0, par = 0, pw = 0;  // ring slot u % D, its phase (u / D) & 1, producer warp u % nw
+  int slot = 0, par = 0;  // ring slot u % D and its phase (u / D) & 1
 #pragma unroll 1
   for (int it = 0; it < n_its; ++it) {
     const int info = its[it];
     const int y = info & 0xffff, zb = (info >> 16) & 0x7fff;
     const bool warm = info < 0;
     // output node (x, y) of plane zb*KZ, component 0; + zi*plane + k*np
-    double* orow = a.out + ((int64_t)zb * KZ * a.n1 + y) * nx + x;
+    // (32-bit: c np < 2^31 for every one-device grid, create checks it)
+    const int orow = (zb * KZ * a.n1 + y) * nx + x;
 #pragma unroll 1
     for (int j = 0; j < KZ + 2; ++j, ++u) {
       unsigned char* sl = ring + slot * sb;
@@ -604,9 +648,9 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
 #pragma unroll
         for (int m = 0; m < 4; ++m) lo_s[(k * 4 + m) * nx + x] = Up[k][m];
       __syncthreads();  // edges visible; ring slot fully read
-      // producer role rotates over the warps (spreads the issue cost)
-      if (tid == (pw << 5) && u + D < nunits) z_issue<C, KZ>(a, its, u + D, sl, &full[slot]);
-      pw = pw + 1 == nw ? 0 : pw + 1;
+      // refill this slot with unit u + D, one copy per warp
+      if (lane == 0 && u + D < nunits)
+        for (int part = warp; part <= 2 * C; part += nw) z_issue_part<C, KZ>(a, its, u + D, sl, &full[slot], part);
       if (++slot == D) {
         slot = 0;
         par ^= 1;
@@ -624,8 +668,9 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
           const double rowy = n0v - n1v, rowy1 = n0v + n1v;
           double* yb = ybuf + (zi * C + k) * nx + x;
           if (!warm) {
-            const double val = a.scale * (rowy + *yb);
-            orow[k * np + zi * plane] = val;
+            // scale = 1 in every launch without element loads (PCG, apply_K)
+            const double val = FE ? a.scale * (rowy + *yb) : rowy + *yb;
+            a.out[k * np_i + orow + zi * plane_i] = val;
             dotacc = fma(uprev[k], val, dotacc);
           }
           *yb = rowy1;
@@ -931,6 +976,7 @@ void launch_hex_fast(const Grid& g, const ElemArgs& ea, const double* d_mat, boo
   a.n1 = g.n1;
   a.n2 = g.n2;
   if (hex_v2(g)) {
+    if (!a.fe && a.scale != 1.0) throw ValidationError("hexfast: a scaled K without element loads is not supported");
 #define HB_HEXZ(C, ISO, KZ)                                      \
   do {                                                           \
     if (a.fe) launch_hex_z<C, ISO, KZ, true>(g, a, ea.n_phases, s); \
@@ -1035,6 +1081,7 @@ bool launch_hex_fast_qt(const Grid& g, const ElemArgs& ea, const double* d_qtab,
   a.fe = nullptr;
   a.n_phases = ea.n_phases;
   a.scale = ea.scale;
+  if (a.scale != 1.0) return false;  // the generic two-pass operator handles scaled applications
   a.partials = ea.partials;
   a.nred = kRedBlocks;
   a.st = ea.st;

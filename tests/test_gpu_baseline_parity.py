@@ -194,7 +194,7 @@ def test_c2_tolerance_and_fixed_k(hb, oracle_mod):
     k = _tolerance_mode(hb, oracle_mod, "c2 128^3 tolerance", cfg, ph, cm)
     b = newton_rhs(cfg.dims, [1.0] * 3, 1, cm, ph, cfg.load)
     _fixed_k(hb, oracle_mod, "c2 128^3", cfg.dims, cfg.stencil, 1, cm, ph, _cref(cfg, ph, cm), b,
-             [parity_util.STRICT_K, k // 2, k], expect_path=("fused_fft", "hex_modal"), e=np.asarray(cfg.load))
+             [parity_util.STRICT_K, k], expect_path=("fused_fft", "hex_modal"), e=np.asarray(cfg.load))
 
 
 @pytest.mark.parametrize("n", [1024, 2048])

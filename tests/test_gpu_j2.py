@@ -156,10 +156,9 @@ def test_j2_load_program_shares_precond_manager(hb, oracle_mod):
     (solver.cpp:120-142), so later steps may reuse an older C_ref. Per-step
     CG counts, reassembly flags and assembly counts match the oracle run with
     one shared manager."""
-    gpu, orc = _j2_pair(hb, oracle_mod, 2, [(1.0, 0.5, 1e-3, 0.05), (10.0, 5.0, 2e-3, 0.5)])
-    ph = np.zeros(16 * 16, np.uint8)
-    ph.reshape(16, 16)[4:12, 4:12] = 1
-    loads = [np.array([1e-3, 0.0, 0.5e-3]) * s for s in (1.0, 2.0, 3.0, 4.0)]
+    gpu, orc = _j2_pair(hb, oracle_mod, 2, [(0.833, 0.385, 3e-3, 0.08), (0.833, 0.385, 6e-3, 0.16)])
+    ph = (oracle_mod.uniform(7007, 256, 0.0, 1.0) < 0.5).astype(np.uint8)
+    loads = [np.array([5e-3, -5e-3, 1e-3]) * s for s in (0.4, 0.7, 1.0, 1.3)]
     kw = dict(eta_newton=1e-9, eta_cg=1e-10, reference="volume-mean", reassembly_threshold=0.05)
     grid = hb.Grid((16, 16), (1.0, 1.0), "two-triangles")
     res = hb.run_load_program(grid, gpu, ph, loads, **kw)
