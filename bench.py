@@ -10,9 +10,10 @@ check, homogenized stress) with all inputs resident in HBM.
   e2e        the same metric through the public C ABI with HOST buffers:
              material upload (phase map H2D) + homfe_gpu_solve (u D2H) per
              step, host clock
-  roofline   the dominant kernel (K apply) of one PCG iteration, timed live
-             with CUDA events, algorithmic bytes (16c+1) N_p per launch
-             against MEASURED_PEAKS.json hbm_gbs
+  roofline   the dominant kernel of one PCG iteration (the largest live
+             CUDA-event time among K apply and the three fused FFT passes),
+             its algorithmic bytes per launch against
+             MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the CPU oracle (faithful restatement of the reference,
              single thread like the reference) on a bounded sample
 

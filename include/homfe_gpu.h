@@ -119,7 +119,9 @@ int homfe_gpu_destroy(homfe_ctx* ctx);
    halo planes, the FFT transposes and scalar all-reductions. Afterwards every
    host-buffer entry point (set_material, solve, apply_K, apply_minv, pcg)
    takes and returns this rank's slab; scalars (<sigma>, iteration counts) are
-   global. 3-d trilinear-hex grids with 128^2 / 256^2 planes. */
+   global. 3-d trilinear-hex grids (fused passes on 128^2 / 256^2 planes,
+   slab spectra through cuFFT on any other plane) and 2-d one-node pixel
+   stencils (row slabs along axis 0). */
 int homfe_nccl_unique_id(void* out128);
 int homfe_gpu_create_dist(const homfe_grid_desc* desc, int32_t rank, int32_t world, const void* nccl_id,
                           homfe_ctx** out);

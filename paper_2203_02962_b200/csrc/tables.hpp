@@ -3,8 +3,9 @@
 //
 // Stencil tables restate proj/src/grid.cpp:81-145 (BilinearQuad,
 // TwoTriangles) and 190-229 (TrilinearHex); the Mandel gradient rows restate
-// proj/src/operators.cpp:16-53. FourTrianglesTwoNode (two node types) is not
-// on the GPU path.
+// proj/src/operators.cpp:16-53. FourTrianglesTwoNode (grid.cpp:147-188, two
+// node types: corner and pixel centre) is kind 2 of make_stencil (SURVEY.md
+// section 8(f), row f3; its preconditioner blocks are probed in probe.cu).
 #pragma once
 
 #include <cmath>
