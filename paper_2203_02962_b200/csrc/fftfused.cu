@@ -533,9 +533,13 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
   constexpr int STAGE = C * BK * N0;  // double2 per stage
   if (a.st && !a.st->active) return;
   extern __shared__ double2 sm_raw[];
-  double2* sm = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(sm_raw) + 127) & ~uintptr_t(127));
+  // 128-byte alignment by pointer arithmetic on the shared symbol itself (an
+  // integer round trip would make every stage access a generic LD/ST)
+  double2* sm = reinterpret_cast<double2*>(reinterpret_cast<unsigned char*>(sm_raw) +
+                                           ((128u - (fft::smem_u32(sm_raw) & 127u)) & 127u));
   double2* stage0 = sm;             // [2][C][NGB][N0][kTG]  (128-B aligned: TMA tensor stores)
   double2* tws = sm + 2 * STAGE;
+  double2* t12 = tws + N0;  // [n1] (sin, sin(t/2)) of axes 1 and 2 (square planes: one table)
   __shared__ __align__(8) uint64_t full[2];
   const int tid = threadIdx.x, g = tid / TPF, t = tid % TPF;
   const int j = g % BK, comp = g / BK;
@@ -570,6 +574,11 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     if ((int)(blockIdx.x + gridDim.x) < ntiles) issue(blockIdx.x + gridDim.x, 1);
   }
   for (int i = tid; i < N0; i += NT) tws[i] = a.tw[i];
+  if (sp.kind == 3)
+    for (int i = tid; i < a.n1; i += NT) {
+      const double4 tv = sp.tab[1][i];
+      t12[i] = make_double2(tv.x, tv.z);
+    }
   // per-column symbol factors (hex, k0-independent parts) and the axis-0 table
   __shared__ double colf[BK][6];
   __shared__ double3 ax0[N0];
@@ -593,16 +602,17 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     }
     if (sp.kind == 3 && tid < BK) {
       // M(k0) = diag(cf0 sh0^2, cf1 S2_0, cf2 S2_0) + offdiag(cf3 sn0, cf4 sn0, cf5 S2_0)
+      // (shared-memory table and the host's division-free Gram factors: the
+      // other warps wait for these four threads at the next block barrier)
       const int k2 = min(c0 + tid, P - 1);
-      const double4 t1 = sp.tab[1][k1], t2 = sp.tab[2][k2];
-      const double S21 = 2.0 - (4.0 / 3.0) * t1.z * t1.z, S22 = 2.0 - (4.0 / 3.0) * t2.z * t2.z;
-      const double w = sp.w, h0 = sp.h[0], h1 = sp.h[1], h2 = sp.h[2];
-      colf[tid][0] = 8.0 * w / (h0 * h0) * S21 * S22;
-      colf[tid][1] = 8.0 * w * t1.z * t1.z / (h1 * h1) * S22;
-      colf[tid][2] = 8.0 * w * t2.z * t2.z / (h2 * h2) * S21;
-      colf[tid][3] = 4.0 * w * t1.x / (h0 * h1) * S22;
-      colf[tid][4] = 4.0 * w * t2.x / (h0 * h2) * S21;
-      colf[tid][5] = 4.0 * w * t1.x * t2.x / (h1 * h2);
+      const double2 t1 = t12[k1], t2 = t12[k2];
+      const double S21 = 2.0 - (4.0 / 3.0) * t1.y * t1.y, S22 = 2.0 - (4.0 / 3.0) * t2.y * t2.y;
+      colf[tid][0] = sp.cd[0] * S21 * S22;
+      colf[tid][1] = sp.cd[1] * t1.y * t1.y * S22;
+      colf[tid][2] = sp.cd[2] * t2.y * t2.y * S21;
+      colf[tid][3] = sp.co[0][1] * t1.x * S22;
+      colf[tid][4] = sp.co[0][2] * t2.x * S21;
+      colf[tid][5] = sp.co[1][2] * t1.x * t2.x;
     }
     __syncthreads();  // raw stage reads done (stage becomes the FFT buffers); colf, tws ready
     double2* buf = stg;               // [C][BK][N0]
@@ -794,7 +804,7 @@ void run_pencils_c(const FusedFft& f, const SpecParams& sp, const PcgState* st, 
   a.nred = kRedBlocks;
   a.dbg = f.dbg;
   const int ntiles = a.L.n1l * a.ntk;
-  const size_t smem = sizeof(double2) * (2 * (size_t)C * BK * N0 + N0) + 128;
+  const size_t smem = sizeof(double2) * (2 * (size_t)C * BK * N0 + N0 + f.np_plane) + 128;
   HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   static int grid_cap[2] = {0, 0};  // resident blocks of this instantiation (persistent grid)
   int& cap = grid_cap[C == 3];
