@@ -353,6 +353,17 @@ __global__ void __launch_bounds__(NP, HB_INV_MINB) k_plane_inv(const __grid_cons
     for (int i = 0; i < 16; ++i) rows[jc * (NP + 1) + 32 * warp + 2 * i + yo] = v[i];
   }
   __syncthreads();
+#ifndef HB_INV_PREFETCH
+#define HB_INV_PREFETCH 1
+#endif
+  if (HB_INV_PREFETCH && a.mode == kModePcg && tid < 64 && !(a.dbg & 256)) {
+    // pull this CTA's p and x rows into L2 while the transforms run, so the
+    // update at the end of each transform group hits L2
+    const int64_t pl = (int64_t)comp * a.np + (int64_t)i0 * NP * NP + (int64_t)rank * 32 * NP + (int64_t)(tid & 31) * NP;
+    const double* src = (tid < 32 ? a.p : a.x) + pl;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"((uint32_t)(NP * sizeof(double)))
+                 : "memory");
+  }
   double2* cbuf = rows + g * (NP + 1);
   fft::fft4step<NP, true>(cbuf, t, tws);
   __syncthreads();
