@@ -250,6 +250,7 @@ int homfe_gpu_index_maps(homfe_ctx* ctx, int64_t* strides3, int64_t* nbr, int32_
 #define HOMFE_PATH_PEER_PULL 32
 #define HOMFE_PATH_ELEM2D 64
 #define HOMFE_PATH_MULTI 128
+#define HOMFE_PATH_SMALL2D 256 /* whole PCG loop in one persistent 16-CTA cluster (256^2 scalar) */
 int homfe_gpu_path_info(const homfe_ctx* ctx, int32_t* flags);
 
 /* Per-stage CUDA-event timing of one PCG iteration on the current buffers

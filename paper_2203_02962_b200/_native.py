@@ -118,4 +118,4 @@ EXPORTED = ("homfe_gpu_last_error", "homfe_isotropic_stiffness", "homfe_gpu_crea
             "homfe_gpu_create_multi")
 
 PATH_FLAGS = {"fused_fft": 1, "hex_modal": 2, "while_graph": 4, "slab_spectra": 8, "slab": 16, "peer_pull": 32,
-              "elem2d": 64, "multi": 128}
+              "elem2d": 64, "multi": 128, "small2d": 256}

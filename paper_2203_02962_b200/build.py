@@ -20,7 +20,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include")]
-SOURCES = ["kernels.cu", "spectral.cu", "hexfast.cu", "fftfused.cu", "quad2d.cu", "j2.cu", "probe.cu", "slabfft.cu", "context.cu"]
+SOURCES = ["kernels.cu", "spectral.cu", "hexfast.cu", "fftfused.cu", "quad2d.cu", "j2.cu", "probe.cu", "slabfft.cu", "small2d.cu", "context.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "tables.hpp", "hex_modes.inc", "spectral.cuh", "fft.cuh"]
 
 

@@ -190,6 +190,8 @@ struct homfe_ctx {
   double graph_eta = -1.0;
   int graph_itmax = -1;
   bool use_while = true;
+  bool small2d = false;            // persistent one-cluster PCG (small2d.cu) allowed
+  double2* d_tw256 = nullptr;      // its W_256 four-step table
   bool body_eager = false;
   cudaGraphExec_t body_exec = nullptr;  // fallback: one iteration per launch
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -892,14 +894,28 @@ PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history,
   }
   write_state(c, eta, it_max);
   HB_CUDA(cudaEventRecord(c->ev0, c->stream));
-  if (c->use_while) {
+  bool ran = false;
+  if (c->small2d && !obs && !c->nl_op && c->have_ref && small2d_eligible(c->g, c->n_phases)) {
+    // the whole loop (init, iterations) in one persistent cluster
+    ran = launch_pcg_small2d(c->spp, c->d_x, c->d_r, c->d_p, c->d_phase, c->d_tri, c->n_phases, c->d_tw256,
+                             c->d_st, c->d_hist, c->stream);
+    if (ran) {
+      capture_tail(c, c->stream);
+      c->launches += 4;
+    } else {
+      c->small2d = false;
+    }
+  }
+  if (ran) {
+  } else if (c->use_while) {
     if (!c->pcg_exec) {
       if (!build_while_graph(c)) {
         c->use_while = false;  // fall back to a host-driven loop of one-iteration graphs
       }
     }
   }
-  if (c->use_while && !obs) {
+  if (ran) {
+  } else if (c->use_while && !obs) {
     HB_CUDA(cudaGraphLaunch(c->pcg_exec, c->stream));
   } else {
     capture_init(c, c->stream);
@@ -948,7 +964,7 @@ PcgResult run_pcg(homfe_ctx* c, double eta, int it_max, double* h_history,
   res.last_history = hist.back();
   if (h_history) std::copy(hist.begin(), hist.end(), h_history);
   const int body_kernels = c->fused ? 6 : 8;
-  c->launches += (int64_t)res.iterations * body_kernels + 8;
+  if (!ran) c->launches += (int64_t)res.iterations * body_kernels + 8;
   return res;
 }
 
@@ -1991,6 +2007,20 @@ homfe_ctx* create_impl(const homfe_grid_desc* desc, int rank, int world, const v
       }
       ctx->slab_fft = true;
     }
+    if (!dist && g.d == 2 && g.c == 1 && g.kind == 1 && g.nn == 1 && g.n0 == 256 && g.n1 == 256) {
+      const char* e2 = std::getenv("HOMFE_SMALL2D");
+      if (!(e2 && e2[0] == '0')) {
+        std::vector<double2> tw;  // four-step layout tw[k2 * 16 + n1] = W_256^{n1 k2} (fft.cuh)
+        for (int k2 = 0; k2 < 16; ++k2)
+          for (int n1 = 0; n1 < 16; ++n1) {
+            const double t = -2.0 * M_PI * (double)(n1 * k2) / 256.0;
+            tw.push_back(make_double2(std::cos(t), std::sin(t)));
+          }
+        ctx->d_tw256 = dalloc<double2>(tw.size());
+        HB_CUDA(cudaMemcpy(ctx->d_tw256, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+        ctx->small2d = true;
+      }
+    }
     if (fused_ok && (dist || !(fenv && fenv[0] == '0'))) {
       const int n1 = g.n1, n0 = g.n0g;
       // twiddles: N <= 256 in the four-step layout tw[k2 * (N/16) + n1] =
@@ -2197,6 +2227,7 @@ int homfe_gpu_destroy(homfe_ctx* c) {
     if (t) cudaFree(t);
   if (c->d_spec) cudaFree(c->d_spec);
   if (c->d_tw) cudaFree(c->d_tw);
+  if (c->d_tw256) cudaFree(c->d_tw256);
   if (c->d_spec2) cudaFree(c->d_spec2);
   if (c->d_spec_r) cudaFree(c->d_spec_r);
   if (c->d_spec2_r) cudaFree(c->d_spec2_r);
@@ -2828,7 +2859,8 @@ int homfe_gpu_path_info(const homfe_ctx* c, int32_t* flags) {
     *flags = (c->fused ? HOMFE_PATH_FUSED_FFT : 0) | (c->hex_fast ? HOMFE_PATH_HEX_MODAL : 0) |
              (c->use_while ? HOMFE_PATH_WHILE_GRAPH : 0) | (c->slab_fft ? HOMFE_PATH_SLAB_SPECTRA : 0) |
              (c->dist ? HOMFE_PATH_SLAB : 0) | (c->peer ? HOMFE_PATH_PEER_PULL : 0) |
-             (elem2d_eligible(c->g) && !c->no_fast2d ? HOMFE_PATH_ELEM2D : 0);
+             (elem2d_eligible(c->g) && !c->no_fast2d ? HOMFE_PATH_ELEM2D : 0) |
+             (c->small2d && small2d_eligible(c->g, c->n_phases) ? HOMFE_PATH_SMALL2D : 0);
   });
 }
 

@@ -151,6 +151,13 @@ inline void set_gram_factors(SpecParams& p) {
 }
 void launch_spectral(const SpecParams& p, double2* spec, const PcgState* st, double* partials,
                      cudaStream_t s);
+// whole PCG solve of a 256^2 scalar TwoTriangles problem in one persistent
+// 16-CTA cluster (small2d.cu); false = not launched (cluster unschedulable)
+bool small2d_eligible(const Grid& g, int n_phases);
+bool launch_pcg_small2d(const SpecParams& sp, double* x, double* r, double* p, const uint8_t* phase,
+                        const double* tri_tab, int n_phases, const double2* tw, PcgState* st, double* hist,
+                        cudaStream_t s);
+
 
 // Slab-decomposed spectra for any plane size (slabfft.cu): planes S
 // [c][n0l][n1][nh] (2-D cuFFT of the local planes) <-> k1 rows W

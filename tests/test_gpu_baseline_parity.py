@@ -186,7 +186,7 @@ def test_c1_tolerance_and_fixed_k(hb, oracle_mod):
     k = _tolerance_mode(hb, oracle_mod, "c1 256^2 tolerance", cfg, ph, cm)
     b = newton_rhs(cfg.dims, [1.0] * 2, 1, cm, ph, cfg.load)
     _fixed_k(hb, oracle_mod, "c1 256^2", cfg.dims, cfg.stencil, 1, cm, ph, _cref(cfg, ph, cm), b,
-             [min(k, parity_util.STRICT_K), k], e=np.asarray(cfg.load))
+             [min(k, parity_util.STRICT_K), k], expect_path=("small2d",), e=np.asarray(cfg.load))
 
 
 def test_c2_tolerance_and_fixed_k(hb, oracle_mod):
