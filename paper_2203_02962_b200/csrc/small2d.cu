@@ -172,15 +172,15 @@ __device__ double precond(const SpecParams& sp, const S2Smem& s, cg::cluster_gro
     const int lane = tid & 31, w = tid >> 5;
     const int i = lane >> 1, half = lane & 1;
     const double2* src = cl.map_shared_rank(s.spec, w) + i * kP;
+    double2 v[kCols / 2];  // all remote loads in flight before the first store
 #pragma unroll
     for (int jj = 0; jj < kCols / 2; ++jj) {
-      const int slot = half * (kCols / 2) + jj;
-      const int k1 = kCols * rank + slot;
-      double2 v;
-      if (k1 == 0) v = make_double2(src[0].x, src[kNX / 2].x);
-      else v = src[k1];
-      s.cb[slot * kCP + kR * w + i] = v;
+      const int k1 = kCols * rank + half * (kCols / 2) + jj;
+      if (k1 == 0) v[jj] = make_double2(src[0].x, src[kNX / 2].x);
+      else v[jj] = src[k1];
     }
+#pragma unroll
+    for (int jj = 0; jj < kCols / 2; ++jj) s.cb[(half * (kCols / 2) + jj) * kCP + kR * w + i] = v[jj];
   }
   __syncthreads();
   // ---- column FFTs (axis 0)
