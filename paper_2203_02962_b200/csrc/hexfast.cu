@@ -351,6 +351,12 @@ __global__ void __launch_bounds__(256, 2) k_hex_fast(const HexArgs a) {
 // (resident blocks) CTAs.
 // ===========================================================================
 constexpr int kZDepth = 3;
+// HB_HEXZ_RFOLD: isotropic catalogs accumulate the modal residual before the
+// z-adjoint (fewer DP operations per element than folding every
+// contribution into both faces)
+#ifndef HB_HEXZ_RFOLD
+#define HB_HEXZ_RFOLD 1
+#endif
 #ifndef HB_HEXZ_MINB3
 #define HB_HEXZ_MINB3 2
 #endif
@@ -574,11 +580,32 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
         // modal residual folded straight into the z-adjoint: A = lower face
         // (seeded with the previous element's upper face), B = upper face
         double A[C][4], B[C][4];  // B: assigned by its first contribution
+        const double* mat = (MATS ? mat_s : a.mat) + ph * MS;
+        if constexpr (HB_HEXZ_RFOLD && ISO && !QT) {
+          // modal residual R[k][v] first (one operation per contribution),
+          // then the z-adjoint: A = seed + R[m] - R[m+4], B = R[m] + R[m+4]
+          // (R[k][0]: the constant mode carries no gradient)
+          double R[C][8];
+          if constexpr (C == 3) {
+            HB_HEX_MODES_RFOLD_ELASTIC_ISO
+          } else {
+            HB_HEX_MODES_RFOLD_SCALAR_ISO
+          }
+#pragma unroll
+          for (int k = 0; k < C; ++k) {
+            A[k][0] = zc[k][0] - R[k][4];
+            B[k][0] = R[k][4];
+#pragma unroll
+            for (int m = 1; m < 4; ++m) {
+              A[k][m] = zc[k][m] + (R[k][m] - R[k][m + 4]);
+              B[k][m] = R[k][m] + R[k][m + 4];
+            }
+          }
+        } else {
 #pragma unroll
         for (int k = 0; k < C; ++k)
 #pragma unroll
           for (int m = 0; m < 4; ++m) A[k][m] = zc[k][m];
-        const double* mat = (MATS ? mat_s : a.mat) + ph * MS;
         if constexpr (QT && C == 3) {
 #pragma unroll
           for (int k = 0; k < C; ++k)
@@ -606,6 +633,7 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
           } else {
             HB_HEX_MODES_FOLD_SCALAR_GEN
           }
+        }
         }
         if constexpr (FE) {  // element load, moved to the modal basis (fwd / 8)
 #pragma unroll
