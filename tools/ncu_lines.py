@@ -1,7 +1,10 @@
 """Per-source-line warp-stall samples of one kernel instance in an ncu
 report (ncu --page source --print-source cuda,sass), top lines first.
-usage: ncu_lines.py REPORT KERNEL_REGEX [LAUNCH_SKIP] [TOP]"""
+usage: ncu_lines.py REPORT KERNEL_REGEX [LAUNCH_SKIP] [TOP]
+NCU_COLUMN selects another per-line column of the source page (e.g.
+"L1 Wavefronts Shared Excessive" for bank conflicts); NCU_COLUMN=? lists them."""
 import csv
+import os
 import subprocess
 import sys
 
@@ -19,7 +22,11 @@ for r in csv.reader(out.splitlines()):
         fname = r[1].split("/")[-1]
         continue
     if r[0] == "Line No":
-        idx = r.index("Warp Stall Sampling (All Samples)")
+        col = os.environ.get("NCU_COLUMN", "Warp Stall Sampling (All Samples)")
+        if col == "?":
+            print("\n".join(r))
+            sys.exit(0)
+        idx = r.index(col)
         continue
     if idx is None or not r[0] or len(r) <= idx:
         continue
