@@ -317,6 +317,89 @@ __device__ __forceinline__ void fft4step_regs(double2 (&v)[16], double2* buf, in
   group_sync();
 }
 
+// The same two transforms on a pencil whose element n lives at buf[F(n)] (F a
+// bijection onto the pencil's own slots, e.g. the interleaved, XOR-swizzled
+// [i0][4] rows of pass 2's TMA stage): the transform runs in the layout the
+// TMA engine loads and stores, so no re-layout pass and no block barrier is
+// needed around it (only the group's own threads touch these slots).
+template <int N, bool INV, class IDX>
+__device__ __forceinline__ void fft4step_map(double2* buf, int t, const double2* __restrict__ tw4, IDX F) {
+  constexpr int A = N / 16;
+  double2 v[16];
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) v[n2] = buf[F(t + A * n2)];
+  dft16<INV>(v);
+  if (t > 0) {
+#pragma unroll
+    for (int k2 = 1; k2 < 16; ++k2) {
+      const double2 w = tw4[k2 * A + t];
+      v[k2] = cmul(v[k2], INV ? conj(w) : w);
+    }
+  }
+  group_sync();
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) buf[F(t * 16 + (k2 ^ (t & 15)))] = v[k2];
+  group_sync();
+  constexpr int PER = 16 / A;
+  double2 u[PER][A];
+#pragma unroll
+  for (int b = 0; b < PER; ++b) {
+    const int k2 = t + b * A;
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) u[b][n1] = buf[F(n1 * 16 + (k2 ^ n1))];
+    if constexpr (A == 16) dft16<INV>(u[b]);
+    else if constexpr (A == 8) dft8<INV>(u[b]);
+    else dft4<INV>(u[b][0], u[b][1], u[b][2], u[b][3]);
+  }
+  group_sync();
+#pragma unroll
+  for (int b = 0; b < PER; ++b) {
+    const int k2 = t + b * A;
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) buf[F(k2 + 16 * k1)] = u[b][k1];
+  }
+  group_sync();
+}
+
+// v: the step-1 inputs x[t + A n2], read by the caller from buf[F(.)] itself
+// (hence the group barrier before the first write).
+template <int N, bool INV, class IDX>
+__device__ __forceinline__ void fft4step_regs_map(double2 (&v)[16], double2* buf, int t,
+                                                  const double2* __restrict__ tw4, IDX F) {
+  constexpr int A = N / 16;
+  dft16<INV>(v);
+  if (t > 0) {
+#pragma unroll
+    for (int k2 = 1; k2 < 16; ++k2) {
+      const double2 w = tw4[k2 * A + t];
+      v[k2] = cmul(v[k2], INV ? conj(w) : w);
+    }
+  }
+  group_sync();
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) buf[F(t * 16 + (k2 ^ (t & 15)))] = v[k2];
+  group_sync();
+  constexpr int PER = 16 / A;
+  double2 u[PER][A];
+#pragma unroll
+  for (int b = 0; b < PER; ++b) {
+    const int k2 = t + b * A;
+#pragma unroll
+    for (int n1 = 0; n1 < A; ++n1) u[b][n1] = buf[F(n1 * 16 + (k2 ^ n1))];
+    if constexpr (A == 16) dft16<INV>(u[b]);
+    else if constexpr (A == 8) dft8<INV>(u[b]);
+    else dft4<INV>(u[b][0], u[b][1], u[b][2], u[b][3]);
+  }
+  group_sync();
+#pragma unroll
+  for (int b = 0; b < PER; ++b) {
+    const int k2 = t + b * A;
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) buf[F(k2 + 16 * k1)] = u[b][k1];
+  }
+  group_sync();
+}
+
 // Full N-point transform of buf (in shared memory) by TPF = N/16 threads.
 // N <= 256: four-step (table layout tw4); N = 512: Stockham (plain W_N).
 template <int N, bool INV>

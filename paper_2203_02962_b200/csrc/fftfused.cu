@@ -61,6 +61,12 @@ constexpr int kTB = 16;  // T2 row pitch granule
 constexpr int kTG = 4;   // T column group: a pencil block's TMA unit
 __host__ __device__ constexpr int t_blocks(int np_plane) { return (np_plane / 2 + 1 + kTB - 1) / kTB; }
 __host__ __device__ constexpr int t_groups(int np_plane) { return (np_plane / 2 + 1 + kTG - 1) / kTG; }
+// Within a 64-byte [i0][4] row of T the column slot is XOR-swizzled by the
+// plane index ((i0 >> 1) & 3, the pattern of CU_TENSOR_MAP_SWIZZLE_64B): a
+// pencil thread's 16-byte reads of rows t, t+1, ... of ONE column then fall
+// into 8 distinct bank groups (unswizzled: 2 -> 4-way conflicts on every
+// stage read and re-layout write of pass 2).
+__host__ __device__ constexpr int t_swz(int i0) { return (i0 >> 1) & 3; }
 struct TLayout {
   int nc, n1l, nzl, nb, ng;  // ng: 4-column groups of T
   int sh1, shz;  // log2 n1l, log2 nzl (both powers of two)
@@ -78,7 +84,7 @@ struct TLayout {
   }
   __device__ __forceinline__ int64_t t(int peer, int comp, int k1l, int k2, int i0l) const {
     return ((((int64_t)peer * nc + comp) * n1l + k1l) * ng + (k2 / kTG)) * ((int64_t)nzl * kTG) +
-           (int64_t)i0l * kTG + (k2 % kTG);
+           (int64_t)i0l * kTG + ((k2 % kTG) ^ t_swz(i0l));
   }
   __device__ __forceinline__ int64_t t2(int peer, int comp, int i0l, int k1l, int k2) const {
     return ((((int64_t)peer * nc + comp) * nzl + i0l) * n1l + k1l) * (int64_t)(nb * kTB) + k2;
@@ -276,17 +282,18 @@ __global__ void __launch_bounds__(NP, HB_FWD_MINB) k_plane_fwd(const PlaneArgs a
   constexpr int NG = t_groups(NP);
   const int64_t zs = (int64_t)a.L.nzl * kTG;
   double2* tdst = a.T + (int64_t)(rank * (16 / kTG)) * zs + i0 * kTG;  // this CTA's 16 columns
+  const int sw = t_swz(i0);
   if (first == 0) {
     // 16 columns: shifts instead of divisions
 #pragma unroll 4
     for (int idx = tid; idx < 16 * NP; idx += NP) {
       const int k1 = idx >> 4, j = idx & 15;
-      tdst[(int64_t)a.L.row1(comp, k1) * NG * zs + (j / kTG) * zs + (j % kTG)] = rows[j * (NP + 1) + k1];
+      tdst[(int64_t)a.L.row1(comp, k1) * NG * zs + (j / kTG) * zs + ((j % kTG) ^ sw)] = rows[j * (NP + 1) + k1];
     }
   } else {
     for (int idx = tid; idx < ncol * NP; idx += NP) {
       const int k1 = idx / ncol, j = idx % ncol + first;
-      tdst[(int64_t)a.L.row1(comp, k1) * NG * zs + (j / kTG) * zs + (j % kTG)] = rows[j * (NP + 1) + k1];
+      tdst[(int64_t)a.L.row1(comp, k1) * NG * zs + (j / kTG) * zs + ((j % kTG) ^ sw)] = rows[j * (NP + 1) + k1];
     }
   }
   if (rank == 0 && g == 0) {
@@ -529,6 +536,20 @@ template <int N0, int C>
 #ifndef HB_PENCIL_MINB
 #define HB_PENCIL_MINB 2
 #endif
+// HB_PENCIL_INLAYOUT: the pencil transforms run in the TMA stage layout itself
+// ([group][i0][4 ^ swizzle] rows: fft4step_*_map), so the stage is never
+// re-laid: two block barriers and two shared-memory passes less per tile.
+#ifndef HB_PENCIL_INLAYOUT
+#define HB_PENCIL_INLAYOUT 1
+#endif
+// HB_PENCIL_HALVES (in-layout, 256-point elastic pencils): the solve couples
+// only the three components of a column, and columns {0,1} / {2,3} of a tile
+// live in warps {0,2,4} / {1,3,5}; each half synchronises its transform ->
+// solve -> transform hand-offs on its own named barrier (96 threads), so the
+// halves drift apart and overlap their shared-memory and FP64 phases.
+#ifndef HB_PENCIL_HALVES
+#define HB_PENCIL_HALVES 0  // measured: 0.235 -> 0.270 ms (the branchy barrier costs registers: 112 B of spills)
+#endif
 __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB)
     k_pencil(const __grid_constant__ SpecParams sp, const __grid_constant__ PencilArgs a,
              const __grid_constant__ CUtensorMap t2map) {
@@ -544,11 +565,12 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
   constexpr int STAGE = C * BK * N0;  // double2 per stage
   if (a.st && !a.st->active) return;
   extern __shared__ double2 sm_raw[];
-  // 128-byte alignment by pointer arithmetic on the shared symbol itself (an
-  // integer round trip would make every stage access a generic LD/ST)
+  // 1024-byte alignment (the 64-byte swizzle of the tensor stores keys on
+  // shared address bits 7-8) by pointer arithmetic on the shared symbol itself
+  // (an integer round trip would make every stage access a generic LD/ST)
   double2* sm = reinterpret_cast<double2*>(reinterpret_cast<unsigned char*>(sm_raw) +
-                                           ((128u - (fft::smem_u32(sm_raw) & 127u)) & 127u));
-  double2* stage0 = sm;             // [2][C][NGB][N0][kTG]  (128-B aligned: TMA tensor stores)
+                                           ((1024u - (fft::smem_u32(sm_raw) & 1023u)) & 1023u));
+  double2* stage0 = sm;             // [2][C][NGB][N0][kTG ^ swizzle]
   double2* tws = sm + 2 * STAGE;
   double2* t12 = tws + N0;  // [n1] (sin, sin(t/2)) of axes 1 and 2 (square planes: one table)
   __shared__ __align__(8) uint64_t full[2];
@@ -599,6 +621,8 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
   }
   double rz = 0.0;
   int it = 0;
+  constexpr bool INL = HB_PENCIL_INLAYOUT;
+  if (INL) __syncthreads();  // tables ready before the first (barrier-free) transform
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it & 1;
     double2* stg = stage0 + st * STAGE;
@@ -607,39 +631,65 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
     fft::mbar_wait(&full[st], (it >> 1) & 1);
     double2 v[16];
     {
-      const double2* src = stg + (comp * NGB + j / kTG) * N0 * kTG + (j % kTG);
+      const double2* src = stg + (comp * NGB + j / kTG) * N0 * kTG;
 #pragma unroll
-      for (int n2 = 0; n2 < 16; ++n2) v[n2] = src[(t + TPF * n2) * kTG];
+      for (int n2 = 0; n2 < 16; ++n2) v[n2] = src[(t + TPF * n2) * kTG + ((j % kTG) ^ t_swz(t + TPF * n2))];
     }
-    if (sp.kind == 3 && tid < BK) {
+    constexpr bool HALVES = INL && HB_PENCIL_HALVES && C == 3 && TPF == 16 && BK == 4;
+    const int half = (tid >> 5) & 1;                       // HALVES: columns {2 half, 2 half + 1}
+    const int hr = ((tid >> 6) << 5) | (tid & 31);         // rank within the half (0..95)
+    auto half_sync = [&] {
+      if (HB_PENCIL_HALVES == 2) {  // register id: ptxas reserves all 16 barriers
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + half), "n"(NT / 2) : "memory");
+      } else if (half) {
+        asm volatile("bar.sync 2, %0;" ::"n"(NT / 2) : "memory");
+      } else {
+        asm volatile("bar.sync 1, %0;" ::"n"(NT / 2) : "memory");
+      }
+    };
+    if (HALVES ? (sp.kind == 3 && hr < 2) : (sp.kind == 3 && tid < BK)) {
+      const int ct = HALVES ? 2 * half + hr : tid;
       // M(k0) = diag(cf0 sh0^2, cf1 S2_0, cf2 S2_0) + offdiag(cf3 sn0, cf4 sn0, cf5 S2_0)
       // (shared-memory table and the host's division-free Gram factors: the
       // other warps wait for these four threads at the next block barrier)
-      const int k2 = min(c0 + tid, P - 1);
+      const int k2 = min(c0 + ct, P - 1);
       const double2 t1 = t12[k1], t2 = t12[k2];
       const double S21 = 2.0 - (4.0 / 3.0) * t1.y * t1.y, S22 = 2.0 - (4.0 / 3.0) * t2.y * t2.y;
-      colf[tid][0] = sp.cd[0] * S21 * S22;
-      colf[tid][1] = sp.cd[1] * t1.y * t1.y * S22;
-      colf[tid][2] = sp.cd[2] * t2.y * t2.y * S21;
-      colf[tid][3] = sp.co[0][1] * t1.x * S22;
-      colf[tid][4] = sp.co[0][2] * t2.x * S21;
-      colf[tid][5] = sp.co[1][2] * t1.x * t2.x;
+      colf[ct][0] = sp.cd[0] * S21 * S22;
+      colf[ct][1] = sp.cd[1] * t1.y * t1.y * S22;
+      colf[ct][2] = sp.cd[2] * t2.y * t2.y * S21;
+      colf[ct][3] = sp.co[0][1] * t1.x * S22;
+      colf[ct][4] = sp.co[0][2] * t2.x * S21;
+      colf[ct][5] = sp.co[1][2] * t1.x * t2.x;
     }
-    __syncthreads();  // raw stage reads done (stage becomes the FFT buffers); colf, tws ready
-    double2* buf = stg;               // [C][BK][N0]
-    double2* pb = buf + g * N0;
-    if (!(a.dbg & 32)) fft::fft4step_regs<N0, false>(v, pb, t, tws);
+    if (!INL) __syncthreads();  // raw stage reads done (stage becomes the FFT buffers); colf, tws ready
+    double2* buf = stg;               // [C][BK][N0]; INL: stays [C][NGB][N0][kTG ^ swizzle]
+    double2* pb = INL ? stg + (comp * NGB + j / kTG) * N0 * kTG : buf + g * N0;
+    const int jm = j % kTG;
+    auto slot = [jm](int n) { return n * kTG + (jm ^ t_swz(n)); };
+    // element (component i, column jj, frequency k0) of the tile
+    auto at = [&](int i, int jj, int k0) -> double2& {
+      if (INL) return stg[((i * NGB + jj / kTG) * N0 + k0) * kTG + ((jj % kTG) ^ t_swz(k0))];
+      return buf[(i * BK + jj) * N0 + k0];
+    };
+    if (INL) {
+      if (!(a.dbg & 32)) fft::fft4step_regs_map<N0, false>(v, pb, t, tws, slot);
+    } else if (!(a.dbg & 32)) fft::fft4step_regs<N0, false>(v, pb, t, tws);
     else
 #pragma unroll
       for (int n2 = 0; n2 < 16; ++n2) pb[t + TPF * n2] = v[n2];
-    __syncthreads();
-    for (int e = tid; e < N0 * BK && !(a.dbg & 16); e += NT) {
-      const int jj = e / N0, k0 = e % N0;
+    if (HALVES) half_sync();
+    else __syncthreads();
+    // the solve: every thread of the block (HALVES: of the half) takes
+    // frequencies of the tile's (the half's) columns, all C components each
+    const int se0 = HALVES ? hr : tid, sen = HALVES ? 2 * N0 : N0 * BK, sed = HALVES ? NT / 2 : NT;
+    for (int e = se0; e < sen && !(a.dbg & 16); e += sed) {
+      const int jj = (HALVES ? 2 * half : 0) + e / N0, k0 = e % N0;
       const int k2 = c0 + jj;
       if (k2 >= P) continue;
       double2 r[C], z[C];
 #pragma unroll
-      for (int i = 0; i < C; ++i) r[i] = buf[(i * BK + jj) * N0 + k0];
+      for (int i = 0; i < C; ++i) r[i] = at(i, jj, k0);
       if (k0 == 0 && k1 == 0 && k2 == 0) {
 #pragma unroll
         for (int i = 0; i < C; ++i) z[i] = make_double2(0.0, 0.0);
@@ -677,17 +727,23 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
         rz = fma(wgt, s, rz);
       }
 #pragma unroll
-      for (int i = 0; i < C; ++i) buf[(i * BK + jj) * N0 + k0] = z[i];
+      for (int i = 0; i < C; ++i) at(i, jj, k0) = z[i];
     }
-    __syncthreads();
+    if (HALVES) half_sync();
+    else __syncthreads();
+    if (INL) {
+      if (!(a.dbg & 32)) fft::fft4step_map<N0, true>(pb, t, tws, slot);
+    } else {
     if (!(a.dbg & 32)) fft::fft4step<N0, true>(pb, t, tws);
 #pragma unroll
     for (int n = 0; n < 16; ++n) v[n] = pb[t + TPF * n];
     __syncthreads();  // every pencil read back: re-lay the stage as [C][group][i0][4]
     {
-      double2* dst = stg + (comp * NGB + j / kTG) * N0 * kTG + (j % kTG);
+      // slots swizzled like T: the tensor map (SWIZZLE_64B) undoes it on the way out
+      double2* dst = stg + (comp * NGB + j / kTG) * N0 * kTG;
 #pragma unroll
-      for (int n = 0; n < 16; ++n) dst[(t + TPF * n) * kTG] = v[n];
+      for (int n = 0; n < 16; ++n) dst[(t + TPF * n) * kTG + ((j % kTG) ^ t_swz(t + TPF * n))] = v[n];
+    }
     }
     fft::fence_proxy_async();  // generic smem writes -> async-proxy (TMA) reads
     __syncthreads();
@@ -815,7 +871,7 @@ void run_pencils_c(const FusedFft& f, const SpecParams& sp, const PcgState* st, 
   a.nred = kRedBlocks;
   a.dbg = f.dbg;
   const int ntiles = a.L.n1l * a.ntk;
-  const size_t smem = sizeof(double2) * (2 * (size_t)C * BK * N0 + N0 + f.np_plane) + 128;
+  const size_t smem = sizeof(double2) * (2 * (size_t)C * BK * N0 + N0 + f.np_plane) + 1024;
   HB_CUDA(cudaFuncSetAttribute(k_pencil<N0, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   static int grid_cap[2] = {0, 0};  // resident blocks of this instantiation (persistent grid)
   int& cap = grid_cap[C == 3];
@@ -862,7 +918,7 @@ void fused_make_maps(FusedFft& f) {
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(f.t2map);
   const CUresult r = encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, f.T2, dims, strides, box, estr,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
 }

@@ -127,6 +127,17 @@ def gen_fold(elastic, iso, modal=False):
     if elastic:
         for md, inc in enumerate(INC3):
             cls = CLASS[md]
+            if iso and modal and cls == 2:
+                # the three doubly-antisymmetric modes only see V[k][7] (one
+                # normal + two shear rows each, same class factor), so their
+                # sum is R[k][7] = f (lambda + 2mu + 2 mu) V[k][7] = mat[9] V[k][7]
+                if md == 4:
+                    out.append("  {  /* modes aas + asa + saa */")
+                    out.append("    const double c7 = mat[9];")
+                    for k in range(3):
+                        acc(k, 7, scale="c7", e=f"V[{k}][7]")
+                    out.append("  }")
+                continue
             rows = sorted({e for e, _, _ in inc})
             out.append(f"  {{  /* mode {MODES[md]} */")
             for e in rows:

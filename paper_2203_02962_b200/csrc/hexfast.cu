@@ -46,12 +46,12 @@ namespace {
 
 
 // Per-phase material table layout (doubles):
-//   ISO:      [3 classes][3] = f*lambda, f*2mu, f*mu   (elastic)
+//   ISO:      [3 classes][3] = f*lambda, f*2mu, f*mu, then f_2*(lambda + 4mu)   (elastic)
 //             [3 classes][1] = f*kappa                 (scalar)
 //   general:  [3 classes][M*M] = f * (S C S)  (S = diag(1,1,1,s2,s2,s2))
 template <int C, bool ISO>
 constexpr int mat_stride() {
-  return ISO ? (C == 3 ? 9 : 3) : (C == 3 ? 3 * 36 : 3 * 9);
+  return ISO ? (C == 3 ? 10 : 3) : (C == 3 ? 3 * 36 : 3 * 9);
 }
 
 // Forward separable (S, D) transform of 8 corner values x[a*4+b*2+c].
@@ -581,7 +581,11 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
         for (int k = 0; k < C; ++k)
 #pragma unroll
           for (int m = 0; m < 4; ++m) {
+#ifdef HB_HEXZ_EXP_NOLO  // timing experiment only (wrong results): no lower-face round trip
+            const double lo = 0.5 * Up[k][m] + zc[k][m];
+#else
             const double lo = lo_s[(k * 4 + m) * nx + x];
+#endif
             V[k][m] = lo + Up[k][m];
             V[k][4 + m] = Up[k][m] - lo;
           }
@@ -682,7 +686,11 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
 #pragma unroll
       for (int k = 0; k < C; ++k)
 #pragma unroll
-        for (int m = 0; m < 4; ++m) lo_s[(k * 4 + m) * nx + x] = Up[k][m];
+        for (int m = 0; m < 4; ++m) {
+#ifndef HB_HEXZ_EXP_NOLO
+          lo_s[(k * 4 + m) * nx + x] = Up[k][m];
+#endif
+        }
       __syncthreads();  // edges visible; ring slot fully read
       // refill this slot with unit u + D, one copy per warp
       if (lane == 0 && u + D < nunits)
@@ -912,6 +920,7 @@ bool hex_fast_tables(const Grid& g, int n_phases, const double* cmats, std::vect
         iso.push_back(f[c] * twomu);
         iso.push_back(f[c] * 0.5 * twomu);  // mu: s2^2 * 2mu on the raw shear rows
       }
+      iso.push_back(f[2] * (lam + 2.0 * twomu));  // modes aas + asa + saa merged (RFOLD)
       for (int c = 0; c < 3; ++c)
         for (int i = 0; i < 6; ++i)
           for (int j = 0; j < 6; ++j) {
