@@ -155,7 +155,9 @@ __global__ void __launch_bounds__(NP, HB_FWD_MINB) k_plane_fwd(const PlaneArgs a
   // reads 2 x 128-byte row segments per step), r - alpha Ap is written back
   // from registers and fed to the FFT: no shared-memory staging of the rows
   // (measured: 128^2 planes 0.031 -> 0.026 ms; 256^2 planes 0.468 -> 0.505 ms,
-  // there the TMA-staged rows win: HB_FWD_REGLOAD = largest plane size using it)
+  // there the TMA-staged rows win: HB_FWD_REGLOAD = largest plane size using it;
+  // a hybrid -- r staged by TMA, Ap loaded in the FFT layout, update in the FFT
+  // registers, no shared-memory update pass -- measured 0.460 -> 0.468 ms)
 #ifndef HB_FWD_REGLOAD
 #define HB_FWD_REGLOAD 128
 #endif
@@ -547,8 +549,10 @@ template <int N0, int C>
 // live in warps {0,2,4} / {1,3,5}; each half synchronises its transform ->
 // solve -> transform hand-offs on its own named barrier (96 threads), so the
 // halves drift apart and overlap their shared-memory and FP64 phases.
+// (1 = immediate barrier ids behind a branch: 112 B of spills, 0.235 -> 0.270 ms;
+// 2 = the id in a register, ptxas then reserves all 16 barriers: 0.235 -> 0.229 ms)
 #ifndef HB_PENCIL_HALVES
-#define HB_PENCIL_HALVES 0  // measured: 0.235 -> 0.270 ms (the branchy barrier costs registers: 112 B of spills)
+#define HB_PENCIL_HALVES 2
 #endif
 __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB)
     k_pencil(const __grid_constant__ SpecParams sp, const __grid_constant__ PencilArgs a,
