@@ -292,7 +292,7 @@ def run_gpu(args, rank, world, local_rank):
     achieved = bytes_k / (kms / 1e3) / 1e9
     traffic = None
     iter_traffic = None
-    tp = os.path.join(ROOT, "profiles", "r01_c3_ncu_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r02_c3_ncu_traffic.json")
     if os.path.exists(tp) and world == 1:
         with open(tp) as f:
             tj = json.load(f)
@@ -345,7 +345,7 @@ def run_gpu(args, rank, world, local_rank):
         "iteration_bytes": {"algorithmic": b_iter, "dram_ncu": iter_traffic},
         "roofline": {"kernel": f"{kdesc} ({kname})", "bound": "hbm", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": achieved / hbm, "traffic": traffic,
-                     "traffic_source": "profiles/r01_c3_ncu_traffic.json (ncu --set full, per launch)"
+                     "traffic_source": "profiles/r02_c3_ncu_traffic.json (ncu --set full, per launch)"
                      if traffic else None,
                      "peak_source": peak_kind, "bytes_per_launch": bytes_k, "kernel_ms": kms},
         "kernel_ms": ({"apply_K": ms[0], "update_r": ms[1], "fft_fwd": ms[2], "spectral": ms[3],

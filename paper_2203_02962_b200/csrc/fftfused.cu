@@ -107,6 +107,7 @@ struct PlaneArgs {
   const PcgState* st;  // PCG mode
   int mode;
   int dbg;             // profiling only: bit mask of skipped phases
+  int ahead;           // L2 prefetch distance in clusters (0 = off): the inputs of cluster cid + ahead
   const double2* t2p[FusedFft::kMaxPeers];  // pass 3: chunk bases per source peer (FusedFft::t2pull)
 };
 
@@ -168,6 +169,14 @@ __global__ void __launch_bounds__(NP, HB_FWD_MINB) k_plane_fwd(const PlaneArgs a
       for (int y = 0; y < 32; ++y) fft::bulk_g2s(rows + y * P, a.r + plane + (int64_t)y * NP, ROWB, &bar);
   }
   for (int i = tid; i < NP; i += NP) tws[i] = a.tw[i];
+  if (a.ahead > 0 && pcg && tid < 64 && cid + a.ahead < (int)(gridDim.x / CL)) {
+    // L2 prefetch of the r and Ap rows of the cluster that will take this one's place
+    const int cn = cid + a.ahead;
+    const int64_t pl = (int64_t)(cn / a.n0) * a.np + (int64_t)(cn % a.n0) * NP * NP + (int64_t)rank * 32 * NP +
+                       (int64_t)(tid & 31) * NP;
+    const double* pf = (tid < 32 ? a.r : a.ap) + pl;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"((uint32_t)ROWB) : "memory");
+  }
   double2 vr[16];  // row pair values in the FFT register layout
   if (regload) {
     const double alpha = a.st->alpha;
@@ -314,6 +323,12 @@ __global__ void __launch_bounds__(NP, HB_FWD_MINB) k_plane_fwd(const PlaneArgs a
 #ifndef HB_INV_MINB
 #define HB_INV_MINB 2
 #endif
+#ifndef HB_INV_AHEAD
+#define HB_INV_AHEAD 0
+#endif
+#ifndef HB_FWD_AHEAD
+#define HB_FWD_AHEAD 0
+#endif
 #ifndef HB_INV_SPLIT
 #define HB_INV_SPLIT 2
 #endif
@@ -337,6 +352,15 @@ __global__ void __launch_bounds__(NP, HB_INV_MINB) k_plane_inv(const __grid_cons
   const int comp = cid / a.n0, i0 = cid % a.n0;
   const int tid = threadIdx.x, g = tid / TPF, t = tid % TPF;
   for (int i = tid; i < NP; i += NP) tws[i] = a.tw[i];
+  if (a.ahead > 0 && cid + a.ahead < (int)(gridDim.x / CL)) {
+    // pull the T2 block of the cluster that will take this one's place into
+    // L2 (row k1 = tid: this rank's 16 columns, 256 bytes), so its first loads
+    // do not wait for HBM
+    const int cn = cid + a.ahead, compn = cn / a.n0, i0n = cn % a.n0;
+    constexpr int PITCHN = t_blocks(NP) * kTB;
+    const double2* pf = a.t2p[a.L.p1(tid)] + (int64_t)a.L.row2(compn, i0n, tid) * PITCHN + rank * 16;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pf), "r"(256u) : "memory");
+  }
   // coalesced column loads: warp w takes k1 rows [32w, 32w+32), each
   // half-warp one row's 16 contiguous columns; transposed into padded buffers
   const int lane = tid & 31, warp = tid >> 5;
@@ -938,6 +962,17 @@ bool fused_fft_eligible(const Grid& g) {
   return true;
 }
 
+// L2 prefetch distance of the plane passes in clusters (HOMFE_PF_FWD /
+// HOMFE_PF_INV override; 0 = off).
+static int plane_ahead(int inverse) {
+  static int v[2] = {-1, -1};
+  if (v[inverse] < 0) {
+    const char* e = std::getenv(inverse ? "HOMFE_PF_INV" : "HOMFE_PF_FWD");
+    v[inverse] = e ? std::atoi(e) : (inverse ? HB_INV_AHEAD : HB_FWD_AHEAD);
+  }
+  return v[inverse];
+}
+
 static void planes(const FusedFft& f, bool inverse, const PlaneArgs& a, cudaStream_t s) {
   if (f.np_plane == 256) run_planes<256>(f, inverse, a, s);
   else run_planes<128>(f, inverse, a, s);
@@ -966,6 +1001,7 @@ void fused_forward(const FusedFft& f, const SpecParams& sp, double* r, const dou
   a.st = st;
   a.mode = ap ? kModePcg : kModePlain;
   a.dbg = f.dbg;
+  a.ahead = plane_ahead(0);
   if (which & 1) planes(f, false, a, s);
   if (which & 2) pencils(f, sp, st, partials, s);
 }
@@ -986,6 +1022,7 @@ void fused_inverse(const FusedFft& f, double* p, double* x, double* z, const Pcg
   a.st = st;
   a.mode = st ? kModePcg : (init ? kModeInit : kModeZ);
   a.dbg = f.dbg;
+  a.ahead = plane_ahead(1);
   planes(f, true, a, s);
 }
 

@@ -21,5 +21,5 @@ for _ in range(reps - 1):
 rep = out["report"]
 print(name, "iteration_ms", rep["cg_device_ms"] / max(rep["cg_total"], 1), "cg", rep["cg_total"])
 ms = np.zeros(8)
-hb._check(_native.lib.homfe_gpu_kernel_times(s.ctx.h, 3, ms.ctypes.data_as(C.POINTER(C.c_double))))
+hb._check(_native.lib.homfe_gpu_kernel_times(s.ctx.h, int(os.environ.get("REPS", "3")), ms.ctypes.data_as(C.POINTER(C.c_double))))
 print(name, out["report"]["cg_total"], ms.round(4).tolist())
