@@ -358,6 +358,9 @@ constexpr int kJUnroll = HB_HEXZ_JUNROLL;  // z-steps per loop body (isotropic v
 // HB_HEXZ_RFOLD: isotropic catalogs accumulate the modal residual before the
 // z-adjoint (fewer DP operations per element than folding every
 // contribution into both faces)
+#ifndef HB_HEXZ_ISSUE
+#define HB_HEXZ_ISSUE 2
+#endif
 #ifndef HB_HEXZ_RFOLD
 #define HB_HEXZ_RFOLD 1
 #endif
@@ -481,6 +484,43 @@ __device__ __forceinline__ void z_issue_part(const HexArgs& a, const int* its, i
       ph = a.phase + (int64_t)zp * plane;
     }
     fft::bulk_g2s(slot + 2 * C * row_bytes, ph + (int64_t)y * nx, nx, bar);
+  }
+}
+
+// The same for unit (i, j) given directly (no division of u) and a
+// compile-time row length NXT (0 = a.n2).
+template <int C, int KZ, int NXT>
+__device__ __forceinline__ void z_issue_lane(const HexArgs& a, const int* its, int i, int j, unsigned char* slot,
+                                             uint64_t* bar, int part) {
+  const int nx = NXT ? NXT : a.n2;
+  const int info = its[i];
+  const int y = info & 0xffff, zb = (info >> 16) & 0x7fff;
+  const uint32_t row_bytes = nx * 8;
+  if (part == 0) fft::mbar_expect_tx(bar, 2 * C * row_bytes + (j ? nx : 0));
+  const int plane = a.n1 * nx;  // < 2^31 (create checks c np < 2^31)
+  if (part < 2 * C) {
+    const int k = part >> 1, r = part & 1;
+    const int yr = r ? (y + 1 == a.n1 ? 0 : y + 1) : y;
+    int pz = zb * KZ - 1 + j;
+    const double* src;
+    if (a.dist) {
+      const bool halo = pz < 0 || pz >= a.n0;
+      src = pz < 0 ? a.halo_lo : (pz >= a.n0 ? a.halo_hi : a.u + (int64_t)pz * plane);
+      src += (int64_t)k * (halo ? a.halo_cs : (int64_t)plane * a.n0);
+    } else {
+      pz = pz < 0 ? pz + a.n0 : (pz >= a.n0 ? pz - a.n0 : pz);
+      src = a.u + ((int64_t)(k * a.n0 + pz) * plane);
+    }
+    fft::bulk_g2s(reinterpret_cast<double*>(slot) + (r * C + k) * nx, src + yr * nx, row_bytes, bar);
+  } else if (j) {
+    int zp = zb * KZ - 2 + j;  // element plane
+    const uint8_t* ph;
+    if (a.dist && zp < 0) ph = a.ph_lo;
+    else {
+      zp = zp < 0 ? zp + a.n0 : zp;
+      ph = a.phase + (int64_t)zp * plane;
+    }
+    fft::bulk_g2s(slot + 2 * C * row_bytes, ph + y * nx, nx, bar);
   }
 }
 
@@ -693,8 +733,23 @@ __global__ void __launch_bounds__(NXT == 512 ? 512 : 256, (NXT == 512 || QT) ? 1
         }
       __syncthreads();  // edges visible; ring slot fully read
       // refill this slot with unit u + D, one copy per warp
+#if HB_HEXZ_ISSUE == 0
       if (lane == 0 && u + D < nunits)
         for (int part = warp; part <= 2 * C; part += nw) z_issue_part<C, KZ>(a, its, u + D, sl, &full[slot], part);
+#else
+      // the 2C + 1 copies of the unit are issued by lanes 0..2C of ONE warp in
+      // the same instruction stream (the warp rotates with u): the other
+      // warps skip the refill bookkeeping (16 % of the kernel's issued
+      // instructions when every warp's lane 0 issued one copy)
+      if (u + D < nunits && warp == (HB_HEXZ_ISSUE == 1 ? (u & (nw - 1)) : 0) && lane <= 2 * C) {
+        int jn = j + D, in = it;
+        if (jn >= KZ + 2) {
+          jn -= KZ + 2;
+          ++in;
+        }
+        z_issue_lane<C, KZ, NXT>(a, its, in, jn, sl, &full[slot], lane);
+      }
+#endif
       if (++slot == D) {
         slot = 0;
         par ^= 1;
