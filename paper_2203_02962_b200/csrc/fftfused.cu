@@ -845,6 +845,9 @@ TLayout layout_of(const FusedFft& f) {
   return TLayout{f.c, f.n1l, f.n0, t_blocks(f.np_plane), t_groups(f.np_plane), ilog2(f.n1l), ilog2(f.n0)};
 }
 
+#ifndef HB_CLUSTER_POLICY
+#define HB_CLUSTER_POLICY 0
+#endif
 template <class K>
 void launch_cluster(K kernel, int grid, int block, int cl, size_t smem, cudaStream_t s, const PlaneArgs& a) {
   HB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -853,13 +856,24 @@ void launch_cluster(K kernel, int grid, int block, int cl, size_t smem, cudaStre
   cfg.blockDim = dim3(block);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = cl;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // cluster scheduling policy preference (HOMFE_CLUSTER_POLICY: 1 = spread, 2 = load balancing)
+  static const int policy = [] {
+    const char* e = std::getenv("HOMFE_CLUSTER_POLICY");
+    return e ? std::atoi(e) : HB_CLUSTER_POLICY;
+  }();
+  if (policy) {
+    attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[1].val.clusterSchedulingPolicyPreference =
+        policy == 2 ? cudaClusterSchedulingPolicyLoadBalancing : cudaClusterSchedulingPolicySpread;
+    cfg.numAttrs = 2;
+  }
   static bool shown = false;
   if (!shown && std::getenv("HOMFE_FFT_OCC")) {
     shown = true;

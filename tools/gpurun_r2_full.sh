@@ -9,4 +9,4 @@ python tools/ab_kernels.py paper_2203_02962_b200/_lib/libhomfe_gpu.so > gpurun_o
 HOMFE_PARITY_LOG=gpurun_out/parity.jsonl timeout 3000 python -m pytest tests -m gpu -q -s --durations=30 > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref_rc=$?
 HOMFE_NO_WHILE_GRAPH=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncul=$?
-MAX_CG=3 timeout 600 ncu --set full --import-source on --clock-control none -k "regex:k_plane_fwd|k_plane_inv|k_hex_z|k_pencil" -s 4 -c 4 -o gpurun_out/full_c3_r2 python tools/profile_step.py c3 > gpurun_out/ncu_full.log 2>&1; echo ncu=$?
+MAX_CG=3 timeout 600 ncu --set full --import-source on --clock-control none -k "regex:k_plane_fwd|k_plane_inv|k_hex_z|k_pencil" -c 20 -o gpurun_out/full_c3_r2 python tools/profile_step.py c3 > gpurun_out/ncu_full.log 2>&1; echo ncu=$?
