@@ -670,6 +670,41 @@ inline NodalField apply_tangent_operator(const GridLayout& layout, const Materia
   return out;
 }
 
+// fields.hpp:64-82: per-quadrature-point tangent matrices, column-major m x m
+// blocks (the reference's TangentField::data layout).
+struct TangentField {
+  int m = 0;
+  Index quads = 0;
+  bool pixel_constant = false;
+  std::vector<double> data;
+  TangentField() = default;
+  TangentField(int m_, Index quads_) : m(m_), quads(quads_), data(static_cast<std::size_t>(m_ * m_ * quads_), 0.0) {}
+  double* block(Index q) { return data.data() + q * m * m; }
+  const double* block(Index q) const { return data.data() + q * m * m; }
+  // uniform(quads, c): the same column-major block everywhere (fields.cpp)
+  static TangentField uniform(Index quads, int m, const std::vector<double>& c_colmajor) {
+    if (static_cast<int>(c_colmajor.size()) != m * m) throw ValidationError("TangentField::uniform: block size");
+    TangentField t(m, quads);
+    for (Index q = 0; q < quads; ++q) std::copy(c_colmajor.begin(), c_colmajor.end(), t.block(q));
+    t.pixel_constant = true;
+    return t;
+  }
+};
+
+// apply_tangent_operator (operators.hpp:31-33, operators.cpp:247-257) with a
+// general per-quadrature-point TangentField: D^T W C_q D u on the device.
+inline NodalField apply_tangent_operator(const GridLayout& layout, const TangentField& tangent, const NodalField& u) {
+  if (u.nodes != layout.num_nodes() || (u.components != 1 && u.components != layout.dim()))
+    throw ValidationError("nodal field shape does not match layout");
+  const int m = u.components == 1 ? layout.dim() : (layout.dim() == 2 ? 3 : 6);
+  if (tangent.m != m) throw ValidationError("tangent dimension does not match layout");
+  if (tangent.quads != layout.num_quads()) throw ValidationError("tangent field size does not match layout");
+  homfe_ctx* ctx = layout.context(u.components);
+  NodalField out(u.components, u.nodes);
+  detail::check(homfe_gpu_apply_tangent_field(ctx, tangent.data.data(), u.data.data(), out.data.data()));
+  return out;
+}
+
 }  // namespace homfe
 
 #endif

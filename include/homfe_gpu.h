@@ -215,6 +215,13 @@ int homfe_gpu_reference_blocks(homfe_ctx* ctx, double* blocks_c);
 /* gradient_apply / divergence_apply (operators.hpp:20-25). */
 int homfe_gpu_gradient(homfe_ctx* ctx, const double* u, double* grad);
 int homfe_gpu_divergence(homfe_ctx* ctx, const double* s, int32_t weighted, double* out);
+/* apply_tangent_operator with a general per-quadrature TangentField
+   (operators.hpp:31-33, operators.cpp:247-257): ku = D^T W C_q D u, tangent =
+   num_quads column-major m x m blocks in the reference's TangentField::data
+   layout (fields.hpp:64-82), any values (not pixel-constant, not symmetric).
+   Needs no material; the field is staged in device memory for the call
+   (m^2 doubles per quadrature point). */
+int homfe_gpu_apply_tangent_field(homfe_ctx* ctx, const double* tangent, const double* u, double* ku);
 /* volume_average (fields.hpp:94-95) of an m-component quad field. */
 int homfe_gpu_volume_average(homfe_ctx* ctx, const double* s, double* out);
 /* pcg_solve (solver.hpp:75-78) with A = K(material), M^-1 = reference set by

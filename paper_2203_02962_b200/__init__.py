@@ -383,14 +383,28 @@ def _phases_from_tangent(grid, tangent):
 
 
 def apply_operator(grid, tangent, u):
-    """Fused matrix-free K u = D^T W C D u (operators.hpp:31-33)."""
+    """Fused matrix-free K u = D^T W C D u (operators.hpp:31-33). A
+    pixel-constant tangent with at most 256 distinct blocks runs the phase-
+    indexed fused kernels; any other TangentField (per-quadrature-point,
+    non-symmetric, more than 256 blocks) runs gradient -> C_q -> weighted
+    divergence on the device (operators.cpp:247-257)."""
     u = _nodal(grid, u)
     ctx = grid.context(u.shape[0])
-    cmats, phases = _phases_from_tangent(grid, tangent)
+    out = np.zeros_like(u)
+    try:
+        cmats, phases = _phases_from_tangent(grid, tangent)
+    except ValidationError:
+        t = _f64(tangent)
+        if t.ndim != 3 or t.shape[0] != grid.num_quads or t.shape[1] != t.shape[2]:
+            raise
+        if t.shape[1] != ctx.m:
+            raise ValidationError("tangent dimension does not match layout")
+        blocks = np.ascontiguousarray(t.transpose(0, 2, 1))  # column-major blocks (fields.hpp:64-82)
+        _check(lib.homfe_gpu_apply_tangent_field(ctx.h, _dp(blocks), _dp(u), _dp(out)))
+        return out
     if cmats.shape[1] != ctx.m:
         raise ValidationError("tangent dimension does not match layout")
     ctx.set_material(cmats, phases)
-    out = np.zeros_like(u)
     _check(lib.homfe_gpu_apply_K(ctx.h, _dp(u), _dp(out)))
     return out
 

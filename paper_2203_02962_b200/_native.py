@@ -73,6 +73,7 @@ def _load():
         "homfe_gpu_reference_blocks": (C.c_int, [vp, P(d)]),
         "homfe_gpu_gradient": (C.c_int, [vp, P(d), P(d)]),
         "homfe_gpu_divergence": (C.c_int, [vp, P(d), i32, P(d)]),
+        "homfe_gpu_apply_tangent_field": (C.c_int, [vp, P(d), P(d), P(d)]),
         "homfe_gpu_volume_average": (C.c_int, [vp, P(d), P(d)]),
         "homfe_gpu_pcg": (C.c_int, [vp, P(d), d, i32, P(d), P(i32), P(d), P(i32)]),
         "homfe_gpu_index_maps": (C.c_int, [vp, P(i64), P(i64), P(i32)]),
@@ -115,7 +116,7 @@ EXPORTED = ("homfe_gpu_last_error", "homfe_isotropic_stiffness", "homfe_gpu_crea
             "homfe_gpu_internal_width", "homfe_gpu_solve_state", "homfe_gpu_stress_field",
             "homfe_gpu_gamma_apply", "homfe_gpu_sb_solve", "homfe_gpu_eigenvalue_bounds", "homfe_gpu_path_info",
             "homfe_gpu_precond_reset", "homfe_gpu_weighted_dot", "homfe_gpu_pcg_observed",
-            "homfe_gpu_create_multi")
+            "homfe_gpu_create_multi", "homfe_gpu_apply_tangent_field")
 
 PATH_FLAGS = {"fused_fft": 1, "hex_modal": 2, "while_graph": 4, "slab_spectra": 8, "slab": 16, "peer_pull": 32,
               "elem2d": 64, "multi": 128, "small2d": 256}

@@ -2684,6 +2684,31 @@ int homfe_gpu_divergence(homfe_ctx* c, const double* s, int32_t weighted, double
   });
 }
 
+int homfe_gpu_apply_tangent_field(homfe_ctx* c, const double* tangent, const double* u, double* ku) {
+  if (is_multi(c)) return multi_unsupported("gpu_apply_tangent_field");
+  if (c && c->dist) {
+    g_err = "not available in slab mode (use a single-device context)";
+    return HOMFE_VALIDATION;
+  }
+  return guarded([&] {
+    HB_CUDA(cudaSetDevice(c->device));
+    if (!tangent || !u || !ku) throw ValidationError("apply_tangent_field: null argument");
+    const int64_t n = c->nvec();
+    const size_t nq = (size_t)c->g.np * c->sp.nq, mm = (size_t)c->g.m * c->g.m;
+    Scratch scr;
+    double* d_t = scr.alloc<double>(nq * mm);
+    double* q = quad_buffer(c);
+    HB_CUDA(cudaMemcpyAsync(d_t, tangent, nq * mm * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    HB_CUDA(cudaMemcpyAsync(c->d_p, u, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    QuadArgs a{c->d_p, nullptr, nullptr, c->d_phase, c->d_cmat, q, nullptr};
+    launch_quad(c->g, c->sp, kQuadGrad, a, c->stream);          // eps_q = D u
+    launch_tangent_field(c->g, c->sp, d_t, q, c->stream);        // sigma_q = C_q eps_q
+    launch_divergence(c->g, c->sp, q, true, c->d_ap, c->stream);  // D^T W sigma
+    HB_CUDA(cudaMemcpyAsync(ku, c->d_ap, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+  });
+}
+
 int homfe_gpu_weighted_dot(homfe_ctx* c, const double* a, const double* b, double* out) {
   if (is_multi(c)) return multi_unsupported("gpu_weighted_dot");
   if (c && c->dist) {

@@ -612,6 +612,41 @@ void launch_divergence(const Grid& g, const StencilParams& sp, const double* sf,
   HB_CUDA(cudaGetLastError());
 }
 
+// sigma_q = C_q eps_q for a general TangentField (tangent_multiply,
+// operators.cpp:183-192): column-major m x m block per quadrature point,
+// one thread per point, in place on the quadrature field.
+template <int M>
+__global__ void __launch_bounds__(kBlock) k_tangent_field(int64_t nq, const double* __restrict__ t,
+                                                         double* __restrict__ q) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+    double e[M], sgm[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      e[j] = q[i * M + j];
+      sgm[j] = 0.0;
+    }
+    const double* blk = t + i * M * M;
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+#pragma unroll
+      for (int r = 0; r < M; ++r) sgm[r] = fma(blk[j * M + r], e[j], sgm[r]);
+#pragma unroll
+    for (int j = 0; j < M; ++j) q[i * M + j] = sgm[j];
+  }
+}
+
+void launch_tangent_field(const Grid& g, const StencilParams& sp, const double* tangent, double* q, cudaStream_t s) {
+  const int64_t nq = g.np * sp.nq;
+  const int blocks = grid_for(nq);
+  switch (g.m) {
+    case 2: k_tangent_field<2><<<blocks, kBlock, 0, s>>>(nq, tangent, q); break;
+    case 3: k_tangent_field<3><<<blocks, kBlock, 0, s>>>(nq, tangent, q); break;
+    case 6: k_tangent_field<6><<<blocks, kBlock, 0, s>>>(nq, tangent, q); break;
+    default: throw ValidationError("tangent field: unsupported strain dimension");
+  }
+  HB_CUDA(cudaGetLastError());
+}
+
 void launch_quad_wsum(const Grid& g, const StencilParams& sp, const double* sf, double* partials, cudaStream_t s) {
   switch (g.m) {
     case 2: k_quad_wsum<2><<<kRedBlocks, kBlock, 0, s>>>(g, sp, sf, partials); break;

@@ -99,6 +99,7 @@ struct QuadArgs {
 void launch_quad(const Grid& g, const StencilParams& sp, int mode, const QuadArgs& a, cudaStream_t s);
 void launch_divergence(const Grid& g, const StencilParams& sp, const double* sfield, bool weighted,
                        double* out, cudaStream_t s);
+void launch_tangent_field(const Grid& g, const StencilParams& sp, const double* tangent, double* q, cudaStream_t s);
 void launch_quad_wdot(const Grid& g, const StencilParams& sp, const double* a, const double* b, double* partials,
                       cudaStream_t s);
 void launch_quad_wsum(const Grid& g, const StencilParams& sp, const double* sfield, double* partials,

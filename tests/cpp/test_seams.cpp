@@ -151,6 +151,26 @@ void operators_and_precond(const GridLayout& g, int c) {
   double err = 0.0;
   for (int i = 0; i < n; ++i) err = std::fmax(err, std::fabs(ku.data[i] - kd[i]));
   check(err < 1e-12 * std::fmax(1.0, maxabs(kd)), "K == D^T W C D", err);
+  // a general per-quadrature TangentField (random, non-symmetric block at every
+  // point, test_operators.cpp:168-193): fused operator == D^T W C_q D u
+  {
+    TangentField tf(m, nq);
+    for (double& v : tf.data) v = uni();
+    std::vector<double> sq(du.size());
+    for (Index q = 0; q < nq; ++q)
+      for (int i = 0; i < m; ++i) {
+        double acc = 0.0;
+        for (int j = 0; j < m; ++j) acc += tf.block(q)[j * m + i] * du[q * m + j];
+        sq[q * m + i] = w * acc;
+      }
+    std::vector<double> kq(n, 0.0);
+    for (int i = 0; i < nqm; ++i)
+      for (int j = 0; j < n; ++j) kq[j] += D[(std::size_t)i * n + j] * sq[i];
+    const NodalField kt = apply_tangent_operator(g, tf, u);
+    double e2 = 0.0;
+    for (int i = 0; i < n; ++i) e2 = std::fmax(e2, std::fabs(kt.data[i] - kq[i]));
+    check(e2 < 1e-12 * std::fmax(1.0, maxabs(kq)), "general TangentField: K == D^T W C_q D", e2);
+  }
   // identity tangent: fused == divergence(gradient(u))
   std::vector<double> id(m * m, 0.0);
   for (int i = 0; i < m; ++i) id[i * m + i] = 1.0;

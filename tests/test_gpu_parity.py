@@ -114,6 +114,35 @@ def test_anisotropic_catalog(hb, oracle_mod):
         assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("dims,stencil,c", [((10, 9), "two-triangles", 1), ((9, 7), "bilinear-quad", 2),
+                                            ((6, 5, 7), "trilinear-hex", 3), ((6, 8), "four-triangles-two-node", 2)])
+def test_general_tangent_field_operator(hb, oracle_mod, dims, stencil, c):
+    """apply_tangent_operator with a general TangentField (operators.cpp:247-257):
+    a different, non-symmetric m x m block at EVERY quadrature point, against the
+    oracle's per-quadrature sweep (the reference's own test sweeps random
+    tangents the same way, test_operators.cpp:168-193)."""
+    rng = np.random.default_rng(21)
+    lengths = [1.0 + 0.2 * a for a in range(len(dims))]
+    g = hb.Grid(dims, lengths, stencil)
+    og = oracle_mod.Grid(dims, lengths, stencil)
+    m = g.dim if c == 1 else g.dim * (g.dim + 1) // 2
+    tangent = rng.uniform(-1, 1, (g.num_quads, m, m))
+    u = rng.uniform(-1, 1, (c, g.num_nodes))
+    ref = oracle_mod.apply_tangent(og, c, tangent, u)
+    got = hb.apply_operator(g, tangent, u).ravel()
+    assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+    # a pixel-constant field through this path equals the phase-indexed kernels
+    cm = _two_phase_iso(hb, g.dim, c)
+    ph = _random_phase(dims, 9)
+    field = cm[np.repeat(ph, g.quads_per_pixel)] + 0.0
+    fused = hb.apply_operator(g, field, u).ravel()
+    field[0, 0, 0] *= 1.0 + 1e-15  # no longer pixel-constant: general path
+    general = hb.apply_operator(g, field, u).ravel()
+    assert np.abs(general - fused).max() <= 1e-12 * np.abs(fused).max()
+    with pytest.raises(hb.ValidationError):
+        hb.apply_operator(g, tangent[:, :-1, :-1], u)
+
+
 # -------------------------------------------------------- preconditioner
 def test_symbol_matches_assembled_blocks(hb, oracle_mod, golden):
     for case in golden.load("precond.npz"):
