@@ -29,7 +29,13 @@ namespace hb {
 namespace {
 
 constexpr int kStrip = 31;
-constexpr int kBand = 64;
+// rows per task: 32 balances the tasks over the resident warps better than
+// 64 on the smaller grids (2048^2: 0.035 -> 0.027 ms per launch; 8192^2:
+// 0.396 -> 0.390 ms) at 1/32 warm-up rows
+#ifndef HB_E2D_BAND
+#define HB_E2D_BAND 32
+#endif
+constexpr int kBand = HB_E2D_BAND;
 #ifndef HB_E2D_PD
 #define HB_E2D_PD 1  // rows loaded ahead
 #endif

@@ -9,7 +9,7 @@ import paper_2203_02962_b200 as hb
 from paper_2203_02962_b200 import _native, inputs
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
-cfg = inputs.config(name)
+cfg = inputs.config(name, n=int(os.environ["N"])) if os.environ.get("N") else inputs.config(name)
 g = hb.Grid(cfg.dims, [1.0] * cfg.dim, cfg.stencil)
 mats = [hb.Material(t, cfg.thermal, cfg.dim) for t in cfg.tangents()]
 s = hb.Solver(g, mats, cfg.phases(), eta_cg=cfg.eta_cg, reference=cfg.reference,
