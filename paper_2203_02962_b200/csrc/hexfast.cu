@@ -498,30 +498,31 @@ __device__ __forceinline__ void z_issue_lane(const HexArgs& a, const int* its, i
   const uint32_t row_bytes = nx * 8;
   if (part == 0) fft::mbar_expect_tx(bar, 2 * C * row_bytes + (j ? nx : 0));
   const int plane = a.n1 * nx;  // < 2^31 (create checks c np < 2^31)
-  if (part < 2 * C) {
-    const int k = part >> 1, r = part & 1;
-    const int yr = r ? (y + 1 == a.n1 ? 0 : y + 1) : y;
-    int pz = zb * KZ - 1 + j;
-    const double* src;
-    if (a.dist) {
-      const bool halo = pz < 0 || pz >= a.n0;
-      src = pz < 0 ? a.halo_lo : (pz >= a.n0 ? a.halo_hi : a.u + (int64_t)pz * plane);
-      src += (int64_t)k * (halo ? a.halo_cs : (int64_t)plane * a.n0);
+  // one straight-line path for the u rows (parts 0..2C-1) and the phase row
+  // (part 2C, element plane = node plane - 1): the lanes differ only in
+  // selected offsets, so the issuing warp does not run two divergent branches
+  const bool isph = part == 2 * C;
+  const int k = part >> 1, r = part & 1;
+  const int yr = (r && !isph) ? (y + 1 == a.n1 ? 0 : y + 1) : y;
+  int pz = zb * KZ - 1 + j - (isph ? 1 : 0);
+  const unsigned char* src;
+  if (a.dist) {
+    if (isph) {
+      src = pz < 0 ? a.ph_lo : a.phase + (int64_t)pz * plane;
     } else {
-      pz = pz < 0 ? pz + a.n0 : (pz >= a.n0 ? pz - a.n0 : pz);
-      src = a.u + ((int64_t)(k * a.n0 + pz) * plane);
+      const bool halo = pz < 0 || pz >= a.n0;
+      const double* s8 = pz < 0 ? a.halo_lo : (pz >= a.n0 ? a.halo_hi : a.u + (int64_t)pz * plane);
+      s8 += (int64_t)k * (halo ? a.halo_cs : (int64_t)plane * a.n0);
+      src = reinterpret_cast<const unsigned char*>(s8);
     }
-    fft::bulk_g2s(reinterpret_cast<double*>(slot) + (r * C + k) * nx, src + yr * nx, row_bytes, bar);
-  } else if (j) {
-    int zp = zb * KZ - 2 + j;  // element plane
-    const uint8_t* ph;
-    if (a.dist && zp < 0) ph = a.ph_lo;
-    else {
-      zp = zp < 0 ? zp + a.n0 : zp;
-      ph = a.phase + (int64_t)zp * plane;
-    }
-    fft::bulk_g2s(slot + 2 * C * row_bytes, ph + y * nx, nx, bar);
+    src += (int64_t)yr * nx * (isph ? 1 : 8);
+  } else {
+    pz = pz < 0 ? pz + a.n0 : (pz >= a.n0 ? pz - a.n0 : pz);
+    const int64_t off = (int64_t)((isph ? 0 : k * a.n0) + pz) * plane + yr * nx;  // elements
+    src = isph ? a.phase + off : reinterpret_cast<const unsigned char*>(a.u + off);
   }
+  const uint32_t dst_off = isph ? 2 * C * row_bytes : (uint32_t)(r * C + k) * row_bytes;
+  if (!isph || j) fft::bulk_g2s(slot + dst_off, src, isph ? (uint32_t)nx : row_bytes, bar);
 }
 
 template <int C, bool ISO, int KZ, bool FE, int NXT, bool QT = false, bool MATS = true>
