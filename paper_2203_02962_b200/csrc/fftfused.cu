@@ -568,6 +568,9 @@ template <int N0, int C>
 #ifndef HB_PENCIL_INLAYOUT
 #define HB_PENCIL_INLAYOUT 1
 #endif
+#ifndef HB_PENCIL_LATEREFILL
+#define HB_PENCIL_LATEREFILL 1
+#endif
 // HB_PENCIL_HALVES (in-layout, 256-point elastic pencils): the solve couples
 // only the three components of a column, and columns {0,1} / {2,3} of a tile
 // live in warps {0,2,4} / {1,3,5}; each half synchronises its transform ->
@@ -649,6 +652,7 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
   }
   double rz = 0.0;
   int it = 0;
+  int pend_tile = -1, pend_st = 0;
   constexpr bool INL = HB_PENCIL_INLAYOUT;
   if (INL) __syncthreads();  // tables ready before the first (barrier-free) transform
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -708,6 +712,14 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
       for (int n2 = 0; n2 < 16; ++n2) pb[t + TPF * n2] = v[n2];
     if (HALVES) half_sync();
     else __syncthreads();
+    if (HB_PENCIL_LATEREFILL && tid == 0 && pend_tile >= 0) {
+      // the previous tile's stage: its stores were issued a forward transform
+      // ago, so this wait returns at once (at the tile end warp 0 sat in it
+      // while the others waited for it at the next barrier)
+      fft::bulk_wait_read();
+      issue(pend_tile, pend_st);
+      pend_tile = -1;
+    }
     // the solve: every thread of the block (HALVES: of the half) takes
     // frequencies of the tile's (the half's) columns, all C components each
     const int se0 = HALVES ? hr : tid, sen = HALVES ? 2 * N0 : N0 * BK, sed = HALVES ? NT / 2 : NT;
@@ -792,8 +804,13 @@ __global__ void __launch_bounds__(C * pencil_bk<C>() * (N0 / 16), HB_PENCIL_MINB
         fft::bulk_commit();
       }
       if (tile + 2 * (int)gridDim.x < ntiles) {
-        fft::bulk_wait_read();  // the stores have read the stage
-        issue(tile + 2 * gridDim.x, st);
+        if (HB_PENCIL_LATEREFILL) {
+          pend_tile = tile + 2 * gridDim.x;  // refilled after the next tile's first barrier
+          pend_st = st;
+        } else {
+          fft::bulk_wait_read();  // the stores have read the stage
+          issue(tile + 2 * gridDim.x, st);
+        }
       }
     }
     // no block barrier here: the other warps go on to the next tile (other
